@@ -1,0 +1,158 @@
+/* =====================================================================================================
+ * turboreg.h — C ABI of the B200-native TurboReg hot path (arXiv 2507.01439).
+ *
+ * The library computes, for each registration pair (a set of N putative correspondences
+ * m_i = (x_i, y_i)), the hot path of TurboReg (Fig. 2 caption):
+ *
+ *   (a2) compatibility graph C at the stringent τ (Eq. 1, Def. 1) as bit rows,
+ *        optionally a second plane C(τ_base) (SURVEY §8(c) reading c3);
+ *   (a3) SC^2 weights Ĝ = C ⊙ (C·C) (Eq. 2) and the O2Graph view Õ (Def. 2);
+ *   (a4) pivots: the K1 highest-weighted O2 edges (Eq. 4, Alg. 1 L4 P:261);
+ *   (a5) Pivot-Guided Search: per pivot, the top-K2 TurboCliques by S^(ij)(z) (Eqs. 5-7 P:202-220,
+ *        Alg. 1);
+ *   (a6) a Kabsch rigid fit per TurboClique;
+ *   (a7) the inlier number g(T) of every hypothesis against all N correspondences;
+ *   (a8) T* = argmax g (Eq. 9).
+ *
+ * Conventions: indices 0-based; y ≈ R·x + t; R row-major; float32 inputs.
+ * Every tie is broken deterministically: pivots (w desc, i asc, j asc); TurboCliques per pivot
+ * (S desc, z asc); the final argmax (g desc, S desc, (i,j,z) asc).
+ *
+ * All kernels are hand-written CUDA for sm_100a; there is no CPU fallback.  Functions return a
+ * turboreg_status; argument and validation failures return before any launch and write nothing.
+ * ===================================================================================================*/
+#ifndef TURBOREG_H
+#define TURBOREG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct turboreg_ctx turboreg_ctx; /* opaque; owns all device workspace and one CUDA stream */
+
+typedef enum {
+    TURBOREG_OK = 0,
+    TURBOREG_ERR_INVALID_ARGUMENT = 1, /* NULL pointer; tau <= 0; k1 < 1; k2 < 1; inlier_threshold <= 0;
+                                          tau_base not 0 and < tau; unknown graph_mode or flags;
+                                          batch < 1 or > max_batch; max_n outside [3, 32768]        */
+    TURBOREG_ERR_TOO_FEW_POINTS = 2,   /* N < 3: no 3-clique exists          — per pair */
+    TURBOREG_ERR_TOO_MANY_POINTS = 3,  /* N > max_n fixed at create                         — per pair */
+    TURBOREG_ERR_NONFINITE_INPUT = 4,  /* a NaN/Inf coordinate                       — per pair */
+    TURBOREG_ERR_NO_HYPOTHESIS = 5,    /* no pivot, no clique, or every clique degenerate;
+                                          R, t are all zeros — never a fabricated transform  — per pair */
+    TURBOREG_ERR_CUDA = 6,             /* a CUDA runtime error (whole call)                              */
+    TURBOREG_ERR_OUT_OF_MEMORY = 7     /* workspace allocation failed at create/set_params (whole call) */
+} turboreg_status;
+
+/* turboreg_params.flags */
+#define TURBOREG_F_STAGE_TIMING 0x1u  /* fill turboreg_result.stage_ms (CUDA events; adds ~12 events)  */
+#define TURBOREG_F_KERNEL_TIMING 0x2u /* accumulate per-kernel CUDA-event times, see turboreg_profile_* */
+
+typedef struct {
+    float tau;              /* τ of Eq. 1, metres, > 0: the stringent TurboClique threshold (Def. 1); drives
+                               SC^2, O2, pivots and cliques                                              */
+    float tau_base;         /* optional second compatibility plane C(τ_base), τ_base >= τ; 0 = not built  */
+    int32_t k1;             /* K1 pivots (Eq. 4); paper: 1000/2000 indoor, 250/500 outdoor     */
+    int32_t k2;             /* K2 TurboCliques per pivot (Eq. 7); paper: 2                       */
+    float inlier_threshold; /* residual bound of g(·), metres, > 0 (paper silent; reading r12)          */
+    int32_t graph_mode;     /* 0 = O2Graph (Def. 2, the paper's method); 1 = undirected SC^2 graph
+                               (Table 5 row 10) with duplicate cliques removed (reading r9)       */
+    uint32_t flags;         /* TURBOREG_F_*                                                               */
+} turboreg_params;
+
+typedef struct {
+    float R[9];                   /* T* rotation, row-major; zeros unless status == TURBOREG_OK        */
+    float t[3];                   /* T* translation                                                     */
+    int32_t inlier_count;         /* g(T*), exact integer                                        */
+    int32_t clique[3];            /* the winning TurboClique, i < j < z; -1 when none                   */
+    int32_t clique_weight;        /* S^(ij)(z) of the winner (Eq. 6)                                     */
+    int32_t num_pivots;           /* |P| = min(K1, #edges with Ĝ > 0)                                    */
+    int32_t num_cliques;          /* |C| <= K1*K2 (no padding, reading r7)                               */
+    int32_t hypotheses_evaluated; /* num_cliques minus degenerate cliques                        */
+    int32_t status;               /* turboreg_status of this pair                                        */
+    float stage_ms[3];            /* graph / PGS / model estimation (App. F.3 naming); 0 unless
+                                     TURBOREG_F_STAGE_TIMING (per call, not per pair)                   */
+    int64_t num_edges;            /* undirected edges of C(τ)                                            */
+} turboreg_result;
+
+/* Create a context on CUDA device `device` able to register up to `max_batch` pairs of up to `max_n`
+ * correspondences per call.  All device workspace is allocated here (no allocation on the register
+ * path); its size grows as max_batch · max_n² / 2 · 2 bytes (SC^2 weights) + max_batch · max_n² / 8.
+ * On success *out receives the context (caller owns it; release with turboreg_destroy). */
+turboreg_status turboreg_create(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
+                                turboreg_ctx** out);
+
+/* Replace the parameters; reallocates the pivot/clique workspace if K1·K2 grows. */
+turboreg_status turboreg_set_params(turboreg_ctx* ctx, const turboreg_params* params);
+
+/* Register one pair.  src_xyz, dst_xyz: N×3 float32 row-major (x_i and y_i), HOST or DEVICE pointers
+ * (detected).  Blocking: on return *out (host) holds the result.  Per-pair failures (2/3/4/5) are
+ * returned as the function value AND in out->status. */
+turboreg_status turboreg_register(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n,
+                                  turboreg_result* out);
+
+/* Register `batch` independent pairs in one pass.  Pair p uses points [offsets[p], offsets[p] + n[p]) of
+ * src_xyz / dst_xyz (N×3 float32, host or device).  offsets and n are HOST arrays.  out: `batch`
+ * results, HOST or DEVICE pointer.  stream: a cudaStream_t (NULL = the context's own stream).
+ * With a host `out` the call blocks until the results are in `out`; with a device `out` and device
+ * inputs it is fully asynchronous on `stream`.  Per-pair failures go into out[p].status and the call
+ * returns TURBOREG_OK; CUDA errors are returned for the whole call. */
+turboreg_status turboreg_register_batch(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz,
+                                        const int64_t* offsets, const int32_t* n, int32_t batch,
+                                        turboreg_result* out, void* stream);
+
+/* Release the context and all its device memory.  NULL is ignored. */
+void turboreg_destroy(turboreg_ctx* ctx);
+
+/* Static, human-readable name of a status. */
+const char* turboreg_status_string(turboreg_status s);
+
+/* ---------------------------------------------------------------------------------- test / profiling */
+/* Intermediates of pair `pair` of the LAST register call (kept in the workspace until the next call),
+ * copied to host buffer dst (capacity `bytes`).  *needed (may be NULL) receives the byte size.  `what`:
+ *   TURBOREG_I_BITS      uint32 [n][W]  rows of C(τ), W = words per row (*needed / (4n))
+ *   TURBOREG_I_BITS_BASE uint32 [n][W]  rows of C(τ_base) (only if tau_base > 0)
+ *   TURBOREG_I_SC2       int32  [n][n]  Ĝ expanded to a dense symmetric matrix
+ *   TURBOREG_I_PIVOTS    int32  [P][3]  (i, j, w) in (i, j) lexicographic order
+ *   TURBOREG_I_CLIQUES   int32  [K1*K2][4] (i, j, z, S) per slot p*K2 + r; empty slots are (-1,-1,-1,0)
+ *   TURBOREG_I_HYPS      float  [K1*K2][16]: R[9], t[3], count (int32 bits), flag (int32 bits:
+ *                        0 valid, 1 degenerate, 2 empty slot), S (int32 bits), 0
+ *   TURBOREG_I_STATE     int64  [16] per-pair scalars: n, W, edges, positive edges, alpha, c_gt, need,
+ *                        num_pivots, nonfinite, ...                                                   */
+#define TURBOREG_I_BITS 1
+#define TURBOREG_I_BITS_BASE 2
+#define TURBOREG_I_SC2 3
+#define TURBOREG_I_PIVOTS 4
+#define TURBOREG_I_CLIQUES 5
+#define TURBOREG_I_HYPS 6
+#define TURBOREG_I_STATE 7
+turboreg_status turboreg_get_intermediates(turboreg_ctx* ctx, int32_t pair, int32_t what, void* dst, size_t bytes,
+                                           size_t* needed);
+
+/* Run steps a3-a5 (SC^2, pivots, PGS) on a caller-supplied adjacency (HOST uint32 bit rows, row r at
+ * bits + r*stride_words, bit c of word c/32 = C_rc; must be symmetric with zero diagonal) for one pair of
+ * n nodes, using the context's K1, K2, graph_mode.  Results are read back with
+ * turboreg_get_intermediates(pair 0, TURBOREG_I_SC2 / _PIVOTS / _CLIQUES). */
+turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* ctx, const uint32_t* bits, int32_t n, int32_t stride_words);
+
+/* Per-kernel CUDA-event timing over a region (requires TURBOREG_F_KERNEL_TIMING in params.flags).
+ * profile_begin resets the accumulators; profile_end synchronises the last call's events and writes,
+ * for each of the library's kernels k < cap: names[k] (static string), ms[k] (summed duration) and
+ * launches[k]; returns the number of kernels in *count. */
+turboreg_status turboreg_profile_begin(turboreg_ctx* ctx);
+turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, float* ms, int64_t* launches,
+                                     int32_t cap, int32_t* count);
+
+/* Number of kernels this context has launched since creation (all calls). */
+int64_t turboreg_launch_count(const turboreg_ctx* ctx);
+
+/* Bytes of device workspace owned by the context. */
+size_t turboreg_workspace_bytes(const turboreg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TURBOREG_H */

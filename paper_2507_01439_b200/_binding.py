@@ -1,0 +1,308 @@
+"""ctypes binding of include/turboreg.h (same names; argument marshalling only).
+
+Inputs may be numpy arrays (host) or CUDA torch tensors (device pointers + the current torch stream).
+Every step of the path runs inside ``libturboreg.so``; this module never computes any part of it.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libturboreg.so")
+
+
+class TurboRegError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = int(status)
+        super().__init__(f"turboreg: {what}: {Status(self.status).name} ({self.status})")
+
+
+class Status(enum.IntEnum):
+    OK = 0
+    INVALID_ARGUMENT = 1
+    TOO_FEW_POINTS = 2
+    TOO_MANY_POINTS = 3
+    NONFINITE_INPUT = 4
+    NO_HYPOTHESIS = 5
+    CUDA = 6
+    OUT_OF_MEMORY = 7
+
+
+F_STAGE_TIMING = 0x1
+F_KERNEL_TIMING = 0x2
+
+I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE = 1, 2, 3, 4, 5, 6, 7
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("tau", ctypes.c_float),
+        ("tau_base", ctypes.c_float),
+        ("k1", ctypes.c_int32),
+        ("k2", ctypes.c_int32),
+        ("inlier_threshold", ctypes.c_float),
+        ("graph_mode", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [
+        ("R", ctypes.c_float * 9),
+        ("t", ctypes.c_float * 3),
+        ("inlier_count", ctypes.c_int32),
+        ("clique", ctypes.c_int32 * 3),
+        ("clique_weight", ctypes.c_int32),
+        ("num_pivots", ctypes.c_int32),
+        ("num_cliques", ctypes.c_int32),
+        ("hypotheses_evaluated", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("stage_ms", ctypes.c_float * 3),
+        ("num_edges", ctypes.c_int64),
+    ]
+
+
+RESULT_DTYPE = np.dtype(
+    {
+        "names": ["R", "t", "inlier_count", "clique", "clique_weight", "num_pivots", "num_cliques",
+                  "hypotheses_evaluated", "status", "stage_ms", "num_edges"],
+        "formats": [("<f4", (9,)), ("<f4", (3,)), "<i4", ("<i4", (3,)), "<i4", "<i4", "<i4", "<i4", "<i4",
+                    ("<f4", (3,)), "<i8"],
+        "offsets": [0, 36, 48, 52, 64, 68, 72, 76, 80, 84, 96],
+        "itemsize": 104,
+    }
+)
+assert ctypes.sizeof(Result) == RESULT_DTYPE.itemsize == 104
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def library():
+    """Load libturboreg.so; raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    lib.turboreg_create.argtypes = [ctypes.POINTER(Params), ctypes.c_int, i32, i32, ctypes.POINTER(P)]
+    lib.turboreg_set_params.argtypes = [P, ctypes.POINTER(Params)]
+    lib.turboreg_register.argtypes = [P, P, P, i32, ctypes.POINTER(Result)]
+    lib.turboreg_register_batch.argtypes = [P, P, P, P, P, i32, P, P]
+    lib.turboreg_destroy.argtypes = [P]
+    lib.turboreg_destroy.restype = None
+    lib.turboreg_status_string.argtypes = [ctypes.c_int]
+    lib.turboreg_status_string.restype = ctypes.c_char_p
+    lib.turboreg_get_intermediates.argtypes = [P, i32, i32, P, u64, ctypes.POINTER(u64)]
+    lib.turboreg_pgs_from_adjacency.argtypes = [P, P, i32, i32]
+    lib.turboreg_profile_begin.argtypes = [P]
+    lib.turboreg_profile_end.argtypes = [P, P, P, P, i32, ctypes.POINTER(i32)]
+    lib.turboreg_launch_count.argtypes = [P]
+    lib.turboreg_launch_count.restype = i64
+    lib.turboreg_workspace_bytes.argtypes = [P]
+    lib.turboreg_workspace_bytes.restype = u64
+    for name in ("turboreg_create", "turboreg_set_params", "turboreg_register", "turboreg_register_batch",
+                 "turboreg_get_intermediates", "turboreg_pgs_from_adjacency", "turboreg_profile_begin",
+                 "turboreg_profile_end"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(st, what):
+    if st != 0:
+        raise TurboRegError(st, what)
+
+
+def _is_torch_cuda(x):
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _ptr(x, dtype=None):
+    """(pointer, keepalive) for a numpy array or a torch tensor (host or CUDA)."""
+    if type(x).__module__.startswith("torch"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if dtype is not None and str(x.dtype) != "torch." + np.dtype(dtype).name:
+            raise TypeError(f"expected {np.dtype(dtype).name} tensor, got {x.dtype}")
+        return ctypes.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data_as(ctypes.c_void_p), a
+
+
+class TurboReg:
+    """One context (device workspace + stream) of the C ABI.
+
+    ``TurboReg(tau, k1, k2, inlier_threshold, max_n=..., max_batch=...)`` then ``register(src, dst)`` or
+    ``register_batch(src, dst, offsets, n)``.  Parameter meanings: include/turboreg.h.
+    """
+
+    def __init__(self, tau, k1=1000, k2=2, inlier_threshold=0.1, *, tau_base=0.0, graph_mode=0,
+                 max_n=5000, max_batch=1, device=0, stage_timing=False, kernel_timing=False):
+        self._lib = library()
+        flags = (F_STAGE_TIMING if stage_timing else 0) | (F_KERNEL_TIMING if kernel_timing else 0)
+        self.params = Params(float(tau), float(tau_base), int(k1), int(k2), float(inlier_threshold),
+                             int(graph_mode), flags)
+        h = ctypes.c_void_p()
+        _check(self._lib.turboreg_create(ctypes.byref(self.params), int(device), int(max_n), int(max_batch),
+                                         ctypes.byref(h)), "create")
+        self._h = h
+        self.max_n, self.max_batch, self.device = int(max_n), int(max_batch), int(device)
+
+    # ------------------------------------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.turboreg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_params(self, **kw):
+        for k, v in kw.items():
+            setattr(self.params, k, v)
+        _check(self._lib.turboreg_set_params(self._h, ctypes.byref(self.params)), "set_params")
+
+    # ------------------------------------------------------------------------------------------ compute
+    def register(self, src, dst):
+        """One pair (host numpy or device torch N×3 float32).  Returns a dict; status in ['status']."""
+        ps, ks = _ptr(src, np.float32)
+        pd, kd = _ptr(dst, np.float32)
+        n = int(src.shape[0])
+        res = Result()
+        st = self._lib.turboreg_register(self._h, ps, pd, n, ctypes.byref(res))
+        if st not in (0, 2, 3, 4, 5):
+            raise TurboRegError(st, "register")
+        return result_to_dict(res)
+
+    def register_batch(self, src, dst, offsets, n, out=None, stream=None):
+        """`batch` pairs; src/dst are (Σn)×3 float32 (host numpy or CUDA torch), offsets/n host arrays.
+
+        ``out``: None → returns a numpy structured array (RESULT_DTYPE, blocking); or a CUDA torch uint8
+        tensor of ≥ batch*104 bytes → asynchronous on ``stream`` (default: torch's current stream)."""
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = np.ascontiguousarray(n, dtype=np.int32)
+        batch = int(n.shape[0])
+        ps, ks = _ptr(src, np.float32)
+        pd, kd = _ptr(dst, np.float32)
+        if stream is None and (_is_torch_cuda(src) or (out is not None and _is_torch_cuda(out))):
+            import torch
+
+            stream = torch.cuda.current_stream().cuda_stream
+        sp = ctypes.c_void_p(int(stream)) if stream else None
+        if out is None:
+            host = np.zeros(batch, dtype=RESULT_DTYPE)
+            st = self._lib.turboreg_register_batch(self._h, ps, pd, offsets.ctypes.data_as(ctypes.c_void_p),
+                                                   n.ctypes.data_as(ctypes.c_void_p), batch,
+                                                   host.ctypes.data_as(ctypes.c_void_p), sp)
+            _check(st, "register_batch")
+            return host
+        po, ko = _ptr(out)
+        st = self._lib.turboreg_register_batch(self._h, ps, pd, offsets.ctypes.data_as(ctypes.c_void_p),
+                                               n.ctypes.data_as(ctypes.c_void_p), batch, po, sp)
+        _check(st, "register_batch")
+        return out
+
+    # ------------------------------------------------------------------------------------------ test views
+    def intermediate(self, pair, what):
+        need = ctypes.c_size_t()
+        _check(self._lib.turboreg_get_intermediates(self._h, int(pair), int(what), None, 0, ctypes.byref(need)),
+               "get_intermediates")
+        buf = np.zeros(max(need.value, 1), np.uint8)
+        _check(self._lib.turboreg_get_intermediates(self._h, int(pair), int(what),
+                                                    buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes, None),
+               "get_intermediates")
+        buf = buf[: need.value]
+        if what in (I_BITS, I_BITS_BASE):
+            return buf.view(np.uint32)
+        if what == I_SC2:
+            v = buf.view(np.int32)
+            n = int(round(np.sqrt(v.size)))
+            return v.reshape(n, n)
+        if what == I_PIVOTS:
+            return buf.view(np.int32).reshape(-1, 3)
+        if what == I_CLIQUES:
+            return buf.view(np.int32).reshape(-1, 4)
+        if what == I_HYPS:
+            return buf.view(np.float32).reshape(-1, 16)
+        if what == I_STATE:
+            s = buf.view(np.int64)
+            keys = ["n", "W", "edges", "epos", "alpha", "c_gt", "need", "npiv", "nonfinite", "b1", "above",
+                    "edges_base"]
+            return {k: int(s[i]) for i, k in enumerate(keys)}
+        return buf
+
+    def bits(self, pair=0, base=False):
+        """C(τ) (or C(τ_base)) of the last call as a dense uint8 [n, n] matrix."""
+        st = self.intermediate(pair, I_STATE)
+        n, W = st["n"], st["W"]
+        words = self.intermediate(pair, I_BITS_BASE if base else I_BITS).reshape(n, W)
+        return np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, :n]
+
+    def pgs_from_adjacency(self, C):
+        C = np.ascontiguousarray(C, dtype=np.uint8)
+        n = C.shape[0]
+        W = (n + 31) // 32
+        padded = np.zeros((n, W * 32), np.uint8)
+        padded[:, :n] = C
+        words = np.packbits(padded, axis=1, bitorder="little").view(np.uint32)
+        words = np.ascontiguousarray(words)
+        _check(self._lib.turboreg_pgs_from_adjacency(self._h, words.ctypes.data_as(ctypes.c_void_p), n, W),
+               "pgs_from_adjacency")
+
+    # ------------------------------------------------------------------------------------------ profiling
+    def profile_begin(self):
+        _check(self._lib.turboreg_profile_begin(self._h), "profile_begin")
+
+    def profile_end(self):
+        cap = 32
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_float * cap)()
+        launches = (ctypes.c_int64 * cap)()
+        cnt = ctypes.c_int32()
+        _check(self._lib.turboreg_profile_end(self._h, names, ms, launches, cap, ctypes.byref(cnt)), "profile_end")
+        return {names[k].decode(): (float(ms[k]), int(launches[k])) for k in range(cnt.value)}
+
+    @property
+    def launch_count(self):
+        return int(self._lib.turboreg_launch_count(self._h))
+
+    @property
+    def workspace_bytes(self):
+        return int(self._lib.turboreg_workspace_bytes(self._h))
+
+
+def result_to_dict(r):
+    if isinstance(r, np.void) or (isinstance(r, np.ndarray) and r.dtype == RESULT_DTYPE):
+        return {k: (r[k].copy() if np.ndim(r[k]) else r[k].item()) for k in RESULT_DTYPE.names}
+    return {
+        "R": np.array(r.R, np.float32).reshape(3, 3),
+        "t": np.array(r.t, np.float32),
+        "inlier_count": r.inlier_count,
+        "clique": tuple(r.clique),
+        "clique_weight": r.clique_weight,
+        "num_pivots": r.num_pivots,
+        "num_cliques": r.num_cliques,
+        "hypotheses_evaluated": r.hypotheses_evaluated,
+        "status": r.status,
+        "stage_ms": tuple(r.stage_ms),
+        "num_edges": r.num_edges,
+    }

@@ -1,0 +1,957 @@
+// =====================================================================================================
+// TurboReg hot-path kernels for sm_100a (B200).  Included once, by turboreg_runtime.cu.
+//
+// Every kernel takes a batch of independent registration pairs (grid.y / grid.z = pair) and reads its
+// pair's geometry from a PairDesc.  Data layout per pair:
+//   src4/dst4  float4[n]          correspondences (x, y, z, 0)
+//   bits       uint32[n][W]       rows of C(τ); bit c of word c/32 = C_rc; W = ceil(n/32) rounded up to 4
+//   edges      uint32[n(n-1)/2]   row i's upper edges (j > i) in increasing j at tri_off(i):
+//                                 (j << 16) | Ĝ_ij   ("rank-indexed" O2 weights, Def. 2)
+//   deg        int32[n]           upper degree of row i
+//   piv        int4[K1]           (i, j, Ĝ_ij, 0) in lexicographic order
+//   cliq       int4[K1*K2]        (i, j, z, S) per slot pivot*K2 + r; empty (-1,-1,-1,0)
+//   hyp        float[K1*K2][16]   R[9], t[3], count, flag, S, 0
+// Float32 arithmetic that decides an integer (Eq. 1 edges, inlier tests) uses explicit _rn intrinsics
+// in exactly the oracle's expression tree (readings r1, r13) so no contraction can change a bit.
+// =====================================================================================================
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace trk {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct PairDesc {
+    const float* src;     // N×3 float32 (device), already offset to this pair
+    const float* dst;
+    int32_t n;            // 0 ⇒ pair skipped (host_status says why)
+    int32_t W;            // words per bit row
+    int32_t host_status;  // turboreg_status decided on the host (0, 2 or 3)
+    int32_t pad;
+};
+
+struct PairState {
+    int32_t nonfinite;  // set by k_ingest
+    int32_t edges;      // E, undirected edges of C(τ)
+    int32_t epos;       // E+, edges with Ĝ > 0
+    int32_t b1;         // radix-select high digit of α
+    int32_t above;      // #weights with high digit > b1
+    int32_t alpha;      // α_K1 (Eq. 4)
+    int32_t c_gt;       // #weights > α
+    int32_t need;       // K1 - c_gt: how many weight-α edges are taken (lexicographically first)
+    int32_t npiv;       // |P|
+    int32_t edges_base; // edges of C(τ_base)
+    int32_t pad[6];
+    int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
+    int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
+};
+
+struct WS {
+    const PairDesc* desc;
+    PairState* st;
+    float4* src4;
+    float4* dst4;
+    int64_t pts_stride;
+    uint32_t* bits;
+    uint32_t* bits_base;
+    int64_t bits_stride;
+    int32_t* deg;
+    int32_t* row_gt;
+    int32_t* row_eq;
+    int32_t* row_take;
+    int32_t* row_off;
+    int64_t row_stride;
+    uint32_t* edges;
+    int64_t edges_stride;
+    int4* piv;
+    int64_t piv_stride;  // K1
+    int4* cliq;
+    float* hyp;
+    int64_t cl_stride;  // K1*K2
+    void* res;          // turboreg_result[batch]
+    float tau, tau_base, thr;
+    int32_t k1, k2, mode;
+};
+
+__device__ __forceinline__ int64_t tri_off(int64_t i, int64_t n) { return i * n - (i * (i + 1)) / 2; }
+
+// Row i restricted to its upper part U_i = {c > i} (the O2 out-neighbourhood, Def. 2).
+__device__ __forceinline__ uint32_t upper_mask(uint32_t v, int w, int i) {
+    int lo = w * 32;
+    if (lo + 31 <= i) return 0u;
+    if (lo > i) return v;
+    int s = i - lo;  // clear bits 0..s
+    return v & ~((2u << s) - 1u);
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long u = __shfl_xor_sync(FULL, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long u = __shfl_xor_sync(FULL, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// ------------------------------------------------------------------------------------------ a1 ingest
+// Repack the caller's N×3 float32 rows into float4 (x, y, z, 0) and flag non-finite input.
+__global__ void __launch_bounds__(256) k_ingest(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    bool bad = false;
+    if (k < d.n) {
+        float sx = d.src[3 * k], sy = d.src[3 * k + 1], sz = d.src[3 * k + 2];
+        float tx = d.dst[3 * k], ty = d.dst[3 * k + 1], tz = d.dst[3 * k + 2];
+        bad = !(isfinite(sx) && isfinite(sy) && isfinite(sz) && isfinite(tx) && isfinite(ty) && isfinite(tz));
+        ws.src4[p * ws.pts_stride + k] = make_float4(sx, sy, sz, 0.f);
+        ws.dst4[p * ws.pts_stride + k] = make_float4(tx, ty, tz, 0.f);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.st[p].nonfinite, 1);
+}
+
+// ------------------------------------------------------------------------------------------ a2 compat
+// Eq. 1 on 32×32 tiles of the upper block triangle.  One warp per tile (I ≤ J): lane l owns
+// column point J*32+l, the 32 row points I*32+r are broadcast by shuffles.  Each test is evaluated once;
+// the ballot over lanes is row word (I*32+r, J) and the lane's own bit accumulation is the mirrored
+// column word (J*32+l, I) — exact because IEEE subtraction is antisymmetric (x_i - x_j = -(x_j - x_i)).
+// Float32 tree = the oracle's: ((dx*dx + dy*dy) + dz*dz), sqrt.rn, |a - b| <= τ (readings r1, r2).
+__device__ __forceinline__ float f32_dist(float ax, float ay, float az, float bx, float by, float bz) {
+    float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
+    return __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)));
+}
+
+template <bool BASE>
+__global__ void __launch_bounds__(256) k_compat(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int T = (n + 31) >> 5;
+    const int64_t ntiles = (int64_t)T * (T + 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= ntiles) return;
+    // tile t → (I, J): tiles of block-row I are J = I..T-1; cum(I) = I*T - I(I-1)/2
+    const double tw = 2.0 * T + 1.0;
+    int I = (int)((tw - sqrt(tw * tw - 8.0 * (double)t)) * 0.5);
+    if (I < 0) I = 0;
+    if (I > T - 1) I = T - 1;
+    auto cum = [&](int64_t r) { return r * T - r * (r - 1) / 2; };
+    while (I + 1 <= T - 1 && cum(I + 1) <= t) ++I;
+    while (I > 0 && cum(I) > t) --I;
+    const int J = I + (int)(t - cum(I));
+
+    const float4* s4 = ws.src4 + p * ws.pts_stride;
+    const float4* d4 = ws.dst4 + p * ws.pts_stride;
+    const int c = J * 32 + lane;
+    const bool cv = c < n;
+    const float4 cs = cv ? s4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 cd = cv ? d4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int r0 = I * 32 + lane;
+    const bool rv = r0 < n;
+    const float4 rs = rv ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 rd = rv ? d4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float tau = ws.tau, taub = ws.tau_base;
+    const int rmax = min(32, n - I * 32);
+    uint32_t roww = 0, colw = 0, rowb = 0, colb = 0;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+        const float xs = __shfl_sync(FULL, rs.x, r), ys = __shfl_sync(FULL, rs.y, r), zs = __shfl_sync(FULL, rs.z, r);
+        const float xd = __shfl_sync(FULL, rd.x, r), yd = __shfl_sync(FULL, rd.y, r), zd = __shfl_sync(FULL, rd.z, r);
+        const float a = f32_dist(xs, ys, zs, cs.x, cs.y, cs.z);
+        const float b = f32_dist(xd, yd, zd, cd.x, cd.y, cd.z);
+        const float delta = fabsf(__fsub_rn(a, b));
+        const bool ok = cv && (r < rmax) && (I * 32 + r != c);
+        const bool e = ok && (delta <= tau);
+        const uint32_t bal = __ballot_sync(FULL, e);
+        if (lane == r) roww = bal;
+        colw |= (uint32_t)e << r;
+        if (BASE) {
+            const bool eb = ok && (delta <= taub);
+            const uint32_t balb = __ballot_sync(FULL, eb);
+            if (lane == r) rowb = balb;
+            colb |= (uint32_t)eb << r;
+        }
+    }
+    uint32_t* bits = ws.bits + p * ws.bits_stride;
+    if (rv) bits[(int64_t)r0 * W + J] = roww;
+    if (cv) bits[(int64_t)c * W + I] = colw;
+    if (I == J && rv)
+        for (int w = T; w < W; ++w) bits[(int64_t)r0 * W + w] = 0u;
+    if (BASE) {
+        uint32_t* bb = ws.bits_base + p * ws.bits_stride;
+        if (rv) bb[(int64_t)r0 * W + J] = rowb;
+        if (cv) bb[(int64_t)c * W + I] = colb;
+        if (I == J && rv)
+            for (int w = T; w < W; ++w) bb[(int64_t)r0 * W + w] = 0u;
+        // edge count of the τ_base plane (upper triangle only)
+        int cntb = (I == J) ? __popc(colb & ((lane == 0) ? 0u : (0xffffffffu >> (32 - lane)))) : __popc(colb);
+        cntb = __reduce_add_sync(FULL, (unsigned)cntb);
+        if (lane == 0 && cntb) atomicAdd(&ws.st[p].edges_base, cntb);
+    }
+}
+
+// ------------------------------------------------------------------------------------------ a3 SC^2
+// Eq. 2 for the O2 edges (i < j): Ĝ_ij = popcount(row_i AND row_j).  One warp per row i:
+// row_i lives in registers (lane-strided words), the warp walks U_i's set bits j in increasing order, G
+// edges at a time so G·WPL row_j loads are in flight, and reduces each partial with REDUX.  The result
+// (j << 16 | Ĝ_ij) goes to edges[tri_off(i) + rank]; positive weights feed a 256-bin histogram of
+// Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
+constexpr int SC2_WARPS = 8;
+constexpr int SC2_ROWS_PER_BLOCK = 64;
+
+template <int WPL>
+__global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws) {
+    constexpr int G = 4;
+    __shared__ uint32_t s_row[SC2_WARPS][32 * WPL];
+    __shared__ int s_hist[256];
+    __shared__ int s_edges;
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
+    if (threadIdx.x == 0) s_edges = 0;
+    __syncthreads();
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int row0 = blockIdx.x * SC2_ROWS_PER_BLOCK;
+    const int row1 = min(row0 + SC2_ROWS_PER_BLOCK, n);
+    int my_edges = 0;
+    for (int i = row0 + warp; i < row1; i += SC2_WARPS) {
+        const uint32_t* ri = bits + (int64_t)i * W;
+        uint32_t reg[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int w = lane + 32 * k;
+            const uint32_t v = (w < W) ? ri[w] : 0u;
+            reg[k] = v;
+            s_row[warp][w] = upper_mask(v, w, i);
+        }
+        __syncwarp();
+        const int64_t base = tri_off(i, n);
+        int rank = 0;
+        uint32_t myval = 0;
+        int w = (i + 1) >> 5;
+        uint32_t word = (w < W) ? s_row[warp][w] : 0u;
+        while (true) {
+            int js[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                while (word == 0u && w + 1 < W) word = s_row[warp][++w];
+                if (word) {
+                    js[g] = w * 32 + (__ffs(word) - 1);
+                    word &= word - 1u;
+                } else {
+                    js[g] = -1;
+                }
+            }
+            if (js[0] < 0) break;
+            uint32_t part[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                part[g] = 0u;
+                if (js[g] >= 0) {
+                    const uint32_t* rj = bits + (int64_t)js[g] * W;
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) {
+                        const int wk = lane + 32 * k;
+                        if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (js[g] < 0) break;
+                const uint32_t tot = __reduce_add_sync(FULL, part[g]);
+                if (lane == (rank & 31)) myval = ((uint32_t)js[g] << 16) | tot;
+                ++rank;
+                if ((rank & 31) == 0) {
+                    edges[base + rank - 32 + lane] = myval;
+                    const uint32_t wv = myval & 0xffffu;
+                    if (wv) atomicAdd(&s_hist[wv >> 7], 1);
+                }
+            }
+        }
+        const int rem = rank & 31;
+        if (rem && lane < rem) {
+            edges[base + (rank - rem) + lane] = myval;
+            const uint32_t wv = myval & 0xffffu;
+            if (wv) atomicAdd(&s_hist[wv >> 7], 1);
+        }
+        if (lane == 0) ws.deg[p * ws.row_stride + i] = rank;
+        my_edges += rank;
+        __syncwarp();
+    }
+    if (lane == 0 && my_edges) atomicAdd(&s_edges, my_edges);
+    __syncthreads();
+    PairState* st = ws.st + p;
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (s_hist[b]) atomicAdd(&st->hist_hi[b], s_hist[b]);
+    if (threadIdx.x == 0 && s_edges) atomicAdd(&st->edges, s_edges);
+}
+
+// ------------------------------------------------------------------------------------------ a4 pivots
+// Eq. 4: α_K1 = K1-th largest O2 weight; all edges > α plus the lexicographically first
+// K1 - #(> α) edges of weight α (readings r4, r5).  Found by a two-digit radix select over the
+// histograms, then an ordered (row-major = lexicographic) compaction.
+
+// Block-wide: hist[0..nb) (nb <= blockDim.x, blockDim.x a multiple of 32, <= 1024).  Finds the bin b with
+// suffix(b) >= K > suffix(b+1); if the total < K, b = lowest.  Returns (b, suffix(b+1)) to every thread.
+__device__ void block_suffix_select(const int* hist, int nb, int K, int lowest, int* out_b, int* out_above,
+                                    int* out_total) {
+    __shared__ int s_w[32];
+    __shared__ int s_res[3];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int bin = nb - 1 - t;  // reversed so an inclusive prefix is a suffix sum
+    const int v = (t < nb) ? hist[bin] : 0;
+    int incl = warp_incl_scan(v);
+    if (lane == 31) s_w[warp] = incl;
+    if (t == 0) { s_res[0] = lowest; s_res[1] = 0; }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        int x = lane < nw ? s_w[lane] : 0;
+        int xi = warp_incl_scan(x);
+        if (lane < nw) s_w[lane] = xi - x;  // exclusive warp offsets
+        if (lane == nw - 1) s_res[2] = xi;  // total
+    }
+    __syncthreads();
+    incl += s_w[warp];
+    const int excl = incl - v;  // = suffix(bin + 1)
+    if (t < nb && bin >= lowest && incl >= K && excl < K) { s_res[0] = bin; s_res[1] = excl; }
+    __syncthreads();
+    const int total = s_res[2];
+    if (total < K) {  // never crosses: take everything from `lowest` up
+        // suffix(lowest + 1) is needed; recompute from the scan
+        if (t < nb && bin == lowest) s_res[1] = excl;
+        __syncthreads();
+        if (t == 0) s_res[0] = lowest;
+        __syncthreads();
+    }
+    *out_b = s_res[0];
+    *out_above = s_res[1];
+    *out_total = total;
+    __syncthreads();
+}
+
+constexpr int SEL_WARPS = 8;
+constexpr int SEL_ROWS_PER_BLOCK = 64;
+
+__global__ void __launch_bounds__(256) k_hist_lo(WS ws) {
+    __shared__ int s_lo[128];
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    int b1, above, total;
+    block_suffix_select(st->hist_hi, 256, ws.k1, 0, &b1, &above, &total);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->b1 = b1; st->above = above; st->epos = total; }
+    for (int b = threadIdx.x; b < 128; b += blockDim.x) s_lo[b] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        const int dg = ws.deg[p * ws.row_stride + i];
+        const uint32_t* e = edges + tri_off(i, n);
+        for (int k = lane; k < dg; k += 32) {
+            const uint32_t w = e[k] & 0xffffu;
+            if (w && (int)(w >> 7) == b1) atomicAdd(&s_lo[w & 127u], 1);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 128; b += blockDim.x)
+        if (s_lo[b]) atomicAdd(&st->hist_lo[b], s_lo[b]);
+}
+
+// α, #(> α) and `need` from the two histograms (identical in every block).
+__device__ void pivot_threshold(WS& ws, PairState* st, int* alpha, int* c_gt, int* need) {
+    const int b1 = st->b1, above = st->above;
+    int l, above_l, tot_l;
+    const int lowest = (b1 == 0) ? 1 : 0;  // weight 0 is never a pivot
+    block_suffix_select(st->hist_lo, 128, ws.k1 - above, lowest, &l, &above_l, &tot_l);
+    *alpha = b1 * 128 + l;
+    *c_gt = above + above_l;
+    *need = ws.k1 - *c_gt;
+}
+
+__global__ void __launch_bounds__(256) k_select_count(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    int alpha, c_gt, need;
+    pivot_threshold(ws, st, &alpha, &c_gt, &need);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->alpha = alpha; st->c_gt = c_gt; st->need = need; }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        const int dg = ws.deg[p * ws.row_stride + i];
+        const uint32_t* e = edges + tri_off(i, n);
+        int gt = 0, eq = 0;
+        for (int k = lane; k < dg; k += 32) {
+            const int w = (int)(e[k] & 0xffffu);
+            gt += (w > alpha);
+            eq += (w == alpha);
+        }
+        gt = __reduce_add_sync(FULL, (unsigned)gt);
+        eq = __reduce_add_sync(FULL, (unsigned)eq);
+        if (lane == 0) {
+            ws.row_gt[p * ws.row_stride + i] = gt;
+            ws.row_eq[p * ws.row_stride + i] = eq;
+        }
+    }
+}
+
+// One block per pair: exclusive scans over rows → how many weight-α edges each row contributes
+// (lexicographic tie order) and each row's output offset.
+__global__ void __launch_bounds__(1024) k_select_scan(WS ws) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry[2];
+    const int p = blockIdx.x;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    const int need = st->need;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) { s_carry[0] = 0; s_carry[1] = 0; }
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int eq = (i < n) ? ws.row_eq[p * ws.row_stride + i] : 0;
+        const int gt = (i < n) ? ws.row_gt[p * ws.row_stride + i] : 0;
+        // scan eq
+        int x = warp_incl_scan(eq);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int ex_eq = s_carry[0] + x - eq + s_w[warp];
+        int take = need - ex_eq;
+        take = take < 0 ? 0 : (take > eq ? eq : take);
+        const int cnt = gt + take;
+        __syncthreads();
+        // scan cnt
+        int c = warp_incl_scan(cnt);
+        __shared__ int s_w2[32];
+        if (lane == 31) s_w2[warp] = c;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w2[lane];
+            int yi = warp_incl_scan(y);
+            s_w2[lane] = yi - y;
+        }
+        __syncthreads();
+        const int off = s_carry[1] + c - cnt + s_w2[warp];
+        if (i < n) {
+            ws.row_take[p * ws.row_stride + i] = take;
+            ws.row_off[p * ws.row_stride + i] = off;
+        }
+        __syncthreads();
+        if (t == 1023) {
+            s_carry[0] = ex_eq + eq;
+            s_carry[1] = off + cnt;
+        }
+        __syncthreads();
+    }
+    if (t == 0) st->npiv = s_carry[1];
+}
+
+__global__ void __launch_bounds__(256) k_select_emit(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const PairState* st = ws.st + p;
+    const int alpha = st->alpha;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    int4* piv = ws.piv + p * ws.piv_stride;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        const int64_t ro = p * ws.row_stride + i;
+        const int take = ws.row_take[ro];
+        if (ws.row_gt[ro] + take == 0) continue;
+        const int dg = ws.deg[ro];
+        int pos = ws.row_off[ro];
+        int eqseen = 0;
+        const uint32_t* e = edges + tri_off(i, n);
+        for (int k0 = 0; k0 < dg; k0 += 32) {
+            const int k = k0 + lane;
+            const uint32_t v = (k < dg) ? e[k] : 0u;
+            const int w = (int)(v & 0xffffu);
+            const bool iseq = (k < dg) && (w == alpha);
+            const unsigned eqb = __ballot_sync(FULL, iseq);
+            const bool sel = (k < dg) && (w > alpha || (iseq && eqseen + __popc(eqb & lt) < take));
+            const unsigned sb = __ballot_sync(FULL, sel);
+            if (sel) piv[pos + __popc(sb & lt)] = make_int4(i, (int)(v >> 16), w, 0);
+            pos += __popc(sb);
+            eqseen += __popc(eqb);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ a5 PGS
+// Alg. 1 L5-13, Eqs. 5-7.  One warp per pivot (i, j): the O2 common neighbours are
+// M = U_i ∧ U_j (z > j > i; for a pivot C_ij = 1, so Ĝ_iz > 0 ⇔ C_iz, reading r10), scanned word-parallel;
+// Ĝ_iz and Ĝ_jz are gathered from the rank-indexed edge lists (rank = prefix popcount of U_i / U_j below
+// z, from a warp scan).  S = Ĝ_ij + Ĝ_iz + Ĝ_jz; the top-K2 by (S desc, z asc) are kept (readings r7, r8):
+// per-lane register lists (K2 <= KL) merged by K2 warp argmax rounds, or K2 threshold rounds otherwise.
+constexpr int PGS_WARPS = 8;
+constexpr int PGS_KL = 8;
+
+template <typename F>
+__device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
+                                                    const uint32_t* ei, const uint32_t* ej, int wij, F&& f) {
+    const int lane = threadIdx.x & 31;
+    int carry_i = 0, carry_j = 0;
+    const int nchunks = (W + 31) >> 5;
+    for (int c = (i + 1) >> 10; c < nchunks; ++c) {  // chunks holding no bit > i contribute nothing
+        const int w = c * 32 + lane;
+        const uint32_t ui = (w < W) ? upper_mask(ri[w], w, i) : 0u;
+        const uint32_t uj = (w < W) ? upper_mask(rj[w], w, j) : 0u;
+        const int pi = __popc(ui), pj = __popc(uj);
+        const int si = warp_incl_scan(pi), sj = warp_incl_scan(pj);
+        const int exi = carry_i + si - pi, exj = carry_j + sj - pj;
+        carry_i += __shfl_sync(FULL, si, 31);
+        carry_j += __shfl_sync(FULL, sj, 31);
+        uint32_t m = ui & uj;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t below = (1u << b) - 1u;
+            const int rk_i = exi + __popc(ui & below);
+            const int rk_j = exj + __popc(uj & below);
+            const int wiz = (int)(__ldg(ei + rk_i) & 0xffffu);
+            const int wjz = (int)(__ldg(ej + rk_j) & 0xffffu);
+            const int z = w * 32 + b;
+            const int S = wij + wiz + wjz;
+            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
+    const int q = blockIdx.y;
+    const PairDesc d = ws.desc[q];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pv = blockIdx.x * PGS_WARPS + warp;
+    const int K1 = ws.k1, K2 = ws.k2;
+    if (pv >= K1) return;
+    int4* out = ws.cliq + q * ws.cl_stride + (int64_t)pv * K2;
+    const int P = ws.st[q].npiv;
+    if (pv >= P) {
+        for (int r = lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
+        return;
+    }
+    const int4 pvt = ws.piv[q * ws.piv_stride + pv];
+    const int i = pvt.x, j = pvt.y, wij = pvt.z;
+    const uint32_t* bits = ws.bits + q * ws.bits_stride;
+    const uint32_t* ri = bits + (int64_t)i * W;
+    const uint32_t* rj = bits + (int64_t)j * W;
+    const uint32_t* edges = ws.edges + q * ws.edges_stride;
+    const uint32_t* ei = edges + tri_off(i, n);
+    const uint32_t* ej = edges + tri_off(j, n);
+    int emitted = 0;
+    if (K2 <= PGS_KL) {
+        unsigned long long top[PGS_KL];
+#pragma unroll
+        for (int r = 0; r < PGS_KL; ++r) top[r] = 0ull;
+        pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
+            if (key > top[PGS_KL - 1]) {  // sorted insertion, descending
+                unsigned long long k = key;
+#pragma unroll
+                for (int r = 0; r < PGS_KL; ++r) {
+                    if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
+                }
+            }
+        });
+        for (int r = 0; r < K2; ++r) {
+            const unsigned long long head = top[0];
+            const unsigned long long best = warp_max_u64(head);
+            if (best == 0ull) break;
+            if (head == best) {  // keys are unique (distinct z), exactly one lane pops
+#pragma unroll
+                for (int s = 0; s < PGS_KL - 1; ++s) top[s] = top[s + 1];
+                top[PGS_KL - 1] = 0ull;
+            }
+            if (lane == 0) {
+                const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
+                out[r] = make_int4(i, j, z, (int)(best >> 32));
+            }
+            ++emitted;
+        }
+    } else {
+        unsigned long long thr = ~0ull;
+        for (int r = 0; r < K2; ++r) {
+            unsigned long long mine = 0ull;
+            pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
+                if (key < thr && key > mine) mine = key;
+            });
+            const unsigned long long best = warp_max_u64(mine);
+            if (best == 0ull) break;
+            if (lane == 0) {
+                const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
+                out[r] = make_int4(i, j, z, (int)(best >> 32));
+            }
+            thr = best;
+            ++emitted;
+        }
+    }
+    for (int r = emitted + lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
+}
+
+// ------------------------------------------------------------------------------------------ a6 Kabsch
+// P:283.  One thread per TurboClique slot, FP64.  Degenerate predicate (reading r11) in the oracle's
+// exact expression tree; then a closed form of the least-squares fit: three points are coplanar, so H
+// has σ3 = 0 and the optimal rotation maps the source plane onto the target plane.  With orthonormal
+// in-plane bases (e1, e2, n_x), (f1, f2, n_y) and the 2×2 cross-covariance M of the in-plane coordinates,
+// the optimum is the better of the rotation family (c, s) ∝ (M00 + M11, M01 - M10) and the reflection
+// family (c, s) ∝ (M00 - M11, M01 + M10), the normal mapped with sign det(Q) so det R = +1.
+__device__ __forceinline__ bool tri_degenerate(double p0x, double p0y, double p0z, double p1x, double p1y,
+                                               double p1z, double p2x, double p2y, double p2z) {
+    const double ax = __dsub_rn(p1x, p0x), ay = __dsub_rn(p1y, p0y), az = __dsub_rn(p1z, p0z);
+    const double bx = __dsub_rn(p2x, p0x), by = __dsub_rn(p2y, p0y), bz = __dsub_rn(p2z, p0z);
+    const double cx = __dsub_rn(__dmul_rn(ay, bz), __dmul_rn(az, by));
+    const double cy = __dsub_rn(__dmul_rn(az, bx), __dmul_rn(ax, bz));
+    const double cz = __dsub_rn(__dmul_rn(ax, by), __dmul_rn(ay, bx));
+    const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz));
+    const double a2 = __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az));
+    const double b2 = __dadd_rn(__dadd_rn(__dmul_rn(bx, bx), __dmul_rn(by, by)), __dmul_rn(bz, bz));
+    return c2 <= __dmul_rn(1e-12, __dmul_rn(a2, b2));
+}
+
+struct d3 { double x, y, z; };
+__device__ __forceinline__ d3 mk(const float4& v) { return {(double)v.x, (double)v.y, (double)v.z}; }
+__device__ __forceinline__ d3 sub(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 cross(d3 a, d3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+__device__ __forceinline__ d3 scale(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ d3 unit(d3 a) { return scale(a, rsqrt(dot(a, a))); }
+
+// Returns false if the fit is degenerate (σ2 <= 1e-12 σ1 of the in-plane covariance, as the oracle's SVD).
+__device__ bool kabsch3(const float4& x0f, const float4& x1f, const float4& x2f, const float4& y0f, const float4& y1f,
+                        const float4& y2f, double R[9], double t[3]) {
+    const d3 x0 = mk(x0f), x1 = mk(x1f), x2 = mk(x2f), y0 = mk(y0f), y1 = mk(y1f), y2 = mk(y2f);
+    const d3 cx = {(x0.x + x1.x + x2.x) / 3.0, (x0.y + x1.y + x2.y) / 3.0, (x0.z + x1.z + x2.z) / 3.0};
+    const d3 cy = {(y0.x + y1.x + y2.x) / 3.0, (y0.y + y1.y + y2.y) / 3.0, (y0.z + y1.z + y2.z) / 3.0};
+    const d3 nx = unit(cross(sub(x1, x0), sub(x2, x0)));
+    const d3 e1 = unit(sub(x1, x0));
+    const d3 e2 = cross(nx, e1);
+    const d3 ny = unit(cross(sub(y1, y0), sub(y2, y0)));
+    const d3 f1 = unit(sub(y1, y0));
+    const d3 f2 = cross(ny, f1);
+    const d3 a[3] = {sub(x0, cx), sub(x1, cx), sub(x2, cx)};
+    const d3 b[3] = {sub(y0, cy), sub(y1, cy), sub(y2, cy)};
+    double M00 = 0, M01 = 0, M10 = 0, M11 = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double A0 = dot(a[k], e1), A1 = dot(a[k], e2);
+        const double B0 = dot(b[k], f1), B1 = dot(b[k], f2);
+        M00 += A0 * B0; M01 += A0 * B1; M10 += A1 * B0; M11 += A1 * B1;
+    }
+    const double pr = M00 + M11, qr = M01 - M10, pf = M00 - M11, qf = M01 + M10;
+    const double vr = sqrt(pr * pr + qr * qr), vf = sqrt(pf * pf + qf * qf);
+    const double s1 = 0.5 * (vr + vf), s2 = 0.5 * fabs(vr - vf);
+    if (!(s1 > 0.0) || s2 <= 1e-12 * s1) return false;
+    double Q00, Q01, Q10, Q11, dsign;
+    if (vr >= vf) {
+        const double c = pr / vr, s = qr / vr;
+        Q00 = c; Q01 = -s; Q10 = s; Q11 = c; dsign = 1.0;
+    } else {
+        const double c = pf / vf, s = qf / vf;
+        Q00 = c; Q01 = s; Q10 = s; Q11 = -c; dsign = -1.0;
+    }
+    // R = F Q E^T + det(Q) n_y n_x^T, F = [f1 f2], E = [e1 e2]
+    const double F[3][2] = {{f1.x, f2.x}, {f1.y, f2.y}, {f1.z, f2.z}};
+    const double E[3][2] = {{e1.x, e2.x}, {e1.y, e2.y}, {e1.z, e2.z}};
+    const double NY[3] = {ny.x, ny.y, ny.z}, NX[3] = {nx.x, nx.y, nx.z};
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const double g0 = F[r][0] * Q00 + F[r][1] * Q10;
+        const double g1 = F[r][0] * Q01 + F[r][1] * Q11;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) R[3 * r + c] = g0 * E[c][0] + g1 * E[c][1] + dsign * NY[r] * NX[c];
+    }
+    t[0] = cy.x - (R[0] * cx.x + R[1] * cx.y + R[2] * cx.z);
+    t[1] = cy.y - (R[3] * cx.x + R[4] * cx.y + R[5] * cx.z);
+    t[2] = cy.z - (R[6] * cx.x + R[7] * cx.y + R[8] * cx.z);
+    return true;
+}
+
+__global__ void __launch_bounds__(128) k_kabsch(WS ws) {
+    const int q = blockIdx.y;
+    const PairDesc d = ws.desc[q];
+    if (d.n == 0) return;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int K = ws.k1 * ws.k2;
+    if (s >= K) return;
+    const int4 c = ws.cliq[q * ws.cl_stride + s];
+    float* h = ws.hyp + (q * ws.cl_stride + s) * 16;
+    float out[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) out[k] = 0.f;
+    int flag = 2;
+    if (c.x >= 0) {
+        const float4* s4 = ws.src4 + q * ws.pts_stride;
+        const float4* d4 = ws.dst4 + q * ws.pts_stride;
+        const float4 x0 = s4[c.x], x1 = s4[c.y], x2 = s4[c.z];
+        const float4 y0 = d4[c.x], y1 = d4[c.y], y2 = d4[c.z];
+        flag = 1;
+        if (!tri_degenerate(x0.x, x0.y, x0.z, x1.x, x1.y, x1.z, x2.x, x2.y, x2.z) &&
+            !tri_degenerate(y0.x, y0.y, y0.z, y1.x, y1.y, y1.z, y2.x, y2.y, y2.z)) {
+            double R[9], t[3];
+            if (kabsch3(x0, x1, x2, y0, y1, y2, R, t)) {
+                flag = 0;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) out[k] = __double2float_rn(R[k]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) out[9 + k] = __double2float_rn(t[k]);
+            }
+        }
+    }
+    out[13] = __int_as_float(flag);
+    out[14] = __int_as_float(c.w);
+    float4* h4 = reinterpret_cast<float4*>(h);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h4[k] = make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+}
+
+// ------------------------------------------------------------------------------------------ a7 scoring
+// g(T) = inlier number.  Block = 128 hypotheses × a chunk of SCORE_PC correspondences that
+// one thread stages into shared memory with two bulk async copies (cp.async.bulk, the TMA engine)
+// completing on an mbarrier; every thread then streams the chunk (broadcast LDS.128) through its own
+// (R, t) in the oracle's fixed fp32 FMA tree (reading r13) and adds its count atomically.
+constexpr int SCORE_HT = 128;
+constexpr int SCORE_PC = 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(SCORE_HT) k_score(WS ws) {
+    __shared__ __align__(16) float4 s_src[SCORE_PC];
+    __shared__ __align__(16) float4 s_dst[SCORE_PC];
+    __shared__ __align__(8) unsigned long long s_bar;
+    const int q = blockIdx.z;
+    const PairDesc d = ws.desc[q];
+    const int n = d.n;
+    if (n == 0) return;
+    const int k0 = blockIdx.y * SCORE_PC;
+    if (k0 >= n) return;
+    const int kc = min(SCORE_PC, n - k0);
+    const int K = ws.k1 * ws.k2;
+    const int h = blockIdx.x * SCORE_HT + threadIdx.x;
+    float* hp = ws.hyp + (q * ws.cl_stride + h) * 16;
+    bool valid = false;
+    float R[9], t[3];
+    if (h < K) {
+        const float4* h4 = reinterpret_cast<const float4*>(hp);
+        const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
+        valid = __float_as_int(e.y) == 0;
+        R[0] = a.x; R[1] = a.y; R[2] = a.z; R[3] = a.w; R[4] = b.x; R[5] = b.y; R[6] = b.z; R[7] = b.w;
+        R[8] = c.x; t[0] = c.y; t[1] = c.z; t[2] = c.w;
+    }
+    if (!__syncthreads_or(valid)) return;
+    const uint32_t bar = smem_u32(&s_bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)kc * 16u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * bytes) : "memory");
+        const float4* gs = ws.src4 + q * ws.pts_stride + k0;
+        const float4* gd = ws.dst4 + q * ws.pts_stride + k0;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(s_src)),
+                     "l"(gs), "r"(bytes), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(s_dst)),
+                     "l"(gd), "r"(bytes), "r"(bar)
+                     : "memory");
+    }
+    {
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0; selp.u32 %0, 1, 0, P; }"
+                : "=r"(done)
+                : "r"(bar)
+                : "memory");
+        }
+    }
+    if (!valid) return;
+    const float thr2 = __fmul_rn(ws.thr, ws.thr);
+    int cnt = 0;
+#pragma unroll 4
+    for (int k = 0; k < kc; ++k) {
+        const float4 x = s_src[k];
+        const float4 y = s_dst[k];
+        const float p0 = __fmaf_rn(R[2], x.z, __fmaf_rn(R[1], x.y, __fmaf_rn(R[0], x.x, t[0])));
+        const float p1 = __fmaf_rn(R[5], x.z, __fmaf_rn(R[4], x.y, __fmaf_rn(R[3], x.x, t[1])));
+        const float p2 = __fmaf_rn(R[8], x.z, __fmaf_rn(R[7], x.y, __fmaf_rn(R[6], x.x, t[2])));
+        const float e0 = __fsub_rn(p0, y.x), e1 = __fsub_rn(p1, y.y), e2 = __fsub_rn(p2, y.z);
+        const float s = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        cnt += (s <= thr2);
+    }
+    if (cnt) atomicAdd(reinterpret_cast<int*>(hp + 12), cnt);
+}
+
+// ------------------------------------------------------------------------------------------ a8 argmax
+// Eq. 9 with reading r14: key (count desc, S desc, (i,j,z) asc), as a max over
+// (count << 17 | S) and then a min over the packed triple among the maxima.  Writes the result record.
+struct DevResult {  // mirrors turboreg_result
+    float R[9];
+    float t[3];
+    int32_t inlier_count;
+    int32_t clique[3];
+    int32_t clique_weight;
+    int32_t num_pivots, num_cliques, hypotheses_evaluated;
+    int32_t status;
+    float stage_ms[3];
+    int64_t num_edges;
+};
+
+__global__ void __launch_bounds__(256) k_finalize(WS ws) {
+    __shared__ unsigned long long s_red[8];
+    __shared__ int s_cnt[2][8];
+    const int q = blockIdx.x;
+    const PairDesc d = ws.desc[q];
+    const PairState* st = ws.st + q;
+    DevResult* res = reinterpret_cast<DevResult*>(ws.res) + q;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int K = ws.k1 * ws.k2;
+    const float* hyp = ws.hyp + q * ws.cl_stride * 16;
+    const int4* cl = ws.cliq + q * ws.cl_stride;
+    unsigned long long best1 = 0ull;
+    int ncl = 0, nev = 0;
+    if (d.n > 0) {
+        for (int s = t; s < K; s += blockDim.x) {
+            const float* h = hyp + (int64_t)s * 16;
+            const int flag = __float_as_int(h[13]);
+            if (flag != 2) ++ncl;
+            if (flag == 0) {
+                ++nev;
+                const unsigned long long key =
+                    ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+                best1 = key > best1 ? key : best1;
+            }
+        }
+    }
+    best1 = warp_max_u64(best1);
+    ncl = __reduce_add_sync(FULL, (unsigned)ncl);
+    nev = __reduce_add_sync(FULL, (unsigned)nev);
+    if (lane == 0) { s_red[warp] = best1; s_cnt[0][warp] = ncl; s_cnt[1][warp] = nev; }
+    __syncthreads();
+    if (t == 0) {
+        unsigned long long b = 0ull;
+        int a = 0, e = 0;
+        for (int w = 0; w < 8; ++w) { b = s_red[w] > b ? s_red[w] : b; a += s_cnt[0][w]; e += s_cnt[1][w]; }
+        s_red[0] = b; s_cnt[0][0] = a; s_cnt[1][0] = e;
+    }
+    __syncthreads();
+    best1 = s_red[0];
+    ncl = s_cnt[0][0];
+    nev = s_cnt[1][0];
+    __syncthreads();
+    unsigned long long bestt = ~0ull;
+    if (d.n > 0 && nev > 0) {
+        for (int s = t; s < K; s += blockDim.x) {
+            const float* h = hyp + (int64_t)s * 16;
+            if (__float_as_int(h[13]) != 0) continue;
+            const unsigned long long key =
+                ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+            if (key != best1) continue;
+            const int4 c = cl[s];
+            const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
+            if (tk < bestt) bestt = tk;
+        }
+    }
+    bestt = warp_min_u64(bestt);
+    __shared__ int s_slot;
+    if (lane == 0) s_red[warp] = bestt;
+    if (t == 0) s_slot = 0x7fffffff;
+    __syncthreads();
+    if (t == 0) {
+        unsigned long long b = ~0ull;
+        for (int w = 0; w < 8; ++w) b = s_red[w] < b ? s_red[w] : b;
+        s_red[0] = b;
+    }
+    __syncthreads();
+    bestt = s_red[0];
+    if (bestt != ~0ull) {  // the slot holding the winning triple (duplicates carry identical values)
+        for (int s = t; s < K; s += blockDim.x) {
+            if (__float_as_int(hyp[(int64_t)s * 16 + 13]) != 0) continue;
+            const int4 c = cl[s];
+            const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
+            if (tk == bestt) atomicMin(&s_slot, s);
+        }
+    }
+    __syncthreads();
+    if (t == 0) {
+        const int bests = (bestt == ~0ull) ? -1 : s_slot;
+        int status = d.host_status;
+        if (status == 0 && st->nonfinite) status = 4;
+        if (status == 0 && bests < 0) status = 5;
+        DevResult r;
+        for (int k = 0; k < 9; ++k) r.R[k] = 0.f;
+        for (int k = 0; k < 3; ++k) r.t[k] = 0.f;
+        r.inlier_count = 0;
+        r.clique[0] = r.clique[1] = r.clique[2] = -1;
+        r.clique_weight = 0;
+        r.num_pivots = (d.n > 0) ? st->npiv : 0;
+        r.num_cliques = (d.n > 0) ? ncl : 0;
+        r.hypotheses_evaluated = (d.n > 0) ? nev : 0;
+        r.status = status;
+        r.stage_ms[0] = r.stage_ms[1] = r.stage_ms[2] = 0.f;
+        r.num_edges = (d.n > 0) ? st->edges : 0;
+        if (status == 0) {
+            const float* h = hyp + (int64_t)bests * 16;
+            for (int k = 0; k < 9; ++k) r.R[k] = h[k];
+            for (int k = 0; k < 3; ++k) r.t[k] = h[9 + k];
+            r.inlier_count = __float_as_int(h[12]);
+            const int4 c = cl[bests];
+            r.clique[0] = c.x; r.clique[1] = c.y; r.clique[2] = c.z;
+            r.clique_weight = c.w;
+        }
+        *res = r;
+    }
+}
+
+}  // namespace trk

@@ -1,0 +1,615 @@
+// =====================================================================================================
+// Host runtime + C ABI of the TurboReg hot path (include/turboreg.h).  Owns the device workspace, the
+// stream, per-kernel event timing and the launch sequence of the hand-written sm_100a kernels in
+// turboreg_kernels.cuh.  No CPU fallback: every step of the path runs in those kernels.
+// =====================================================================================================
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "turboreg.h"
+#include "turboreg_kernels.cuh"
+
+static_assert(sizeof(trk::DevResult) == sizeof(turboreg_result), "result layout");
+
+namespace {
+
+enum KernelId {
+    KID_INGEST = 0,
+    KID_COMPAT,
+    KID_SC2,
+    KID_HIST_LO,
+    KID_SEL_COUNT,
+    KID_SEL_SCAN,
+    KID_SEL_EMIT,
+    KID_PGS,
+    KID_KABSCH,
+    KID_SCORE,
+    KID_FINALIZE,
+    KID_COUNT
+};
+const char* kKernelNames[KID_COUNT] = {"k_ingest",      "k_compat",     "k_sc2",   "k_hist_lo",
+                                       "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
+                                       "k_kabsch",      "k_score",      "k_finalize"};
+// stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2};
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
+
+}  // namespace
+
+struct turboreg_ctx {
+    turboreg_params prm{};
+    int device = 0;
+    int32_t max_n = 0, max_batch = 0, Wmax = 0;
+    cudaStream_t own_stream = nullptr;
+    // device workspace
+    void* d_base = nullptr;
+    size_t ws_bytes = 0;
+    trk::WS ws{};
+    trk::PairDesc* d_desc = nullptr;
+    void* d_results = nullptr;
+    float* d_inputs = nullptr;  // staging for host inputs: 2 × max_batch × max_n × 3 floats
+    // pinned host staging
+    trk::PairDesc* h_desc = nullptr;
+    turboreg_result* h_results = nullptr;
+    float* h_inputs = nullptr;
+    // bookkeeping of the last call
+    int32_t last_batch = 0;
+    std::vector<int32_t> last_n;
+    // timing
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<int> ev_kid;
+    double k_ms[KID_COUNT] = {0};
+    int64_t k_launches[KID_COUNT] = {0};
+    int64_t launches = 0;
+};
+
+namespace {
+
+turboreg_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return TURBOREG_OK;
+    if (e == cudaErrorMemoryAllocation) return TURBOREG_ERR_OUT_OF_MEMORY;
+    return TURBOREG_ERR_CUDA;
+}
+#define CK(x)                                                       \
+    do {                                                            \
+        cudaError_t e__ = (x);                                      \
+        if (e__ != cudaSuccess) {                                   \
+            if (std::getenv("TURBOREG_DEBUG"))                      \
+                std::fprintf(stderr, "turboreg: %s at %s:%d\n",     \
+                             cudaGetErrorString(e__), __FILE__, __LINE__); \
+            return cuda_status(e__);                                \
+        }                                                           \
+    } while (0)
+
+bool params_valid(const turboreg_params* p) {
+    if (!p) return false;
+    if (!(p->tau > 0.f) || !std::isfinite(p->tau)) return false;
+    if (!(p->tau_base == 0.f || (p->tau_base >= p->tau && std::isfinite(p->tau_base)))) return false;
+    if (p->k1 < 1 || p->k2 < 1) return false;
+    if ((int64_t)p->k1 * p->k2 > (int64_t)1 << 30) return false;
+    if (!(p->inlier_threshold > 0.f) || !std::isfinite(p->inlier_threshold)) return false;
+    if (p->graph_mode != 0) return false;  // undirected SC^2 mode: not in this build yet
+    if (p->flags & ~(TURBOREG_F_STAGE_TIMING | TURBOREG_F_KERNEL_TIMING)) return false;
+    return true;
+}
+
+void free_ws(turboreg_ctx* c) {
+    if (c->d_base) cudaFree(c->d_base);
+    c->d_base = nullptr;
+    c->ws_bytes = 0;
+}
+
+// Carve one allocation into the per-pair arrays (sizes by max_n, max_batch, K1*K2).
+turboreg_status alloc_ws(turboreg_ctx* c) {
+    free_ws(c);
+    const int64_t B = c->max_batch, N = c->max_n, W = c->Wmax;
+    const int64_t K1 = c->prm.k1, KC = (int64_t)c->prm.k1 * c->prm.k2;
+    const bool base = c->prm.tau_base > 0.f;
+    struct Item { size_t bytes; void** dst; };
+    trk::WS& w = c->ws;
+    w.pts_stride = N;
+    w.bits_stride = N * W;
+    w.row_stride = N;
+    w.edges_stride = std::max<int64_t>(1, N * (N - 1) / 2);
+    w.piv_stride = K1;
+    w.cl_stride = KC;
+    void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
+    void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
+    void* p_res; void* p_in;
+    std::vector<Item> items = {
+        {sizeof(trk::PairDesc) * B, &p_desc},
+        {sizeof(trk::PairState) * B, &p_st},
+        {sizeof(float4) * N * B, &p_src4},
+        {sizeof(float4) * N * B, &p_dst4},
+        {sizeof(uint32_t) * N * W * B, &p_bits},
+        {sizeof(int32_t) * N * B, &p_deg},
+        {sizeof(int32_t) * N * B, &p_gt},
+        {sizeof(int32_t) * N * B, &p_eq},
+        {sizeof(int32_t) * N * B, &p_take},
+        {sizeof(int32_t) * N * B, &p_off},
+        {sizeof(uint32_t) * (size_t)w.edges_stride * B, &p_edges},
+        {sizeof(int4) * K1 * B, &p_piv},
+        {sizeof(int4) * KC * B, &p_cl},
+        {sizeof(float) * 16 * KC * B, &p_hyp},
+        {sizeof(turboreg_result) * B, &p_res},
+        {sizeof(float) * 6 * N * B, &p_in},
+    };
+    if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
+    size_t total = 0;
+    for (auto& it : items) total += round_up((int64_t)it.bytes, 256);
+    void* basep = nullptr;
+    CK(cudaSetDevice(c->device));
+    CK(cudaMalloc(&basep, total));
+    char* cur = static_cast<char*>(basep);
+    for (auto& it : items) {
+        *it.dst = cur;
+        cur += round_up((int64_t)it.bytes, 256);
+    }
+    c->d_base = basep;
+    c->ws_bytes = total;
+    c->d_desc = static_cast<trk::PairDesc*>(p_desc);
+    w.desc = c->d_desc;
+    w.st = static_cast<trk::PairState*>(p_st);
+    w.src4 = static_cast<float4*>(p_src4);
+    w.dst4 = static_cast<float4*>(p_dst4);
+    w.bits = static_cast<uint32_t*>(p_bits);
+    w.bits_base = static_cast<uint32_t*>(p_bitsb);
+    w.deg = static_cast<int32_t*>(p_deg);
+    w.row_gt = static_cast<int32_t*>(p_gt);
+    w.row_eq = static_cast<int32_t*>(p_eq);
+    w.row_take = static_cast<int32_t*>(p_take);
+    w.row_off = static_cast<int32_t*>(p_off);
+    w.edges = static_cast<uint32_t*>(p_edges);
+    w.piv = static_cast<int4*>(p_piv);
+    w.cliq = static_cast<int4*>(p_cl);
+    w.hyp = static_cast<float*>(p_hyp);
+    w.res = p_res;
+    c->d_results = p_res;
+    c->d_inputs = static_cast<float*>(p_in);
+    return TURBOREG_OK;
+}
+
+void set_ws_params(turboreg_ctx* c) {
+    c->ws.tau = c->prm.tau;
+    c->ws.tau_base = c->prm.tau_base;
+    c->ws.thr = c->prm.inlier_threshold;
+    c->ws.k1 = c->prm.k1;
+    c->ws.k2 = c->prm.k2;
+    c->ws.mode = c->prm.graph_mode;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// --------------------------------------------------------------------------------- launch sequencing
+struct Launcher {
+    turboreg_ctx* c;
+    cudaStream_t s;
+    bool timed;
+    cudaEvent_t ev() {
+        if (c->ev_used == c->ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            c->ev_pool.push_back(e);
+        }
+        return c->ev_pool[c->ev_used++];
+    }
+    template <typename F>
+    cudaError_t run(int kid, F&& f) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (timed) { a = ev(); b = ev(); cudaEventRecord(a, s); }
+        f();
+        cudaError_t e = cudaGetLastError();
+        if (timed) { cudaEventRecord(b, s); c->ev_kid.push_back(kid); }
+        c->launches++;
+        c->k_launches[kid]++;
+        return e;
+    }
+};
+
+// Fold the recorded event pairs into the per-kernel accumulators (synchronises on the events).
+void harvest_events(turboreg_ctx* c, float* stage_ms) {
+    for (size_t k = 0; k < c->ev_kid.size(); ++k) {
+        float ms = 0.f;
+        cudaEventSynchronize(c->ev_pool[2 * k + 1]);
+        cudaEventElapsedTime(&ms, c->ev_pool[2 * k], c->ev_pool[2 * k + 1]);
+        c->k_ms[c->ev_kid[k]] += ms;
+        if (stage_ms) stage_ms[kKernelStage[c->ev_kid[k]]] += ms;
+    }
+    c->ev_kid.clear();
+    c->ev_used = 0;
+}
+
+enum RunMode { RUN_FULL = 0, RUN_FROM_ADJ = 1 };
+
+turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode) {
+    trk::WS ws = c->ws;
+    const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
+    Launcher L{c, s, timed};
+    const int Wb = words_per_row(std::max(maxn_batch, 1));
+    const unsigned B = (unsigned)batch;
+    CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
+    if (mode == RUN_FULL) {
+        CK(L.run(KID_INGEST, [&] {
+            trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
+        }));
+        const int T = (maxn_batch + 31) / 32;
+        const int64_t ntiles = (int64_t)T * (T + 1) / 2;
+        CK(L.run(KID_COMPAT, [&] {
+            const dim3 g((unsigned)((ntiles + 7) / 8), B);
+            if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws);
+            else trk::k_compat<false><<<g, 256, 0, s>>>(ws);
+        }));
+    }
+    const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
+    const int wpl = (Wb + 31) / 32;
+    CK(L.run(KID_SC2, [&] {
+        if (wpl <= 1) trk::k_sc2<1><<<grow, 256, 0, s>>>(ws);
+        else if (wpl <= 2) trk::k_sc2<2><<<grow, 256, 0, s>>>(ws);
+        else if (wpl <= 4) trk::k_sc2<4><<<grow, 256, 0, s>>>(ws);
+        else if (wpl <= 5) trk::k_sc2<5><<<grow, 256, 0, s>>>(ws);
+        else if (wpl <= 8) trk::k_sc2<8><<<grow, 256, 0, s>>>(ws);
+        else if (wpl <= 16) trk::k_sc2<16><<<grow, 256, 0, s>>>(ws);
+        else trk::k_sc2<32><<<grow, 256, 0, s>>>(ws);
+    }));
+    const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
+    CK(L.run(KID_HIST_LO, [&] { trk::k_hist_lo<<<gsel, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_SEL_COUNT, [&] { trk::k_select_count<<<gsel, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_SEL_SCAN, [&] { trk::k_select_scan<<<B, 1024, 0, s>>>(ws); }));
+    CK(L.run(KID_SEL_EMIT, [&] { trk::k_select_emit<<<gsel, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_PGS, [&] {
+        trk::k_pgs<<<dim3((c->prm.k1 + trk::PGS_WARPS - 1) / trk::PGS_WARPS, B), trk::PGS_WARPS * 32, 0, s>>>(ws);
+    }));
+    if (mode == RUN_FULL) {
+        const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
+        CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
+        CK(L.run(KID_SCORE, [&] {
+            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT),
+                         (unsigned)((maxn_batch + trk::SCORE_PC - 1) / trk::SCORE_PC), B);
+            trk::k_score<<<g, trk::SCORE_HT, 0, s>>>(ws);
+        }));
+        CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
+    }
+    return TURBOREG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* turboreg_status_string(turboreg_status s) {
+    switch (s) {
+        case TURBOREG_OK: return "ok";
+        case TURBOREG_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case TURBOREG_ERR_TOO_FEW_POINTS: return "too few points (N < 3)";
+        case TURBOREG_ERR_TOO_MANY_POINTS: return "too many points (N > max_n)";
+        case TURBOREG_ERR_NONFINITE_INPUT: return "non-finite input coordinate";
+        case TURBOREG_ERR_NO_HYPOTHESIS: return "no hypothesis";
+        case TURBOREG_ERR_CUDA: return "CUDA error";
+        case TURBOREG_ERR_OUT_OF_MEMORY: return "out of device memory";
+    }
+    return "unknown status";
+}
+
+turboreg_status turboreg_create(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
+                                turboreg_ctx** out) {
+    if (!out || !params_valid(params) || max_n < 3 || max_n > 32768 || max_batch < 1 || max_batch > 65535)
+        return TURBOREG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return TURBOREG_ERR_CUDA;
+    }
+    turboreg_ctx* c = new (std::nothrow) turboreg_ctx();
+    if (!c) return TURBOREG_ERR_OUT_OF_MEMORY;
+    c->prm = *params;
+    c->device = device;
+    c->max_n = max_n;
+    c->max_batch = max_batch;
+    c->Wmax = words_per_row(max_n);
+    turboreg_status st = TURBOREG_OK;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        st = TURBOREG_ERR_CUDA;
+    }
+    if (st == TURBOREG_OK) st = alloc_ws(c);
+    if (st == TURBOREG_OK) {
+        if (cudaMallocHost(&c->h_desc, sizeof(trk::PairDesc) * max_batch) != cudaSuccess ||
+            cudaMallocHost(&c->h_results, sizeof(turboreg_result) * max_batch) != cudaSuccess)
+            st = TURBOREG_ERR_OUT_OF_MEMORY;
+    }
+    if (st != TURBOREG_OK) {
+        cudaGetLastError();
+        turboreg_destroy(c);
+        return st;
+    }
+    set_ws_params(c);
+    *out = c;
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_set_params(turboreg_ctx* c, const turboreg_params* p) {
+    if (!c || !params_valid(p)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const bool realloc = (int64_t)p->k1 * p->k2 != (int64_t)c->prm.k1 * c->prm.k2 || p->k1 != c->prm.k1 ||
+                         ((p->tau_base > 0.f) != (c->prm.tau_base > 0.f));
+    c->prm = *p;
+    set_ws_params(c);
+    if (realloc) {
+        cudaStreamSynchronize(c->own_stream);
+        cudaDeviceSynchronize();
+        turboreg_status st = alloc_ws(c);
+        if (st != TURBOREG_OK) return st;
+    }
+    return TURBOREG_OK;
+}
+
+void turboreg_destroy(turboreg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+    free_ws(c);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->h_desc) cudaFreeHost(c->h_desc);
+    if (c->h_results) cudaFreeHost(c->h_results);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const float* dst, const int64_t* offsets,
+                                        const int32_t* n, int32_t batch, turboreg_result* out, void* stream) {
+    if (!c || !src || !dst || !offsets || !n || !out || batch < 1 || batch > c->max_batch)
+        return TURBOREG_ERR_INVALID_ARGUMENT;
+    for (int32_t p = 0; p < batch; ++p)
+        if (offsets[p] < 0 || n[p] < 0) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    const bool dev_in = is_device_ptr(src) && is_device_ptr(dst);
+    const bool dev_out = is_device_ptr(out);
+    if (is_device_ptr(src) != is_device_ptr(dst)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    // host inputs: copy each pair's rows into the device staging area (pairs are packed contiguously)
+    const float* dsrc = src;
+    const float* ddst = dst;
+    std::vector<int64_t> dev_off(offsets, offsets + batch);
+    if (!dev_in) {
+        int64_t cursor = 0;
+        float* stage_src = c->d_inputs;
+        float* stage_dst = c->d_inputs + 3 * (int64_t)c->max_n * c->max_batch;
+        // coalesce runs of contiguous pairs into single copies
+        int32_t p = 0;
+        while (p < batch) {
+            int32_t q = p;
+            int64_t len = (n[p] >= 3 && n[p] <= c->max_n) ? n[p] : 0;
+            while (q + 1 < batch && offsets[q + 1] == offsets[q] + n[q] && n[q + 1] >= 3 && n[q + 1] <= c->max_n && len > 0) {
+                ++q;
+                len += n[q];
+            }
+            if (len > 0) {
+                CK(cudaMemcpyAsync(stage_src + 3 * cursor, src + 3 * offsets[p], sizeof(float) * 3 * len,
+                                   cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(stage_dst + 3 * cursor, dst + 3 * offsets[p], sizeof(float) * 3 * len,
+                                   cudaMemcpyHostToDevice, s));
+                int64_t cc = cursor;
+                for (int32_t r = p; r <= q; ++r) { dev_off[r] = cc; cc += n[r]; }
+                cursor += len;
+            }
+            p = q + 1;
+        }
+        dsrc = stage_src;
+        ddst = stage_dst;
+    }
+    int32_t maxn_batch = 3;
+    c->last_n.assign(n, n + batch);
+    for (int32_t p = 0; p < batch; ++p) {
+        trk::PairDesc& d = c->h_desc[p];
+        d.src = dsrc + 3 * dev_off[p];
+        d.dst = ddst + 3 * dev_off[p];
+        d.host_status = 0;
+        d.pad = 0;
+        if (n[p] < 3) d.host_status = TURBOREG_ERR_TOO_FEW_POINTS;
+        else if (n[p] > c->max_n) d.host_status = TURBOREG_ERR_TOO_MANY_POINTS;
+        d.n = d.host_status ? 0 : n[p];
+        d.W = d.n ? words_per_row(d.n) : 0;
+        if (d.n > maxn_batch) maxn_batch = d.n;
+    }
+    CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc) * batch, cudaMemcpyHostToDevice, s));
+    c->last_batch = batch;
+    turboreg_status st = launch_all(c, batch, maxn_batch, s, RUN_FULL);
+    if (st != TURBOREG_OK) return st;
+    const bool want_stage = c->prm.flags & TURBOREG_F_STAGE_TIMING;
+    if (dev_out) {
+        CK(cudaMemcpyAsync(out, c->d_results, sizeof(turboreg_result) * batch, cudaMemcpyDeviceToDevice, s));
+        if (want_stage && !c->profiling) {
+            CK(cudaStreamSynchronize(s));
+            harvest_events(c, nullptr);
+        }
+    } else {
+        CK(cudaMemcpyAsync(c->h_results, c->d_results, sizeof(turboreg_result) * batch, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float stage[3] = {0, 0, 0};
+        if (want_stage && !c->profiling) harvest_events(c, stage);
+        std::memcpy(out, c->h_results, sizeof(turboreg_result) * batch);
+        if (want_stage)
+            for (int32_t p = 0; p < batch; ++p) std::memcpy(out[p].stage_ms, stage, sizeof(stage));
+    }
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_register(turboreg_ctx* c, const float* src, const float* dst, int32_t n, turboreg_result* out) {
+    if (!c || !out) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const int64_t off = 0;
+    turboreg_result tmp;
+    const bool dev_out = is_device_ptr(out);
+    if (dev_out) return TURBOREG_ERR_INVALID_ARGUMENT;
+    turboreg_status st = turboreg_register_batch(c, src, dst, &off, &n, 1, &tmp, nullptr);
+    if (st != TURBOREG_OK) return st;
+    *out = tmp;
+    return (turboreg_status)tmp.status;
+}
+
+turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_t what, void* dst, size_t bytes,
+                                           size_t* needed) {
+    if (!c || pair < 0 || pair >= c->last_batch) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    const int n = c->last_n[pair];
+    if (n < 3 || n > c->max_n) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const int W = words_per_row(n);
+    const trk::WS& w = c->ws;
+    trk::PairState st;
+    CK(cudaMemcpy(&st, w.st + pair, sizeof(st), cudaMemcpyDeviceToHost));
+    size_t need = 0;
+    switch (what) {
+        case TURBOREG_I_BITS:
+        case TURBOREG_I_BITS_BASE: {
+            if (what == TURBOREG_I_BITS_BASE && !w.bits_base) return TURBOREG_ERR_INVALID_ARGUMENT;
+            need = sizeof(uint32_t) * (size_t)n * W;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            const uint32_t* src = (what == TURBOREG_I_BITS ? w.bits : w.bits_base) + pair * w.bits_stride;
+            CK(cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_SC2: {
+            need = sizeof(int32_t) * (size_t)n * n;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            std::vector<int32_t> deg(n);
+            std::vector<uint32_t> e((size_t)n * (n - 1) / 2);
+            CK(cudaMemcpy(deg.data(), w.deg + pair * w.row_stride, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(e.data(), w.edges + pair * w.edges_stride, sizeof(uint32_t) * e.size(), cudaMemcpyDeviceToHost));
+            int32_t* G = static_cast<int32_t*>(dst);
+            std::memset(G, 0, need);
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t off = i * n - i * (i + 1) / 2;
+                for (int k = 0; k < deg[i]; ++k) {
+                    const uint32_t v = e[off + k];
+                    const int64_t j = v >> 16;
+                    const int32_t wt = (int32_t)(v & 0xffffu);
+                    G[i * n + j] = wt;
+                    G[j * n + i] = wt;
+                }
+            }
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_PIVOTS: {
+            const int P = st.npiv;
+            need = sizeof(int32_t) * 3 * (size_t)P;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            std::vector<int4> v(P);
+            if (P) CK(cudaMemcpy(v.data(), w.piv + pair * w.piv_stride, sizeof(int4) * P, cudaMemcpyDeviceToHost));
+            int32_t* o = static_cast<int32_t*>(dst);
+            for (int k = 0; k < P; ++k) { o[3 * k] = v[k].x; o[3 * k + 1] = v[k].y; o[3 * k + 2] = v[k].z; }
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_CLIQUES: {
+            need = sizeof(int4) * (size_t)w.cl_stride;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            CK(cudaMemcpy(dst, w.cliq + pair * w.cl_stride, need, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_HYPS: {
+            need = sizeof(float) * 16 * (size_t)w.cl_stride;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            CK(cudaMemcpy(dst, w.hyp + pair * w.cl_stride * 16, need, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_STATE: {
+            need = sizeof(int64_t) * 16;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            int64_t* o = static_cast<int64_t*>(dst);
+            const int64_t vals[16] = {n, W, st.edges, st.epos, st.alpha, st.c_gt, st.need, st.npiv,
+                                      st.nonfinite, st.b1, st.above, st.edges_base, 0, 0, 0, 0};
+            std::memcpy(o, vals, sizeof(vals));
+            return TURBOREG_OK;
+        }
+        default: return TURBOREG_ERR_INVALID_ARGUMENT;
+    }
+}
+
+turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bits, int32_t n, int32_t stride_words) {
+    if (!c || !bits || n < 3 || n > c->max_n || stride_words < (n + 31) / 32) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    const int W = words_per_row(n);
+    std::vector<uint32_t> rows((size_t)n * W, 0u);
+    const int used = (n + 31) / 32;
+    for (int r = 0; r < n; ++r)
+        for (int k = 0; k < used; ++k) {
+            uint32_t v = bits[(size_t)r * stride_words + k];
+            if (k == used - 1 && (n & 31)) v &= (1u << (n & 31)) - 1u;
+            rows[(size_t)r * W + k] = v;
+        }
+    cudaStream_t s = c->own_stream;
+    CK(cudaMemcpyAsync(c->ws.bits, rows.data(), sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice, s));
+    trk::PairDesc& d = c->h_desc[0];
+    d.src = nullptr;
+    d.dst = nullptr;
+    d.n = n;
+    d.W = W;
+    d.host_status = 0;
+    d.pad = 0;
+    CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc), cudaMemcpyHostToDevice, s));
+    c->last_batch = 1;
+    c->last_n.assign(1, n);
+    turboreg_status st = launch_all(c, 1, n, s, RUN_FROM_ADJ);
+    if (st != TURBOREG_OK) return st;
+    CK(cudaStreamSynchronize(s));
+    if (!c->profiling) harvest_events(c, nullptr);
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_profile_begin(turboreg_ctx* c) {
+    if (!c || !(c->prm.flags & TURBOREG_F_KERNEL_TIMING)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    harvest_events(c, nullptr);
+    for (int k = 0; k < KID_COUNT; ++k) { c->k_ms[k] = 0.0; c->k_launches[k] = 0; }
+    c->profiling = true;
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_profile_end(turboreg_ctx* c, const char** names, float* ms, int64_t* launches, int32_t cap,
+                                     int32_t* count) {
+    if (!c) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    harvest_events(c, nullptr);
+    c->profiling = false;
+    for (int k = 0; k < KID_COUNT && k < cap; ++k) {
+        if (names) names[k] = kKernelNames[k];
+        if (ms) ms[k] = (float)c->k_ms[k];
+        if (launches) launches[k] = c->k_launches[k];
+    }
+    if (count) *count = KID_COUNT;
+    return TURBOREG_OK;
+}
+
+int64_t turboreg_launch_count(const turboreg_ctx* c) { return c ? c->launches : 0; }
+
+size_t turboreg_workspace_bytes(const turboreg_ctx* c) { return c ? c->ws_bytes : 0; }
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+"""CUDA path vs oracle, element by element, through the C ABI (needs a B200: `pytest -m gpu`)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_compare import compare_pair, rot_angle_rad
+from tests.helpers import py_triangles
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tr_mod():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2507_01439_b200 import TurboReg
+
+    return TurboReg
+
+
+def _run_single(TurboReg, cfg, n=None, pair=0, max_n=None):
+    inst = synth.workload_instance(cfg, pair=pair, n=n)
+    nn = inst["src"].shape[0]
+    tr = TurboReg(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=max_n or nn, max_batch=1)
+    res = tr.register(inst["src"], inst["dst"])
+    return tr, inst, res
+
+
+@pytest.mark.parametrize("key", ["A", "B", "C", "D"])
+def test_configs_full_parity(tr_mod, key):
+    cfg = synth.CONFIGS[key]
+    tr, inst, res = _run_single(tr_mod, cfg)
+    stats = compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+    print(key, stats)
+    assert res["status"] == 0
+    assert synth.rotation_error_deg(res["R"], inst["R"]) < 5.0
+
+
+@pytest.mark.parametrize("n", [3, 4, 31, 32, 33, 63, 65, 97, 1337, 2049])
+def test_ragged_sizes(tr_mod, n):
+    cfg = synth.CONFIGS["A"]
+    tr, inst, res = _run_single(tr_mod, cfg, n=n, max_n=max(n, 100))
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+@pytest.mark.parametrize("k1,k2", [(1, 1), (7, 3), (500, 8), (300, 9), (5000, 2)])
+def test_budgets(tr_mod, k1, k2):
+    cfg = synth.CONFIGS["A"]
+    inst = synth.workload_instance(cfg, pair=3)
+    tr = tr_mod(cfg.tau, k1, k2, cfg.inlier_threshold, max_n=cfg.n)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, k1, k2, cfg.inlier_threshold, result=res)
+
+
+def test_batch_mixed_sizes_and_statuses(tr_mod):
+    cfg = synth.CONFIGS["A"]
+    sizes = [500, 2, 333, 600, 77, 0, 500]
+    insts, srcs, dsts = [], [], []
+    for p, n in enumerate(sizes):
+        inst = synth.workload_instance(cfg, pair=10 + p, n=max(n, 1))
+        s, d = inst["src"][:n], inst["dst"][:n]
+        if p == 6:
+            d = d.copy()
+            d[17, 1] = np.nan
+        insts.append(inst)
+        srcs.append(s)
+        dsts.append(d)
+    n = np.array(sizes, np.int32)
+    off = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=550, max_batch=len(sizes))
+    res = tr.register_batch(np.concatenate(srcs), np.concatenate(dsts), off, n)
+    assert [int(r) for r in res["status"]] == [0, 2, 0, 3, 0, 2, 4]
+    for p in (0, 2, 4):
+        r = {k: res[p][k] for k in res.dtype.names}
+        compare_pair(tr, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+    for p in (1, 3, 5, 6):
+        assert np.all(res[p]["R"] == 0) and np.all(res[p]["t"] == 0)
+
+
+def test_device_inputs_match_host_inputs(tr_mod):
+    import torch
+
+    cfg = synth.CONFIGS["A"]
+    inst = synth.workload_instance(cfg, pair=5)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=cfg.n, max_batch=2)
+    host = tr.register_batch(np.concatenate([inst["src"]] * 2), np.concatenate([inst["dst"]] * 2),
+                             np.array([0, cfg.n]), np.array([cfg.n, cfg.n]))
+    ds = torch.from_numpy(np.concatenate([inst["src"]] * 2)).cuda()
+    dd = torch.from_numpy(np.concatenate([inst["dst"]] * 2)).cuda()
+    out = torch.zeros(2 * 104, dtype=torch.uint8, device="cuda")
+    tr.register_batch(ds, dd, np.array([0, cfg.n]), np.array([cfg.n, cfg.n]), out=out)
+    torch.cuda.synchronize()
+    from paper_2507_01439_b200 import RESULT_DTYPE
+
+    dev = out.cpu().numpy().view(RESULT_DTYPE)
+    assert dev.tobytes() == host.tobytes()
+    assert host[0].tobytes() == host[1].tobytes()
+
+
+@pytest.mark.parametrize("density", [0.05, 0.2, 0.5])
+@pytest.mark.parametrize("seed", range(2))
+def test_injected_adjacency_full_budget(tr_mod, density, seed):
+    # SC^2 weights bit-exact and App. C: O2 with K1 = all edges, K2 = N gives every triangle exactly once
+    n = 60 + 37 * seed
+    C = synth.erdos_renyi(n, density, 900 + seed)
+    tr = tr_mod(0.01, n * n, n, 0.1, max_n=n)
+    tr.pgs_from_adjacency(C)
+    from paper_2507_01439_b200._binding import I_CLIQUES, I_PIVOTS, I_SC2
+
+    G = tr.intermediate(0, I_SC2)
+    assert (G == oracle.sc2(C)).all()
+    O = oracle.o2(oracle.sc2(C))
+    piv = oracle.select_pivots(O, n * n)
+    assert sorted(map(tuple, piv.tolist())) == list(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
+    cl = tr.intermediate(0, I_CLIQUES)
+    cl = cl[cl[:, 0] >= 0]
+    assert sorted(map(tuple, cl[:, :3].tolist())) == sorted(py_triangles(C))
+    ref, _ = oracle.pgs(O, piv, n)
+    assert sorted(map(tuple, cl.tolist())) == sorted(map(tuple, ref.tolist()))
+
+
+@pytest.mark.parametrize("k1,k2", [(3, 2), (40, 1), (100, 5)])
+def test_injected_adjacency_budgets(tr_mod, k1, k2):
+    n = 150
+    C = synth.erdos_renyi(n, 0.2, 4242)
+    tr = tr_mod(0.01, k1, k2, 0.1, max_n=n)
+    tr.pgs_from_adjacency(C)
+    from paper_2507_01439_b200._binding import I_CLIQUES, I_PIVOTS
+
+    O = oracle.o2(oracle.sc2(C))
+    piv = oracle.select_pivots(O, k1)
+    assert sorted(map(tuple, piv.tolist())) == list(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
+    ref, _ = oracle.pgs(O, piv, k2)
+    cl = tr.intermediate(0, I_CLIQUES)
+    cl = cl[cl[:, 0] >= 0]
+    assert sorted(map(tuple, cl.tolist())) == sorted(map(tuple, ref.tolist()))
+
+
+def test_complete_graph_all_ties(tr_mod):
+    # K_N: every weight N-2, the K1 pivots are the lexicographically first edges
+    n = 70
+    C = (1 - np.eye(n)).astype(np.uint8)
+    tr = tr_mod(0.01, 100, 3, 0.1, max_n=n)
+    tr.pgs_from_adjacency(C)
+    from paper_2507_01439_b200._binding import I_CLIQUES, I_PIVOTS
+
+    piv = tr.intermediate(0, I_PIVOTS)
+    lex = [(i, j) for i in range(n) for j in range(i + 1, n)][:100]
+    assert list(map(tuple, piv[:, :2].tolist())) == lex and (piv[:, 2] == n - 2).all()
+    cl = tr.intermediate(0, I_CLIQUES)
+    O = oracle.o2(oracle.sc2(C))
+    ref, _ = oracle.pgs(O, oracle.select_pivots(O, 100), 3)
+    assert sorted(map(tuple, cl[cl[:, 0] >= 0].tolist())) == sorted(map(tuple, ref.tolist()))
+
+
+def test_tau_base_plane(tr_mod):
+    cfg = synth.CONFIGS["A"]
+    inst = synth.workload_instance(cfg, pair=8)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, tau_base=4 * cfg.tau, max_n=cfg.n)
+    res = tr.register(inst["src"], inst["dst"])
+    Cb = tr.bits(0, base=True)
+    ref_b, eb, _, _ = oracle.compat(inst["src"], inst["dst"], 4 * cfg.tau)
+    assert (Cb == ref_b).all()
+    from paper_2507_01439_b200._binding import I_STATE
+
+    assert tr.intermediate(0, I_STATE)["edges_base"] == eb
+    C = tr.bits(0)
+    assert (C <= Cb).all()  # τ-monotonicity
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+def test_noise_free_exact_recovery(tr_mod):
+    # App. A.3: congruent triangles fix T; 0 outliers, σ = 0 → every inlier counted
+    inst = synth.generate(400, 1.0, (1, 1, 1), 0.0, seed=31)
+    tr = tr_mod(0.001, 200, 2, 0.001, max_n=400)
+    res = tr.register(inst["src"], inst["dst"])
+    assert res["status"] == 0 and res["inlier_count"] == 400
+    assert rot_angle_rad(res["R"], inst["R"]) < 1e-5
+    assert np.abs(res["t"] - inst["t"]).max() < 1e-5
+
+
+def test_no_hypothesis(tr_mod):
+    # all-outlier, tiny τ: no edge has a positive SC^2 weight → NoHypothesis, zero transform
+    rng = np.random.default_rng(0)
+    src = rng.uniform(-1, 1, (300, 3)).astype(np.float32)
+    dst = rng.uniform(-1, 1, (300, 3)).astype(np.float32)
+    tr = tr_mod(1e-7, 100, 2, 0.01, max_n=300)
+    res = tr.register(src, dst)
+    assert res["status"] == 5 and np.all(res["R"] == 0) and res["num_pivots"] == 0
+
+
+def test_full_size_batch_sampled_parity(tr_mod):
+    # BASELINE sizes in the bench's launch configuration (a batch of config-E pairs), sampled pairs checked
+    # against the oracle element by element, every pair checked for planted recovery.
+    cfg = synth.CONFIGS["E"]
+    P = 6
+    insts = [synth.workload_instance(cfg, pair=p) for p in range(P)]
+    n = np.full(P, cfg.n, np.int32)
+    off = (np.arange(P) * cfg.n).astype(np.int64)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=cfg.n, max_batch=P)
+    res = tr.register_batch(np.concatenate([i["src"] for i in insts]), np.concatenate([i["dst"] for i in insts]),
+                            off, n)
+    for p in (0, P - 1):
+        r = {k: res[p][k] for k in res.dtype.names}
+        compare_pair(tr, p, insts[p]["src"], insts[p]["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+    for p in range(P):
+        assert res[p]["status"] == 0
+        assert synth.rotation_error_deg(res[p]["R"].reshape(3, 3), insts[p]["R"]) <= 5
+        assert synth.translation_error(res[p]["t"], insts[p]["t"]) <= 0.1
