@@ -1,0 +1,380 @@
+#!/usr/bin/env python3
+"""Benchmark: registrations/sec at N=5000 with 1K TurboCliques (K1=1000, K2=2) on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--pairs P] [--impl reference]
+
+One step = one pass of the whole hot path (compat → SC^2 → pivots → PGS → Kabsch → scoring → argmax)
+over a batch of P synthetic 3DMatch-shaped pairs per GPU (BASELINE.json configs[4] shape with the
+configs[1] parameters; weak scaling: every rank registers its own P pairs).  Inputs are resident in
+HBM when the timed region starts; L2 is flushed (256 MiB write) before every timed step.  Timing is
+CUDA events on the launching stream, max over ranks.  Rank 0 prints one JSON line.
+
+`--impl reference` times the CPU oracle (oracle/, the only other place this script executes it) on the
+host cores, a bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "registrations/s"
+CFG = synth.CONFIGS["E"]
+PAIRS_PER_GPU = 203  # ceil(1623 / 8): the 3DMatch pair count split over the 8-GPU box
+L2_FLUSH_BYTES = 256 << 20
+POPC_PER_CLK_PER_SM = 16  # CUDA C Programming Guide arithmetic-instruction throughput table
+SMS = 148
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for k, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ workload
+def make_inputs(rank, pairs, n=None):
+    n = n or CFG.n
+    src = np.empty((pairs * n, 3), np.float32)
+    dst = np.empty((pairs * n, 3), np.float32)
+    gts = []
+    for p in range(pairs):
+        inst = synth.workload_instance(CFG, pair=rank * pairs + p, n=n)
+        src[p * n:(p + 1) * n] = inst["src"]
+        dst[p * n:(p + 1) * n] = inst["dst"]
+        gts.append((inst["R"], inst["t"]))
+    return src, dst, gts
+
+
+def algorithmic_work(tr, pairs):
+    """Per-kernel algorithmic units of the last call, summed over its pairs."""
+    from paper_2507_01439_b200._binding import I_STATE
+
+    edges = words = tests = resid = 0
+    for p in range(pairs):
+        st = tr.intermediate(p, I_STATE)
+        n = st["n"]
+        edges += st["edges"]
+        words += st["edges"] * ((n + 31) // 32)
+        tests += n * (n - 1) // 2
+    return {"sc2_word_ops": words, "compat_pair_tests": tests, "edges": edges}
+
+
+def cpu_sample(seconds=12.0, min_pairs=2):
+    """The oracle as it stands, single-threaded, on config-E pairs until `seconds` elapse."""
+    import oracle
+
+    oracle.build()
+    done, t0 = 0, time.perf_counter()
+    while True:
+        inst = synth.workload_instance(CFG, pair=10_000 + done)
+        r = oracle.estimate(inst["src"], inst["dst"], CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold)
+        assert r["status"] == 0
+        done += 1
+        el = time.perf_counter() - t0
+        if done >= min_pairs and el >= seconds:
+            break
+    return {"value": done / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{done} config-E pairs (N=5000, K1=1000, K2=2, seeds {CFG.seed + 10000}..), single thread, "
+                      f"{el:.1f} s"}
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    cores = 1
+    times = []
+    for step in range(args.warmup + args.steps):
+        inst = synth.workload_instance(CFG, pair=20_000 + step)
+        t0 = time.perf_counter()
+        r = oracle.estimate(inst["src"], inst["dst"], CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold)
+        dt = time.perf_counter() - t0
+        assert r["status"] == 0
+        if step >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[4] 3DMatch-shaped pairs (N=5000, K1=1000, K2=2); one pair per step",
+                   "pairs_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{len(times)} config-E pairs, one per step, single-threaded C++ oracle"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ CUDA arm
+def run_cuda(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_01439_b200 import RESULT_DTYPE, TurboReg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pairs = args.pairs
+    n = CFG.n
+    src_h, dst_h, gts = make_inputs(rank, pairs)
+    off = (np.arange(pairs) * n).astype(np.int64)
+    nn = np.full(pairs, n, np.int32)
+    src_d = torch.from_numpy(src_h).to(dev)
+    dst_d = torch.from_numpy(dst_h).to(dev)
+    out_d = torch.zeros(pairs * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)  # explicit stream: kernels, events and the L2 flush all on it
+    torch.cuda.set_stream(stream)
+    tr = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=pairs, device=local_rank,
+                  kernel_timing=True)
+
+    def step():
+        tr.register_batch(src_d, dst_d, off, nn, out=out_d, stream=stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on the warm-up output (planted recovery)
+    res = out_d.cpu().numpy().view(RESULT_DTYPE)
+    ok = sum(int(r["status"] == 0 and synth.rotation_error_deg(r["R"].reshape(3, 3), g[0]) <= 5) for r, g in zip(res, gts))
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = tr.launch_count
+    tr.profile_begin()
+    barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(float(k))  # L2 flush (256 MiB write), outside the event region
+        ev0[k].record(stream)
+        step()
+        ev1[k].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    kern = tr.profile_end()
+    launches = tr.launch_count - launches0
+    clk = clocks.stop()
+    dev_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms_max = float(t.item())
+    value = world * pairs * args.steps / (dev_ms_max / 1000.0)
+
+    # ---- end-to-end through the public API with pinned HOST buffers (H2D + D2H inside the timed region)
+    src_p = torch.from_numpy(src_h).pin_memory()
+    dst_p = torch.from_numpy(dst_h).pin_memory()
+    tr_e2e = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=pairs, device=local_rank)
+    for _ in range(max(1, args.warmup)):
+        tr_e2e.register_batch(src_p, dst_p, off, nn)
+    e2e_times = []
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        host_res = tr_e2e.register_batch(src_p, dst_p, off, nn)  # blocking: copies in, kernels, result out
+        e2e_times.append(time.perf_counter() - t0)
+    te = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * pairs * args.steps / float(te.item())
+    assert (host_res["status"] == 0).all()
+    tr_e2e.close()
+
+    # ---- single-pair latency (configs[1]) for context
+    tr1 = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=1, device=local_rank)
+    s1, d1 = src_d[:n].contiguous(), dst_d[:n].contiguous()
+    o1 = torch.zeros(RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        tr1.register_batch(s1, d1, off[:1], nn[:1], out=o1, stream=stream.cuda_stream)
+    lat = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tr1.register_batch(s1, d1, off[:1], nn[:1], out=o1, stream=stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b))
+    tr1.close()
+
+    # gather per-pair results (the only collective: NCCL all_gather of fixed-size records, outside timing)
+    if world > 1:
+        gathered = [torch.zeros_like(out_d) for _ in range(world)]
+        dist.all_gather(gathered, out_d)
+        all_ok = sum(int((g.cpu().numpy().view(RESULT_DTYPE)["status"] == 0).sum()) for g in gathered)
+    else:
+        all_ok = int((res["status"] == 0).sum())
+
+    if rank != 0:
+        return
+    work = algorithmic_work(tr, pairs)
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    # dominant kernel by measured time
+    dom = max(kern.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_launches) = dom
+    avg_launch_s = dom_ms / max(dom_launches, 1) / 1000.0
+    roof = None
+    if dom_name == "k_sc2":
+        peak = POPC_PER_CLK_PER_SM * SMS * sm_max * 1e6 / 1e12  # Tword-ops/s
+        achieved = work["sc2_word_ops"] / avg_launch_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (32-bit AND+POPC word ops)",
+                "frac": achieved / peak, "kernel": dom_name,
+                "per_unit": "ceil(N/32) word ops per O2 edge; units per launch = Σ_pairs E_p",
+                "peak_source": f"POPC {POPC_PER_CLK_PER_SM}/clk/SM x {SMS} SMs x {sm_max:.0f} MHz (DESIGN.md)"}
+    elif dom_name == "k_compat":
+        ops_per_test = 2  # two sqrt.rn on the MUFU-fed path; see DESIGN.md
+        peak = SMS * 16 * sm_max * 1e6 / 1e12 / ops_per_test
+        achieved = work["compat_pair_tests"] / avg_launch_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Ttests/s", "frac": achieved / peak,
+                "kernel": dom_name}
+    if roof is not None:
+        roof["traffic"] = ncu_traffic(dom_name)
+        roof["measured_ms_per_launch"] = avg_launch_s * 1000
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[4]: batch of 3DMatch-shaped pairs (configs[1] parameters)",
+                   "pairs_per_gpu": pairs, "N": n, "K1": CFG.k1, "K2": CFG.k2, "tau_m": CFG.tau,
+                   "inlier_threshold_m": CFG.inlier_threshold, "inlier_ratio": CFG.inlier_ratio,
+                   "l2": "flushed before every timed step (256 MiB write)", "parallelism": f"dp{world} (pairs)"},
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(src_h.nbytes + dst_h.nbytes),
+                "d2h_bytes_per_step": int(pairs * RESULT_DTYPE.itemsize)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+        "single_pair_latency_ms": float(np.median(lat)),
+        "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{pairs * world}",
+        "wall_s_timed_region": wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample()
+    print(json.dumps(line), flush=True)
+    tr.close()
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch from the committed ncu --set full summary (profiles/), or None."""
+    import glob
+
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+            if kernel in d:
+                return d[kernel]
+        except Exception:
+            pass
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--pairs", type=int, default=PAIRS_PER_GPU)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_cuda(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,16 @@ turboreg_status turboreg_profile_begin(turboreg_ctx* ctx);
 turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, float* ms, int64_t* launches,
                                      int32_t cap, int32_t* count);
 
+/* Tuning / test knobs (never change results, only which kernels compute them):
+ *   "sc2_path"         0 = auto: dense high-degree block on tcgen05 tensor cores + sparse popcount for the
+ *                          rest (default); 1 = popcount only; 2 = dense block on CUDA cores (__dp4a) —
+ *                          a cross-check of the tensor-core path
+ *   "heavy_min_rows"   minimum |H| for the dense block to be used (default 128)
+ *   "heavy_min_degree" minimum degree of a heavy row (default 32)
+ *   "heavy_cap"        maximum |H| (multiple of 256, <= the allocated capacity)
+ * Returns TURBOREG_ERR_INVALID_ARGUMENT for unknown names or values. */
+turboreg_status turboreg_set_option(turboreg_ctx* ctx, const char* name, int64_t value);
+
 /* Number of kernels this context has launched since creation (all calls). */
 int64_t turboreg_launch_count(const turboreg_ctx* ctx);
 

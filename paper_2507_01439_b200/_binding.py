@@ -106,6 +106,8 @@ def library():
     lib.turboreg_pgs_from_adjacency.argtypes = [P, P, i32, i32]
     lib.turboreg_profile_begin.argtypes = [P]
     lib.turboreg_profile_end.argtypes = [P, P, P, P, i32, ctypes.POINTER(i32)]
+    lib.turboreg_set_option.argtypes = [P, ctypes.c_char_p, i64]
+    lib.turboreg_set_option.restype = ctypes.c_int
     lib.turboreg_launch_count.argtypes = [P]
     lib.turboreg_launch_count.restype = i64
     lib.turboreg_workspace_bytes.argtypes = [P]
@@ -181,6 +183,10 @@ class TurboReg:
             setattr(self.params, k, v)
         _check(self._lib.turboreg_set_params(self._h, ctypes.byref(self.params)), "set_params")
 
+    def set_option(self, name, value):
+        """Tuning/test knobs of include/turboreg.h (sc2_path, heavy_min_rows, heavy_min_degree, heavy_cap)."""
+        _check(self._lib.turboreg_set_option(self._h, name.encode(), int(value)), f"set_option({name})")
+
     # ------------------------------------------------------------------------------------------ compute
     def register(self, src, dst):
         """One pair (host numpy or device torch N×3 float32).  Returns a dict; status in ['status']."""
@@ -246,7 +252,7 @@ class TurboReg:
         if what == I_STATE:
             s = buf.view(np.int64)
             keys = ["n", "W", "edges", "epos", "alpha", "c_gt", "need", "npiv", "nonfinite", "b1", "above",
-                    "edges_base"]
+                    "edges_base", "heavy_h", "heavy_thr", "deg_sum"]
             return {k: int(s[i]) for i, k in enumerate(keys)}
         return buf
 

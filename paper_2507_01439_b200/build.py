@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libturboreg.so")
 SOURCES = [os.path.join(CSRC, "turboreg_runtime.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "turboreg_kernels.cuh"), os.path.join(ROOT, "include", "turboreg.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "turboreg_kernels.cuh"), os.path.join(CSRC, "turboreg_sc2_mma.cuh"), os.path.join(ROOT, "include", "turboreg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -39,7 +39,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed ({r.returncode}) building {LIB}")
+    if verbose:
+        sys.stderr.write(r.stdout + r.stderr)
     os.replace(tmp, LIB)
     return LIB
 

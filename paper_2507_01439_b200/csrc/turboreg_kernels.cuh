@@ -16,6 +16,7 @@
 // =====================================================================================================
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace trk {
@@ -42,7 +43,11 @@ struct PairState {
     int32_t need;       // K1 - c_gt: how many weight-α edges are taken (lexicographically first)
     int32_t npiv;       // |P|
     int32_t edges_base; // edges of C(τ_base)
-    int32_t pad[6];
+    int32_t heavy_h;    // |H|, rows whose SC^2 block runs on the tensor cores (0 = none)
+    int32_t heavy_thr;  // degree threshold that defined H
+    unsigned long long deg_sum;  // Σ_i deg(i) = 2E
+    int32_t deg_max;             // max_i deg(i)
+    int32_t pad[1];
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
@@ -70,6 +75,20 @@ struct WS {
     float* hyp;
     int64_t cl_stride;  // K1*K2
     void* res;          // turboreg_result[batch]
+    // heavy/light SC^2 split (turboreg_sc2_mma.cuh)
+    int32_t* deg_full;    // [n] full degree
+    int32_t* hpos;        // [n] position in H or -1
+    int32_t* heavy_list;  // [cap] H in index order
+    uint16_t* lists;      // [n][LIST_MAX] sorted neighbour lists of rows with degree <= LIST_MAX
+    int64_t lists_stride;
+    uint32_t* heavy_mask; // [W] bitset of H
+    uint8_t* heavy_X;     // [cap][Kcap] uint8 rows of C restricted to H
+    int64_t heavy_X_stride;
+    int32_t heavy_Kcap;
+    int32_t heavy_cap;    // max |H| (multiple of 256)
+    uint16_t* heavy_D;    // [cap][cap] X X^T
+    int64_t heavy_D_stride;
+    int32_t heavy_min_rows, heavy_min_deg, sc2_path;
     float tau, tau_base, thr;
     int32_t k1, k2, mode;
 };
@@ -130,37 +149,67 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
 
 // ------------------------------------------------------------------------------------------ a2 compat
 // Eq. 1 on 32×32 tiles of the upper block triangle.  One warp per tile (I ≤ J): lane l owns
-// column point J*32+l, the 32 row points I*32+r are broadcast by shuffles.  Each test is evaluated once;
-// the ballot over lanes is row word (I*32+r, J) and the lane's own bit accumulation is the mirrored
-// column word (J*32+l, I) — exact because IEEE subtraction is antisymmetric (x_i - x_j = -(x_j - x_i)).
-// Float32 tree = the oracle's: ((dx*dx + dy*dy) + dz*dz), sqrt.rn, |a - b| <= τ (readings r1, r2).
+// column point J*32+l; the 32 row points I*32+r are staged in shared memory and read as broadcasts.  Each
+// test is evaluated once: the ballot over lanes is row word (I*32+r, J), the lane's own bit accumulation
+// the mirrored column word (J*32+l, I) — exact because IEEE subtraction is antisymmetric.
+//
+// The decision must equal the oracle's float32 tree bit for bit: a = sqrt.rn((dx*dx + dy*dy) + dz*dz),
+// b likewise, edge ⇔ |a - b| <= τ (readings r1, r2).  Two correctly rounded square roots per test are
+// the expensive part, so a certified filter decides first, without square roots.  With A = a², B = b²,
+// S = A + B:
+//   S < τ²  ⇒ edge;   S > τ²  ⇒ ( edge ⇔ q := (A − B)² − τ²(2S − τ²) <= 0 )     (q = (S−τ²)² − 4AB)
+// In float32 (ε = 2^-24, FMAs) the error of q is below 8ε|A−B|S + 15ετ²S and the filter decides only when
+// |q| > 2^-19 (|A−B| + τ² + 2^-21 S) S and S is outside τ²(1 ± 2^-16).  These margins also exceed the
+// oracle's own float32 rounding band around τ (|Δ − τ| <= 2^-22 (a + b)), so wherever the filter decides it
+// provably agrees with the exact tree.  The rest — pairs with |Δ − τ| ≲ 2^-20 (a + b),
+// a few per million — are re-evaluated with the exact tree after the tile loop (lanes that met one redo
+// their 32 tests; the warp re-ballots), so the common path carries no branch.
 __device__ __forceinline__ float f32_dist(float ax, float ay, float az, float bx, float by, float bz) {
     float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
     return __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)));
 }
 
-template <bool BASE>
-__global__ void __launch_bounds__(256) k_compat(WS ws) {
-    const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    const int n = d.n;
-    if (n == 0) return;
-    const int W = d.W;
-    const int T = (n + 31) >> 5;
-    const int64_t ntiles = (int64_t)T * (T + 1) / 2;
-    const int lane = threadIdx.x & 31;
-    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= ntiles) return;
-    // tile t → (I, J): tiles of block-row I are J = I..T-1; cum(I) = I*T - I(I-1)/2
-    const double tw = 2.0 * T + 1.0;
-    int I = (int)((tw - sqrt(tw * tw - 8.0 * (double)t)) * 0.5);
-    if (I < 0) I = 0;
-    if (I > T - 1) I = T - 1;
-    auto cum = [&](int64_t r) { return r * T - r * (r - 1) / 2; };
-    while (I + 1 <= T - 1 && cum(I + 1) <= t) ++I;
-    while (I > 0 && cum(I) > t) --I;
-    const int J = I + (int)(t - cum(I));
+// Packed float32 pairs (sm_100 f32x2 ALU ops: two IEEE round-to-nearest results per instruction).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    return (f2_t)__float_as_uint(lo) | ((f2_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t f2_lo(f2_t v) { return (uint32_t)v; }
+__device__ __forceinline__ uint32_t f2_hi(f2_t v) { return (uint32_t)(v >> 32); }
 
+// Filter decision for one test from its float32 bit patterns (all compared quantities but q are >= 0, and
+// for non-negative IEEE floats integer order is float order): returns 1 edge, 0 no edge, 2 unsure.
+__device__ __forceinline__ uint32_t filter_decide(uint32_t Sb, uint32_t qb, uint32_t Tqb, uint32_t s_lo_b,
+                                                  uint32_t s_hi_b, bool* unsure) {
+    const bool sure_in = Sb < s_lo_b;
+    const bool sure_q = (Sb > s_hi_b) && ((qb & 0x7fffffffu) > Tqb);
+    const bool qle0 = (int32_t)qb <= 0;  // q <= 0 (q is finite for finite inputs)
+    *unsure = !(sure_in || sure_q);
+    return (sure_in || (sure_q && qle0)) ? 1u : 0u;
+}
+
+// One 32×32 tile (I, J >= I) by one warp; the block's 32 row points are staged in shared memory, packed
+// as row pairs (x_{2k}, x_{2k+1}, y_{2k}, y_{2k+1}) / (z_{2k}, z_{2k+1}) so one f32x2 op serves two tests.
+template <bool BASE>
+__device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, int T, int I, int J,
+                                            const float4* s_rs, const float4* s_rd, const float4* s_pxy,
+                                            const float2* s_pz, const float4* s_qxy, const float2* s_qz) {
+    const int lane = threadIdx.x & 31;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
     const float4* d4 = ws.dst4 + p * ws.pts_stride;
     const int c = J * 32 + lane;
@@ -169,36 +218,95 @@ __global__ void __launch_bounds__(256) k_compat(WS ws) {
     const float4 cd = cv ? d4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int r0 = I * 32 + lane;
     const bool rv = r0 < n;
-    const float4 rs = rv ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 rd = rv ? d4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float tau = ws.tau, taub = ws.tau_base;
     const int rmax = min(32, n - I * 32);
-    uint32_t roww = 0, colw = 0, rowb = 0, colb = 0;
-#pragma unroll 4
-    for (int r = 0; r < 32; ++r) {
-        const float xs = __shfl_sync(FULL, rs.x, r), ys = __shfl_sync(FULL, rs.y, r), zs = __shfl_sync(FULL, rs.z, r);
-        const float xd = __shfl_sync(FULL, rd.x, r), yd = __shfl_sync(FULL, rd.y, r), zd = __shfl_sync(FULL, rd.z, r);
-        const float a = f32_dist(xs, ys, zs, cs.x, cs.y, cs.z);
-        const float b = f32_dist(xd, yd, zd, cd.x, cd.y, cd.z);
-        const float delta = fabsf(__fsub_rn(a, b));
-        const bool ok = cv && (r < rmax) && (I * 32 + r != c);
-        const bool e = ok && (delta <= tau);
-        const uint32_t bal = __ballot_sync(FULL, e);
-        if (lane == r) roww = bal;
-        colw |= (uint32_t)e << r;
-        if (BASE) {
-            const bool eb = ok && (delta <= taub);
-            const uint32_t balb = __ballot_sync(FULL, eb);
-            if (lane == r) rowb = balb;
-            colb |= (uint32_t)eb << r;
+    // validity masks: column word bit r ⇔ row I*32+r exists (and is not this lane's own point);
+    // row word bit l ⇔ column J*32+l exists (and is not this lane's own point)
+    uint32_t okc = cv ? (rmax >= 32 ? 0xffffffffu : ((1u << rmax) - 1u)) : 0u;
+    const uint32_t cvb = __ballot_sync(FULL, cv);
+    uint32_t okr = rv ? cvb : 0u;
+    if (I == J) { okc &= ~(1u << lane); okr &= ~(1u << lane); }
+    uint32_t colw = 0, roww = 0, colb = 0, rowb = 0;
+    if (!BASE) {
+        const float t2 = __fmul_rn(tau, tau);
+        const f2_t t2x2 = f2_pack(t2, t2);
+        const float m2t2 = -2.0f * t2;
+        const float t4 = __fmul_rn(t2, t2);
+        const f2_t m2t2x2 = f2_pack(m2t2, m2t2), t4x2 = f2_pack(t4, t4);
+        const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), c19 = f2_pack(0x1p-19f, 0x1p-19f);
+        const f2_t mone = f2_pack(-1.0f, -1.0f);
+        const uint32_t s_hi_b = __float_as_uint(__fmul_rn(t2, 1.0f + 0x1p-16f));
+        const uint32_t s_lo_b = __float_as_uint(__fmul_rn(t2, 1.0f - 0x1p-16f));
+        const f2_t ncx = f2_pack(-cs.x, -cs.x), ncy = f2_pack(-cs.y, -cs.y), ncz = f2_pack(-cs.z, -cs.z);
+        const f2_t ndx = f2_pack(-cd.x, -cd.x), ndy = f2_pack(-cd.y, -cd.y), ndz = f2_pack(-cd.z, -cd.z);
+        bool unsure_any = false;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const float4 P = s_pxy[k];
+            const float2 Pz = s_pz[k];
+            const float4 Q = s_qxy[k];
+            const float2 Qz = s_qz[k];
+            const f2_t dx = f2_add(f2_pack(P.x, P.y), ncx), dy = f2_add(f2_pack(P.z, P.w), ncy);
+            const f2_t dz = f2_add(f2_pack(Pz.x, Pz.y), ncz);
+            const f2_t ex = f2_add(f2_pack(Q.x, Q.y), ndx), ey = f2_add(f2_pack(Q.z, Q.w), ndy);
+            const f2_t ez = f2_add(f2_pack(Qz.x, Qz.y), ndz);
+            const f2_t A = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+            const f2_t B = f2_fma(ez, ez, f2_fma(ey, ey, f2_mul(ex, ex)));
+            const f2_t S = f2_add(A, B);
+            const f2_t D = f2_fma(B, mone, A);
+            const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
+            const f2_t absD = D & 0x7fffffff7fffffffull;
+            const f2_t Tq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, c19));
+            bool u0, u1;
+            const uint32_t e0 = filter_decide(f2_lo(S), f2_lo(q), f2_lo(Tq), s_lo_b, s_hi_b, &u0);
+            const uint32_t e1 = filter_decide(f2_hi(S), f2_hi(q), f2_hi(Tq), s_lo_b, s_hi_b, &u1);
+            unsure_any |= u0 | u1;
+            colw |= (e0 << (2 * k)) | (e1 << (2 * k + 1));
+            const uint32_t b0 = __ballot_sync(FULL, e0), b1 = __ballot_sync(FULL, e1);
+            roww = (lane == 2 * k) ? b0 : roww;
+            roww = (lane == 2 * k + 1) ? b1 : roww;
+        }
+        if (__any_sync(FULL, unsure_any)) {  // rare: redo this lane's 32 tests with the exact tree
+            if (unsure_any) {
+                colw = 0u;
+                for (int r = 0; r < 32; ++r) {
+                    const float4 ps = s_rs[r];
+                    const float4 pd = s_rd[r];
+                    const float a = f32_dist(ps.x, ps.y, ps.z, cs.x, cs.y, cs.z);
+                    const float b = f32_dist(pd.x, pd.y, pd.z, cd.x, cd.y, cd.z);
+                    colw |= (fabsf(__fsub_rn(a, b)) <= tau) ? (1u << r) : 0u;
+                }
+            }
+            for (int r = 0; r < 32; ++r) {
+                const uint32_t bal = __ballot_sync(FULL, (colw >> r) & 1u);
+                roww = (lane == r) ? bal : roww;
+            }
+        }
+    } else {
+        for (int r = 0; r < 32; ++r) {
+            const float4 ps = s_rs[r];
+            const float4 pd = s_rd[r];
+            const float a = f32_dist(ps.x, ps.y, ps.z, cs.x, cs.y, cs.z);
+            const float b = f32_dist(pd.x, pd.y, pd.z, cd.x, cd.y, cd.z);
+            const float delta = fabsf(__fsub_rn(a, b));
+            const bool e = delta <= tau, eb = delta <= taub;
+            colw |= e ? (1u << r) : 0u;
+            colb |= eb ? (1u << r) : 0u;
+            const uint32_t bal = __ballot_sync(FULL, e), balb = __ballot_sync(FULL, eb);
+            roww = (lane == r) ? bal : roww;
+            rowb = (lane == r) ? balb : rowb;
         }
     }
+    colw &= okc;
+    roww &= okr;
     uint32_t* bits = ws.bits + p * ws.bits_stride;
     if (rv) bits[(int64_t)r0 * W + J] = roww;
     if (cv) bits[(int64_t)c * W + I] = colw;
     if (I == J && rv)
         for (int w = T; w < W; ++w) bits[(int64_t)r0 * W + w] = 0u;
     if (BASE) {
+        colb &= okc;
+        rowb &= okr;
         uint32_t* bb = ws.bits_base + p * ws.bits_stride;
         if (rv) bb[(int64_t)r0 * W + J] = rowb;
         if (cv) bb[(int64_t)c * W + I] = colb;
@@ -211,99 +319,320 @@ __global__ void __launch_bounds__(256) k_compat(WS ws) {
     }
 }
 
+// Block b of a pair owns block-rows I = b and I = T-1-b (equal work: T+1 tiles); its 8 warps sweep J.
+template <bool BASE>
+__global__ void __launch_bounds__(256) k_compat(WS ws) {
+    __shared__ float4 s_rs[32];
+    __shared__ float4 s_rd[32];
+    __shared__ float4 s_pxy[16];
+    __shared__ float2 s_pz[16];
+    __shared__ float4 s_qxy[16];
+    __shared__ float2 s_qz[16];
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int T = (n + 31) >> 5;
+    const int b = blockIdx.x;
+    if (2 * b >= T) return;
+    const int warp = threadIdx.x >> 5;
+    const float4* s4 = ws.src4 + p * ws.pts_stride;
+    const float4* d4 = ws.dst4 + p * ws.pts_stride;
+    for (int half = 0; half < 2; ++half) {
+        const int I = half == 0 ? b : T - 1 - b;
+        if (half == 1 && I == b) break;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int t = threadIdx.x, r0 = I * 32 + t;
+            const float4 a = r0 < n ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 q = r0 < n ? d4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            s_rs[t] = a;
+            s_rd[t] = q;
+            float* pxy = reinterpret_cast<float*>(s_pxy) + 4 * (t >> 1) + (t & 1);
+            float* qxy = reinterpret_cast<float*>(s_qxy) + 4 * (t >> 1) + (t & 1);
+            pxy[0] = a.x; pxy[2] = a.y;
+            qxy[0] = q.x; qxy[2] = q.y;
+            reinterpret_cast<float*>(s_pz)[t] = a.z;
+            reinterpret_cast<float*>(s_qz)[t] = q.z;
+        }
+        __syncthreads();
+        for (int J = I + warp; J < T; J += 8)
+            compat_tile<BASE>(ws, p, n, W, T, I, J, s_rs, s_rd, s_pxy, s_pz, s_qxy, s_qz);
+    }
+}
+
 // ------------------------------------------------------------------------------------------ a3 SC^2
-// Eq. 2 for the O2 edges (i < j): Ĝ_ij = popcount(row_i AND row_j).  One warp per row i:
-// row_i lives in registers (lane-strided words), the warp walks U_i's set bits j in increasing order, G
-// edges at a time so G·WPL row_j loads are in flight, and reduces each partial with REDUX.  The result
-// (j << 16 | Ĝ_ij) goes to edges[tri_off(i) + rank]; positive weights feed a 256-bin histogram of
-// Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
+// Eq. 2 for every O2 edge (i < j), assembled in row i's rank order.  One warp per row i;
+// U_i's words are enumerated lane-parallel (lane = word, rank = warp prefix of popcounts), one edge per
+// lane per round:
+//   * both endpoints heavy → Ĝ_ij was computed on the tensor cores: gather D[hpos i][hpos j];
+//   * otherwise (the sparse remainder) → popcount(row_i AND row_j): row_i in registers (lane-strided),
+//     G light edges at a time so G·WPL row_j loads are in flight, REDUX per edge.
+// The result (j << 16 | Ĝ_ij) goes to edges[tri_off(i) + rank]; positive weights feed a 256-bin histogram
+// of Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
 constexpr int SC2_WARPS = 8;
 constexpr int SC2_ROWS_PER_BLOCK = 64;
+constexpr int SEL_WARPS = 8;
+constexpr int SEL_ROWS_PER_BLOCK = 64;
+template <int WPL>
+constexpr int sc2_smem_bytes() { return SC2_WARPS * (96 * WPL + 32) * 4; }
+
+// Persistent: warps claim (pair, row) items from a global counter, so the very uneven row costs (a heavy
+// row scans ~|H|/32 D blocks, a light row handles a few dozen sparse edges) balance across the GPU.
+//
+// Per row i the edges j > i (O2, Def. 2) are assembled in rank order from three sources:
+//   (1) i, j both heavy: D[hpos i][hpos j] from the tensor-core block (scan of D row hpos(i));
+//   (2) i or j sparse (degree <= LIST_MAX, compact sorted neighbour list L): Ĝ_ij = |L_j ∩ N(i)| (or
+//       |L_i ∩ N(j)|), one edge per lane, testing list entries against the row bitmap in shared memory
+//       (or against row j's words);
+//   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
+constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
+constexpr int LIST_MAX = 64;
+
+// |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned) against row i's bitmap in
+// shared memory; all list bytes are fetched with independent 16-byte loads first.
+__device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len, const uint32_t* sr) {
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c * 8 < len) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (c * 8 + e < len) {
+                const uint32_t k = (wv[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                cnt += (sr[k >> 5] >> (k & 31)) & 1u;
+            }
+        }
+    }
+    return cnt;
+}
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws) {
+__global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws, int* counter, int maxn, int batch) {
     constexpr int G = 4;
-    __shared__ uint32_t s_row[SC2_WARPS][32 * WPL];
+    // per warp: U_i words [32 WPL], exclusive prefix counts [32 WPL], full row i [32 WPL], L_i [LIST_MAX]
+    extern __shared__ uint32_t s_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* su = s_dyn + warp * (96 * WPL + LIST_MAX / 2);
+    int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
+    uint32_t* sr = su + 64 * WPL;
+    uint16_t* sl = reinterpret_cast<uint16_t*>(su + 96 * WPL);
+    const int64_t total = (int64_t)maxn * batch;
+    while (true) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(counter, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= total) break;
+        const int p = item / maxn, i = item % maxn;
+        const PairDesc d = ws.desc[p];
+        const int n = d.n;
+        if (i >= n) continue;
+        const int W = d.W;
+        const int nchunks = (W + 31) >> 5;
+        const uint32_t* bits = ws.bits + p * ws.bits_stride;
+        const uint32_t* ri = bits + (int64_t)i * W;
+        const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+        const uint16_t* lists = ws.lists + p * ws.lists_stride;
+        const int32_t* hpos = ws.hpos + p * ws.row_stride;
+        uint32_t reg[WPL];
+        int carry = 0;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int w = lane + 32 * k;
+            const uint32_t v = (w < W) ? ri[w] : 0u;
+            reg[k] = v;
+            sr[w] = v;
+            const uint32_t u = (w < W) ? upper_mask(v, w, i) : 0u;
+            const int cnt = __popc(u);
+            const int incl = warp_incl_scan(cnt);
+            su[w] = u;
+            sp[w] = carry + incl - cnt;
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+        const int di = deg_full[i];
+        const bool ilist = di <= LIST_MAX;
+        if (ilist) {
+            for (int t = lane; t < di; t += 32) sl[t] = lists[(int64_t)i * LIST_MAX + t];
+        }
+        __syncwarp();
+        uint32_t* erow = ws.edges + p * ws.edges_stride + tri_off(i, n);
+        const int hi = hpos[i];
+        if (hi >= 0) {
+            // (1) heavy-heavy edges: scan D row hi over heavy columns a > hi (a ascending ⇔ j ascending)
+            const int h = ws.st[p].heavy_h;
+            const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
+            const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
+            for (int a0 = hi + 1; a0 < h; a0 += 128) {
+                int jv[4];
+                uint32_t wv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int a = a0 + 32 * q + lane;
+                    jv[q] = (a < h) ? __ldg(hlist + a) : -1;
+                    wv[q] = (a < h) ? (uint32_t)__ldg(Drow + a) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = jv[q];
+                    if (j >= 0) {
+                        const int w = j >> 5, b = j & 31;
+                        const uint32_t uw = su[w];
+                        if ((uw >> b) & 1u) erow[sp[w] + __popc(uw & ((1u << b) - 1u))] = ((uint32_t)j << 16) | wv[q];
+                    }
+                }
+            }
+        }
+        if (ilist) {
+            // (2a) sparse row: its upper neighbours are L_i[lo..di); one edge per lane
+            int lo = 0;
+            for (int t = lane; t < di; t += 32) lo += (int)sl[t] <= i;
+            lo = __reduce_add_sync(FULL, (unsigned)lo);
+            for (int t = lo + lane; t < di; t += 32) {
+                const int j = sl[t];
+                const int hj = hpos[j];
+                if (hi >= 0 && hj >= 0) continue;  // from D
+                const int dj = deg_full[j];
+                uint32_t cnt = 0;
+                if (dj <= LIST_MAX) {  // |L_j ∩ N(i)|: L_j entries against row i's bitmap (shared memory)
+                    cnt = list_bitmap_count(lists + (int64_t)j * LIST_MAX, dj, sr);
+                } else {  // |L_i ∩ N(j)|: L_i entries against row j's words
+                    const uint32_t* rj = bits + (int64_t)j * W;
+                    for (int q = 0; q < di; ++q) {
+                        const int k = sl[q];
+                        cnt += (__ldg(rj + (k >> 5)) >> (k & 31)) & 1u;
+                    }
+                }
+                erow[t - lo] = ((uint32_t)j << 16) | cnt;
+            }
+        } else {
+            // dense row: enumerate U_i (minus heavy columns if i is heavy) lane-parallel
+            const uint32_t* hmask = ws.heavy_mask + p * (ws.bits_stride / ws.row_stride);
+            for (int c = (i + 1) >> 10; c < nchunks; ++c) {
+                const int w = c * 32 + lane;
+                uint32_t u = (w < W) ? su[w] : 0u;
+                if (hi >= 0 && w < W) u &= ~__ldg(hmask + w);
+                const int rk = (w < W) ? sp[w] : 0;
+                const uint32_t uall = (w < W) ? su[w] : 0u;
+                while (__any_sync(FULL, u != 0u)) {
+                    const bool has = u != 0u;
+                    int j = -1, myr = 0;
+                    bool dense_j = false;
+                    if (has) {
+                        const int b = __ffs(u) - 1;
+                        u &= u - 1u;
+                        j = w * 32 + b;
+                        myr = rk + __popc(uall & ((1u << b) - 1u));
+                        const int dj = deg_full[j];
+                        if (dj <= LIST_MAX) {  // (2b) |L_j ∩ N(i)| against row i's bitmap
+                            erow[myr] = ((uint32_t)j << 16) | list_bitmap_count(lists + (int64_t)j * LIST_MAX, dj, sr);
+                        } else {
+                            dense_j = true;
+                        }
+                    }
+                    // (3) dense-dense: warp-cooperative popcount, G at a time
+                    unsigned lb = __ballot_sync(FULL, dense_j);
+                    while (lb) {
+                        int jj[G], rr[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            int src = -1;
+                            if (lb) {
+                                src = __ffs(lb) - 1;
+                                lb &= lb - 1u;
+                            }
+                            jj[g] = __shfl_sync(FULL, j, src < 0 ? 0 : src);
+                            rr[g] = __shfl_sync(FULL, myr, src < 0 ? 0 : src);
+                            if (src < 0) jj[g] = -1;
+                        }
+                        uint32_t part[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            part[g] = 0u;
+                            if (jj[g] >= 0) {
+                                const uint32_t* rj = bits + (int64_t)jj[g] * W;
+#pragma unroll
+                                for (int k = 0; k < WPL; ++k) {
+                                    const int wk = lane + 32 * k;
+                                    if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            if (jj[g] < 0) break;
+                            const uint32_t tot = __reduce_add_sync(FULL, part[g]);
+                            if (lane == g) erow[rr[g]] = ((uint32_t)jj[g] << 16) | tot;
+                        }
+                    }
+                }
+            }
+        }
+        if (lane == 0) ws.deg[p * ws.row_stride + i] = carry;
+        __syncwarp();
+    }
+}
+
+// Sorted neighbour lists (uint16) of the sparse rows (degree <= LIST_MAX), one warp per row.
+__global__ void __launch_bounds__(256) k_lists(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        if (ws.deg_full[p * ws.row_stride + i] > LIST_MAX) continue;
+        uint16_t* L = lists + (int64_t)i * LIST_MAX;
+        int carry = 0;
+        for (int c = 0; c * 32 < W; ++c) {
+            const int w = c * 32 + lane;
+            uint32_t v = (w < W) ? bits[(int64_t)i * W + w] : 0u;
+            const int cnt = __popc(v);
+            const int incl = warp_incl_scan(cnt);
+            int pos = carry + incl - cnt;
+            while (v) {
+                const int b = __ffs(v) - 1;
+                v &= v - 1u;
+                L[pos++] = (uint16_t)(w * 32 + b);
+            }
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+    }
+}
+
+// Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4) and the
+// edge count E = Σ deg.
+__global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
     __shared__ int s_hist[256];
     __shared__ int s_edges;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
     if (n == 0) return;
-    const int W = d.W;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
     if (threadIdx.x == 0) s_edges = 0;
     __syncthreads();
-    const uint32_t* bits = ws.bits + p * ws.bits_stride;
-    uint32_t* edges = ws.edges + p * ws.edges_stride;
-    const int row0 = blockIdx.x * SC2_ROWS_PER_BLOCK;
-    const int row1 = min(row0 + SC2_ROWS_PER_BLOCK, n);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
     int my_edges = 0;
-    for (int i = row0 + warp; i < row1; i += SC2_WARPS) {
-        const uint32_t* ri = bits + (int64_t)i * W;
-        uint32_t reg[WPL];
-#pragma unroll
-        for (int k = 0; k < WPL; ++k) {
-            const int w = lane + 32 * k;
-            const uint32_t v = (w < W) ? ri[w] : 0u;
-            reg[k] = v;
-            s_row[warp][w] = upper_mask(v, w, i);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        const int dg = ws.deg[p * ws.row_stride + i];
+        my_edges += dg;
+        const uint32_t* e = edges + tri_off(i, n);
+        for (int k = lane; k < dg; k += 32) {
+            const uint32_t w = e[k] & 0xffffu;
+            const int bin = (int)(w >> 7);
+            const unsigned m = __match_any_sync(__activemask(), w ? bin : -1);
+            if (w && lane == __ffs(m) - 1) atomicAdd(&s_hist[bin], __popc(m));
         }
-        __syncwarp();
-        const int64_t base = tri_off(i, n);
-        int rank = 0;
-        uint32_t myval = 0;
-        int w = (i + 1) >> 5;
-        uint32_t word = (w < W) ? s_row[warp][w] : 0u;
-        while (true) {
-            int js[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                while (word == 0u && w + 1 < W) word = s_row[warp][++w];
-                if (word) {
-                    js[g] = w * 32 + (__ffs(word) - 1);
-                    word &= word - 1u;
-                } else {
-                    js[g] = -1;
-                }
-            }
-            if (js[0] < 0) break;
-            uint32_t part[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                part[g] = 0u;
-                if (js[g] >= 0) {
-                    const uint32_t* rj = bits + (int64_t)js[g] * W;
-#pragma unroll
-                    for (int k = 0; k < WPL; ++k) {
-                        const int wk = lane + 32 * k;
-                        if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (js[g] < 0) break;
-                const uint32_t tot = __reduce_add_sync(FULL, part[g]);
-                if (lane == (rank & 31)) myval = ((uint32_t)js[g] << 16) | tot;
-                ++rank;
-                if ((rank & 31) == 0) {
-                    edges[base + rank - 32 + lane] = myval;
-                    const uint32_t wv = myval & 0xffffu;
-                    if (wv) atomicAdd(&s_hist[wv >> 7], 1);
-                }
-            }
-        }
-        const int rem = rank & 31;
-        if (rem && lane < rem) {
-            edges[base + (rank - rem) + lane] = myval;
-            const uint32_t wv = myval & 0xffffu;
-            if (wv) atomicAdd(&s_hist[wv >> 7], 1);
-        }
-        if (lane == 0) ws.deg[p * ws.row_stride + i] = rank;
-        my_edges += rank;
-        __syncwarp();
     }
     if (lane == 0 && my_edges) atomicAdd(&s_edges, my_edges);
     __syncthreads();
@@ -311,6 +640,141 @@ __global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws) {
     for (int b = threadIdx.x; b < 256; b += blockDim.x)
         if (s_hist[b]) atomicAdd(&st->hist_hi[b], s_hist[b]);
     if (threadIdx.x == 0 && s_edges) atomicAdd(&st->edges, s_edges);
+}
+
+// ------------------------------------------------------------------------------------------ a3 heavy split
+// Full degrees (popcount of each bit row) and their sum.
+__global__ void __launch_bounds__(256) k_degree(WS ws) {
+    __shared__ unsigned long long s_sum;
+    __shared__ int s_max;
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    if (threadIdx.x == 0) { s_sum = 0ull; s_max = 0; }
+    __syncthreads();
+    const int W = d.W, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    unsigned mine = 0;
+    int mx = 0;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+        unsigned c = 0;
+        for (int w = lane; w < W; w += 32) c += __popc(bits[(int64_t)i * W + w]);
+        c = __reduce_add_sync(FULL, c);
+        if (lane == 0) ws.deg_full[p * ws.row_stride + i] = (int)c;
+        mine += c;
+        mx = max(mx, (int)c);
+    }
+    if (lane == 0 && mine) { atomicAdd(&s_sum, (unsigned long long)mine); atomicMax(&s_max, mx); }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_sum) { atomicAdd(&ws.st[p].deg_sum, s_sum); atomicMax(&ws.st[p].deg_max, s_max); }
+}
+
+// One block per pair: H = rows with degree >= θ, θ = max(heavy_min_deg, ⌈max degree / 3⌉), raised until
+// |H| <= heavy_cap; |H| < heavy_min_rows ⇒ no tensor-core block.  Ordered compaction (H in index order, so
+// i < j ⇔ hpos(i) < hpos(j)).
+__global__ void __launch_bounds__(1024) k_heavy(WS ws) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry, s_cnt;
+    const int p = blockIdx.x;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int32_t* deg = ws.deg_full + p * ws.row_stride;
+    int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int thr = max(ws.heavy_min_deg, (st->deg_max + 2) / 3);
+    int cnt = 0;
+    for (int it = 0; it < 64; ++it) {
+        if (t == 0) s_cnt = 0;
+        __syncthreads();
+        int c = 0;
+        for (int i = t; i < n; i += 1024) c += deg[i] >= thr;
+        c = __reduce_add_sync(FULL, (unsigned)c);
+        if (lane == 0 && c) atomicAdd(&s_cnt, c);
+        __syncthreads();
+        cnt = s_cnt;
+        __syncthreads();
+        if (cnt <= ws.heavy_cap) break;
+        thr += max(1, thr / 4);
+    }
+    const bool use = ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
+    if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; }
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (use && i < n && deg[i] >= thr) ? 1 : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) hpos[i] = f ? pos : -1;
+        if (f) ws.heavy_list[p * ws.heavy_cap + pos] = i;
+        const unsigned fb = __ballot_sync(FULL, f);
+        if (lane == 0) {
+            const int wi = (r0 + warp * 32) >> 5;
+            if (wi < d.W) ws.heavy_mask[p * (ws.bits_stride / ws.row_stride) + wi] = fb;
+        }
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+}
+
+// X[a][k] = C[H_a][k] as uint8 0/1 for a < |H| rounded up to 256 (zero rows beyond |H|), k < 32 W.
+__global__ void __launch_bounds__(256) k_expand(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int h = ws.st[p].heavy_h;
+    if (h == 0) return;
+    const int W = d.W;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // thread e → (source row i, word w); heavy rows land at X row hpos(i), light rows are skipped
+    const int64_t total = (int64_t)n * W;
+    if (e >= total) return;
+    const int i = (int)(e / W), w = (int)(e % W);
+    const int a = ws.hpos[p * ws.row_stride + i];
+    if (a < 0) return;
+    const uint32_t v = ws.bits[p * ws.bits_stride + (int64_t)i * W + w];
+    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap + 32 * w;
+    uint4 lo, hi4;
+    uint32_t b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t nib = (v >> (4 * q)) & 0xfu;
+        b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+    }
+    lo = make_uint4(b[0], b[1], b[2], b[3]);
+    hi4 = make_uint4(b[4], b[5], b[6], b[7]);
+    reinterpret_cast<uint4*>(X)[0] = lo;
+    reinterpret_cast<uint4*>(X)[1] = hi4;
+}
+
+// Zero rows [h, round_up(h, 256)) of X so the last MMA row tile reads zeros.
+__global__ void __launch_bounds__(256) k_expand_pad(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    if (d.n == 0) return;
+    const int h = ws.st[p].heavy_h;
+    if (h == 0) return;
+    const int hp = (h + 255) / 256 * 256;
+    const int64_t rowbytes = (int64_t)d.W * 32;
+    const int64_t total = (int64_t)(hp - h) * rowbytes / 16;
+    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = h + e / (rowbytes / 16), c = e % (rowbytes / 16);
+        reinterpret_cast<uint4*>(X + r * ws.heavy_Kcap)[c] = make_uint4(0, 0, 0, 0);
+    }
 }
 
 // ------------------------------------------------------------------------------------------ a4 pivots
@@ -356,9 +820,6 @@ __device__ void block_suffix_select(const int* hist, int nb, int K, int lowest, 
     *out_total = total;
     __syncthreads();
 }
-
-constexpr int SEL_WARPS = 8;
-constexpr int SEL_ROWS_PER_BLOCK = 64;
 
 __global__ void __launch_bounds__(256) k_hist_lo(WS ws) {
     __shared__ int s_lo[128];

@@ -3,6 +3,8 @@
 // stream, per-kernel event timing and the launch sequence of the hand-written sm_100a kernels in
 // turboreg_kernels.cuh.  No CPU fallback: every step of the path runs in those kernels.
 // =====================================================================================================
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -11,10 +13,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "turboreg.h"
 #include "turboreg_kernels.cuh"
+#include "turboreg_sc2_mma.cuh"
 
 static_assert(sizeof(trk::DevResult) == sizeof(turboreg_result), "result layout");
 
@@ -23,7 +27,13 @@ namespace {
 enum KernelId {
     KID_INGEST = 0,
     KID_COMPAT,
+    KID_DEGREE,
+    KID_HEAVY,
+    KID_LISTS,
+    KID_EXPAND,
+    KID_SC2_MMA,
     KID_SC2,
+    KID_HIST_HI,
     KID_HIST_LO,
     KID_SEL_COUNT,
     KID_SEL_SCAN,
@@ -34,14 +44,23 @@ enum KernelId {
     KID_FINALIZE,
     KID_COUNT
 };
-const char* kKernelNames[KID_COUNT] = {"k_ingest",      "k_compat",     "k_sc2",   "k_hist_lo",
+const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_lists",
+                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_hist_hi",     "k_hist_lo",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
-                                       "k_kabsch",      "k_score",      "k_finalize"};
+                                       "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
+constexpr int HEAVY_CAP_MAX = 2048;
+
+int mma_tiles_for(int cap) {
+    const int RB = cap / trk::MMA_BM, CB = cap / trk::MMA_BN;
+    int t = 0;
+    for (int rb = 0; rb < RB; ++rb) t += CB - rb / 2;
+    return t;
+}
 
 }  // namespace
 
@@ -57,6 +76,7 @@ struct turboreg_ctx {
     trk::PairDesc* d_desc = nullptr;
     void* d_results = nullptr;
     float* d_inputs = nullptr;  // staging for host inputs: 2 × max_batch × max_n × 3 floats
+    int* d_counters = nullptr;  // per-call work-queue counters
     // pinned host staging
     trk::PairDesc* h_desc = nullptr;
     turboreg_result* h_results = nullptr;
@@ -72,6 +92,11 @@ struct turboreg_ctx {
     double k_ms[KID_COUNT] = {0};
     int64_t k_launches[KID_COUNT] = {0};
     int64_t launches = 0;
+    // SC^2 heavy/light split
+    int32_t heavy_cap_alloc = 0;
+    CUtensorMap tmX;
+    bool tmX_ok = false;
+    int32_t opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
 };
 
 namespace {
@@ -126,7 +151,8 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists;
+    const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
         {sizeof(trk::PairState) * B, &p_st},
@@ -144,6 +170,14 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(float) * 16 * KC * B, &p_hyp},
         {sizeof(turboreg_result) * B, &p_res},
         {sizeof(float) * 6 * N * B, &p_in},
+        {sizeof(int32_t) * N * B, &p_degf},
+        {sizeof(int32_t) * N * B, &p_hpos},
+        {(size_t)(cap * Kcap * B), &p_X},
+        {sizeof(uint16_t) * (size_t)(cap * cap * B), &p_D},
+        {sizeof(int32_t) * (size_t)(cap * B), &p_hl},
+        {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
+        {sizeof(int) * 16, &p_ctr},
+        {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     size_t total = 0;
@@ -177,10 +211,43 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.res = p_res;
     c->d_results = p_res;
     c->d_inputs = static_cast<float*>(p_in);
+    w.deg_full = static_cast<int32_t*>(p_degf);
+    w.hpos = static_cast<int32_t*>(p_hpos);
+    w.heavy_X = static_cast<uint8_t*>(p_X);
+    w.heavy_X_stride = cap * Kcap;
+    w.heavy_Kcap = (int32_t)Kcap;
+    w.heavy_D = static_cast<uint16_t*>(p_D);
+    w.heavy_D_stride = cap * cap;
+    w.heavy_list = static_cast<int32_t*>(p_hl);
+    w.heavy_mask = static_cast<uint32_t*>(p_hm);
+    c->d_counters = static_cast<int*>(p_ctr);
+    w.lists = static_cast<uint16_t*>(p_lists);
+    w.lists_stride = N * trk::LIST_MAX;
+    // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle
+    c->tmX_ok = false;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && encode) {
+        const cuuint64_t dims[3] = {(cuuint64_t)Kcap, (cuuint64_t)cap, (cuuint64_t)B};
+        const cuuint64_t strides[2] = {(cuuint64_t)Kcap, (cuuint64_t)(Kcap * cap)};
+        const cuuint32_t box[3] = {trk::MMA_BK, trk::MMA_BM, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode(&c->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p_X, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        c->tmX_ok = (r == CUDA_SUCCESS);
+    }
+    cudaGetLastError();
     return TURBOREG_OK;
 }
 
 void set_ws_params(turboreg_ctx* c) {
+    c->ws.heavy_cap = c->opt_heavy_cap > 0 ? std::min(c->opt_heavy_cap, c->heavy_cap_alloc) : c->heavy_cap_alloc;
+    c->ws.heavy_min_rows = c->opt_heavy_min_rows;
+    c->ws.heavy_min_deg = c->opt_heavy_min_deg;
+    c->ws.sc2_path = (c->opt_sc2_path == 0 && !c->tmX_ok) ? 1 : c->opt_sc2_path;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -246,30 +313,56 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     const int Wb = words_per_row(std::max(maxn_batch, 1));
     const unsigned B = (unsigned)batch;
     CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
+    CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 16, s));
     if (mode == RUN_FULL) {
         CK(L.run(KID_INGEST, [&] {
             trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
         }));
         const int T = (maxn_batch + 31) / 32;
-        const int64_t ntiles = (int64_t)T * (T + 1) / 2;
         CK(L.run(KID_COMPAT, [&] {
-            const dim3 g((unsigned)((ntiles + 7) / 8), B);
+            const dim3 g((unsigned)((T + 1) / 2), B);
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws);
             else trk::k_compat<false><<<g, 256, 0, s>>>(ws);
         }));
     }
     const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
+    CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
+    CK(L.run(KID_LISTS, [&] { trk::k_lists<<<grow, 256, 0, s>>>(ws); }));
+    if (ws.sc2_path != 1) {
+        CK(L.run(KID_EXPAND, [&] {
+            const int64_t total = (int64_t)maxn_batch * Wb;
+            trk::k_expand<<<dim3((unsigned)((total + 255) / 256), B), 256, 0, s>>>(ws);
+            trk::k_expand_pad<<<dim3(64, B), 256, 0, s>>>(ws);
+        }));
+        CK(L.run(KID_SC2_MMA, [&] {
+            if (ws.sc2_path == 2) {
+                const unsigned g = (unsigned)(ws.heavy_cap / 64);
+                trk::k_sc2_dp4a<<<dim3(g, g, B), 256, 0, s>>>(ws);
+            } else {
+                trk::k_sc2_mma<<<dim3((unsigned)mma_tiles_for(ws.heavy_cap), B), trk::MMA_THREADS, trk::MMA_SMEM_BYTES,
+                                 s>>>(c->tmX, ws);
+            }
+        }));
+    }
     const int wpl = (Wb + 31) / 32;
-    CK(L.run(KID_SC2, [&] {
-        if (wpl <= 1) trk::k_sc2<1><<<grow, 256, 0, s>>>(ws);
-        else if (wpl <= 2) trk::k_sc2<2><<<grow, 256, 0, s>>>(ws);
-        else if (wpl <= 4) trk::k_sc2<4><<<grow, 256, 0, s>>>(ws);
-        else if (wpl <= 5) trk::k_sc2<5><<<grow, 256, 0, s>>>(ws);
-        else if (wpl <= 8) trk::k_sc2<8><<<grow, 256, 0, s>>>(ws);
-        else if (wpl <= 16) trk::k_sc2<16><<<grow, 256, 0, s>>>(ws);
-        else trk::k_sc2<32><<<grow, 256, 0, s>>>(ws);
-    }));
+    {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+        const dim3 gp((unsigned)(nsm * trk::SC2_PERSIST_BLOCKS_PER_SM));
+        int* ctr = c->d_counters;
+        CK(L.run(KID_SC2, [&] {
+            if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws, ctr, maxn_batch, batch);
+            else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws, ctr, maxn_batch, batch);
+            else if (wpl <= 4) trk::k_sc2<4><<<gp, 256, trk::sc2_smem_bytes<4>(), s>>>(ws, ctr, maxn_batch, batch);
+            else if (wpl <= 5) trk::k_sc2<5><<<gp, 256, trk::sc2_smem_bytes<5>(), s>>>(ws, ctr, maxn_batch, batch);
+            else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws, ctr, maxn_batch, batch);
+            else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws, ctr, maxn_batch, batch);
+            else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws, ctr, maxn_batch, batch);
+        }));
+    }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
+    CK(L.run(KID_HIST_HI, [&] { trk::k_hist_hi<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HIST_LO, [&] { trk::k_hist_lo<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_COUNT, [&] { trk::k_select_count<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_SCAN, [&] { trk::k_select_scan<<<B, 1024, 0, s>>>(ws); }));
@@ -325,8 +418,11 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     c->max_n = max_n;
     c->max_batch = max_batch;
     c->Wmax = words_per_row(max_n);
+    c->heavy_cap_alloc = (int32_t)std::max<int64_t>(256, std::min<int64_t>(round_up(max_n, 256), HEAVY_CAP_MAX));
     turboreg_status st = TURBOREG_OK;
-    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    // A blocking stream: it orders itself with the legacy default stream, so inputs produced there (e.g. by
+    // torch's default stream) are complete before our kernels read them.
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreate(&c->own_stream) != cudaSuccess) {
         st = TURBOREG_ERR_CUDA;
     }
     if (st == TURBOREG_OK) st = alloc_ws(c);
@@ -341,7 +437,39 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
         return st;
     }
     set_ws_params(c);
+    if (cudaFuncSetAttribute(trk::k_sc2_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::MMA_SMEM_BYTES) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<16>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        turboreg_destroy(c);
+        return TURBOREG_ERR_CUDA;
+    }
     *out = c;
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t value) {
+    if (!c || !name) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const std::string k(name);
+    if (k == "sc2_path") {
+        if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_sc2_path = (int32_t)value;
+    } else if (k == "heavy_min_rows") {
+        if (value < 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_heavy_min_rows = (int32_t)value;
+    } else if (k == "heavy_min_degree") {
+        if (value < 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_heavy_min_deg = (int32_t)value;
+    } else if (k == "heavy_cap") {
+        if (value < 0 || value % 256 || value > c->heavy_cap_alloc) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_heavy_cap = (int32_t)value;
+    } else {
+        return TURBOREG_ERR_INVALID_ARGUMENT;
+    }
+    set_ws_params(c);
     return TURBOREG_OK;
 }
 
@@ -356,6 +484,7 @@ turboreg_status turboreg_set_params(turboreg_ctx* c, const turboreg_params* p) {
         cudaDeviceSynchronize();
         turboreg_status st = alloc_ws(c);
         if (st != TURBOREG_OK) return st;
+        set_ws_params(c);
     }
     return TURBOREG_OK;
 }
@@ -545,7 +674,8 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
             int64_t* o = static_cast<int64_t*>(dst);
             const int64_t vals[16] = {n, W, st.edges, st.epos, st.alpha, st.c_gt, st.need, st.npiv,
-                                      st.nonfinite, st.b1, st.above, st.edges_base, 0, 0, 0, 0};
+                                      st.nonfinite, st.b1, st.above, st.edges_base, st.heavy_h, st.heavy_thr,
+                                      (int64_t)st.deg_sum, 0};
             std::memcpy(o, vals, sizeof(vals));
             return TURBOREG_OK;
         }

@@ -209,3 +209,66 @@ def test_full_size_batch_sampled_parity(tr_mod):
         assert res[p]["status"] == 0
         assert synth.rotation_error_deg(res[p]["R"].reshape(3, 3), insts[p]["R"]) <= 5
         assert synth.translation_error(res[p]["t"], insts[p]["t"]) <= 0.1
+
+
+@pytest.mark.parametrize("path,min_rows", [(0, 1), (0, 128), (1, 128), (2, 1)])
+@pytest.mark.parametrize("key,n", [("A", None), ("B", 1500), ("D", 2100), ("C", None)])
+def test_sc2_paths_agree_with_oracle(tr_mod, path, min_rows, key, n):
+    # tensor-core dense block (path 0), popcount only (1), CUDA-core dp4a dense block (2): identical Ĝ
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=1, n=n)
+    nn = inst["src"].shape[0]
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn)
+    tr.set_option("sc2_path", path)
+    tr.set_option("heavy_min_rows", min_rows)
+    tr.set_option("heavy_min_degree", 1 if min_rows == 1 else 32)
+    res = tr.register(inst["src"], inst["dst"])
+    from paper_2507_01439_b200._binding import I_STATE
+
+    st = tr.intermediate(0, I_STATE)
+    if path == 1:
+        assert st["heavy_h"] == 0
+    elif min_rows == 1:
+        assert st["heavy_h"] > 0
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+def test_sc2_heavy_block_on_dense_injected_graph(tr_mod):
+    # a graph whose heavy block spans several 128×256 MMA tiles plus a ragged edge
+    n = 900
+    C = synth.erdos_renyi(n, 0.04, 77)
+    rng = np.random.default_rng(1)
+    dense = rng.choice(n, 700, replace=False)
+    for a in dense:
+        row = dense[rng.random(700) < 0.7]
+        C[a, row] = 1
+        C[row, a] = 1
+    np.fill_diagonal(C, 0)
+    tr = tr_mod(0.01, 500, 3, 0.1, max_n=n)
+    tr.set_option("heavy_min_rows", 1)
+    tr.pgs_from_adjacency(C)
+    from paper_2507_01439_b200._binding import I_CLIQUES, I_SC2, I_STATE
+
+    assert tr.intermediate(0, I_STATE)["heavy_h"] > 256
+    assert (tr.intermediate(0, I_SC2) == oracle.sc2(C)).all()
+    O = oracle.o2(oracle.sc2(C))
+    ref, _ = oracle.pgs(O, oracle.select_pivots(O, 500), 3)
+    cl = tr.intermediate(0, I_CLIQUES)
+    assert sorted(map(tuple, cl[cl[:, 0] >= 0].tolist())) == sorted(map(tuple, ref.tolist()))
+
+
+@pytest.mark.parametrize("scale,tau", [(1.5, 0.5), (1.5, float(np.float32(0.5 * np.sqrt(2)))),
+                                       (1.25, float(np.float32(0.25 * np.sqrt(5)))), (1.001, 1e-3)])
+def test_compat_adversarial_threshold_ties(tr_mod, scale, tau):
+    # lattice points: thousands of pairs sit exactly on (or one rounding away from) the threshold, the worst
+    # case for the certified sqrt-free filter; C must still equal the oracle's float32 tree bit for bit
+    g = np.stack(np.meshgrid(np.arange(9), np.arange(9), np.arange(8), indexing="ij"), -1).reshape(-1, 3)
+    src = g.astype(np.float32)
+    dst = (g * scale + np.array([0.25, -3.0, 7.0])).astype(np.float32)
+    n = src.shape[0]
+    tr = tr_mod(tau, 50, 2, 0.01, max_n=n)
+    tr.register(src, dst)
+    ref, e, near, _ = oracle.compat(src, dst, tau)
+    assert near > 100  # the case really is adversarial
+    got = tr.bits(0)
+    assert (got == ref).all(), int((got != ref).sum())
