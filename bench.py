@@ -97,13 +97,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ workload
-def make_inputs(rank, pairs, n=None):
+def make_inputs(rank, pairs, n=None, world=1):
+    """This rank's shard of the configs[4] sweep: global pairs shard_range(world·pairs, world, rank)."""
+    from paper_2507_01439_b200.sharding import shard_range
+
     n = n or CFG.n
+    b, e = shard_range(world * pairs, world, rank)
+    assert e - b == pairs
     src = np.empty((pairs * n, 3), np.float32)
     dst = np.empty((pairs * n, 3), np.float32)
     gts = []
     for p in range(pairs):
-        inst = synth.workload_instance(CFG, pair=rank * pairs + p, n=n)
+        inst = synth.workload_instance(CFG, pair=b + p, n=n)
         src[p * n:(p + 1) * n] = inst["src"]
         dst[p * n:(p + 1) * n] = inst["dst"]
         gts.append((inst["R"], inst["t"]))
@@ -186,7 +191,7 @@ def run_cuda(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     pairs = args.pairs
     n = CFG.n
-    src_h, dst_h, gts = make_inputs(rank, pairs)
+    src_h, dst_h, gts = make_inputs(rank, pairs, world=world)
     off = (np.arange(pairs) * n).astype(np.int64)
     nn = np.full(pairs, n, np.int32)
     src_d = torch.from_numpy(src_h).to(dev)
@@ -278,9 +283,10 @@ def run_cuda(args, rank, world, local_rank):
 
     # gather per-pair results (the only collective: NCCL all_gather of fixed-size records, outside timing)
     if world > 1:
-        gathered = [torch.zeros_like(out_d) for _ in range(world)]
-        dist.all_gather(gathered, out_d)
-        all_ok = sum(int((g.cpu().numpy().view(RESULT_DTYPE)["status"] == 0).sum()) for g in gathered)
+        from paper_2507_01439_b200.sharding import gather_results
+
+        allres = gather_results(out_d, world * pairs)
+        all_ok = int((allres["status"] == 0).sum())
     else:
         all_ok = int((res["status"] == 0).sum())
 

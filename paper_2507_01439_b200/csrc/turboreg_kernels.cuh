@@ -192,15 +192,18 @@ __device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
 __device__ __forceinline__ uint32_t f2_lo(f2_t v) { return (uint32_t)v; }
 __device__ __forceinline__ uint32_t f2_hi(f2_t v) { return (uint32_t)(v >> 32); }
 
-// Filter decision for one test from its float32 bit patterns (all compared quantities but q are >= 0, and
-// for non-negative IEEE floats integer order is float order): returns 1 edge, 0 no edge, 2 unsure.
-__device__ __forceinline__ uint32_t filter_decide(uint32_t Sb, uint32_t qb, uint32_t Tqb, uint32_t s_lo_b,
-                                                  uint32_t s_hi_b, bool* unsure) {
-    const bool sure_in = Sb < s_lo_b;
-    const bool sure_q = (Sb > s_hi_b) && ((qb & 0x7fffffffu) > Tqb);
-    const bool qle0 = (int32_t)qb <= 0;  // q <= 0 (q is finite for finite inputs)
-    *unsure = !(sure_in || sure_q);
-    return (sure_in || (sure_q && qle0)) ? 1u : 0u;
+// Warp-level 32×32 bit-matrix transpose: lane l holds row l (bit b = column b); returns column l.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t masks[5] = {0xffff0000u, 0xff00ff00u, 0xf0f0f0f0u, 0xccccccccu, 0xaaaaaaaau};
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int sft = 16 >> st;
+        const uint32_t m = masks[st];
+        const uint32_t y = __shfl_xor_sync(FULL, x, sft);
+        x = (lane & sft) ? ((x & m) | ((y >> sft) & ~m)) : ((x & ~m) | ((y << sft) & m));
+    }
+    return x;
 }
 
 // One 32×32 tile (I, J >= I) by one warp; the block's 32 row points are staged in shared memory, packed
@@ -235,11 +238,16 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
         const f2_t m2t2x2 = f2_pack(m2t2, m2t2), t4x2 = f2_pack(t4, t4);
         const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), c19 = f2_pack(0x1p-19f, 0x1p-19f);
         const f2_t mone = f2_pack(-1.0f, -1.0f);
-        const uint32_t s_hi_b = __float_as_uint(__fmul_rn(t2, 1.0f + 0x1p-16f));
-        const uint32_t s_lo_b = __float_as_uint(__fmul_rn(t2, 1.0f - 0x1p-16f));
         const f2_t ncx = f2_pack(-cs.x, -cs.x), ncy = f2_pack(-cs.y, -cs.y), ncz = f2_pack(-cs.z, -cs.z);
         const f2_t ndx = f2_pack(-cd.x, -cd.x), ndy = f2_pack(-cd.y, -cd.y), ndz = f2_pack(-cd.z, -cd.z);
-        bool unsure_any = false;
+        const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
+        const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
+        const f2_t nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
+        // Sign-bit algebra per test (bit 31 of each float word):
+        //   a = S − s_lo  (< 0 ⇔ sure edge),  c = s_hi − S  (< 0 ⇔ S > s_hi),
+        //   b = |q| − Tq  computed as (−Tq) + |q| ... sign set ⇔ |q| < Tq, so sure_q ⇔ ~b & c,
+        //   edge = a | (sure_q & q<0),  all-sure accumulator &= a | sure_q.
+        uint32_t sacc = 0xffffffffu;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const float4 P = s_pxy[k];
@@ -256,16 +264,22 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
             const f2_t D = f2_fma(B, mone, A);
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t Tq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, c19));
-            bool u0, u1;
-            const uint32_t e0 = filter_decide(f2_lo(S), f2_lo(q), f2_lo(Tq), s_lo_b, s_hi_b, &u0);
-            const uint32_t e1 = filter_decide(f2_hi(S), f2_hi(q), f2_hi(Tq), s_lo_b, s_hi_b, &u1);
-            unsure_any |= u0 | u1;
-            colw |= (e0 << (2 * k)) | (e1 << (2 * k + 1));
-            const uint32_t b0 = __ballot_sync(FULL, e0), b1 = __ballot_sync(FULL, e1);
-            roww = (lane == 2 * k) ? b0 : roww;
-            roww = (lane == 2 * k + 1) ? b1 : roww;
+            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
+            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
+            const f2_t a = f2_add(S, ns_lo2);
+            const f2_t cc = f2_fma(S, mone, s_hi2);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t av = h ? f2_hi(a) : f2_lo(a), bv = h ? f2_hi(b) : f2_lo(b);
+                const uint32_t cv2 = h ? f2_hi(cc) : f2_lo(cc), qv = h ? f2_hi(q) : f2_lo(q);
+                const uint32_t sq = ~bv & cv2;        // sure_q in bit 31 (|q| > Tq and S > s_hi)
+                const uint32_t e = av | (sq & qv);    // edge in bit 31
+                sacc &= av | sq;                      // bit 31 stays set while every test is decided
+                colw = __funnelshift_l(e, colw, 1);   // colw = colw << 1 | e >> 31 (bit-reversed order)
+            }
         }
+        colw = __brev(colw);
+        const bool unsure_any = (int32_t)sacc >= 0;
         if (__any_sync(FULL, unsure_any)) {  // rare: redo this lane's 32 tests with the exact tree
             if (unsure_any) {
                 colw = 0u;
@@ -277,11 +291,8 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
                     colw |= (fabsf(__fsub_rn(a, b)) <= tau) ? (1u << r) : 0u;
                 }
             }
-            for (int r = 0; r < 32; ++r) {
-                const uint32_t bal = __ballot_sync(FULL, (colw >> r) & 1u);
-                roww = (lane == r) ? bal : roww;
-            }
         }
+        roww = transpose32(colw);
     } else {
         for (int r = 0; r < 32; ++r) {
             const float4 ps = s_rs[r];
