@@ -47,7 +47,9 @@ struct PairState {
     int32_t heavy_thr;  // degree threshold that defined H
     unsigned long long deg_sum;  // Σ_i deg(i) = 2E
     int32_t deg_max;             // max_i deg(i)
-    int32_t pad[1];
+    int32_t n_light;             // rows with a list and not heavy (k_sc2_light)
+    int32_t n_dense;             // the other rows (k_sc2)
+    int32_t pad[3];
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
@@ -80,6 +82,8 @@ struct WS {
     int32_t* hpos;        // [n] position in H or -1
     int32_t* heavy_list;  // [cap] H in index order
     uint16_t* lists;      // [n][LIST_MAX] sorted neighbour lists of rows with degree <= LIST_MAX
+    int32_t* light_list;  // [n] sparse non-heavy rows, index order
+    int32_t* dense_list;  // [n] all other rows, index order
     int64_t lists_stride;
     uint32_t* heavy_mask; // [W] bitset of H
     uint8_t* heavy_X;     // [cap][Kcap] uint8 rows of C restricted to H
@@ -88,7 +92,7 @@ struct WS {
     int32_t heavy_cap;    // max |H| (multiple of 256)
     uint16_t* heavy_D;    // [cap][cap] X X^T
     int64_t heavy_D_stride;
-    int32_t heavy_min_rows, heavy_min_deg, sc2_path;
+    int32_t heavy_min_rows, heavy_min_deg, sc2_path, sc2_variant;
     float tau, tau_base, thr;
     int32_t k1, k2, mode;
 };
@@ -386,8 +390,11 @@ constexpr int SC2_WARPS = 8;
 constexpr int SC2_ROWS_PER_BLOCK = 64;
 constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 64;
+constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
 template <int WPL>
-constexpr int sc2_smem_bytes() { return SC2_WARPS * (96 * WPL + 32) * 4; }
+constexpr int sc2_warp_words() { return 96 * WPL + LIST_MAX / 2 + 32 * WPL; }
+template <int WPL>
+constexpr int sc2_smem_bytes() { return SC2_WARPS * sc2_warp_words<WPL>() * 4; }
 
 // Persistent: warps claim (pair, row) items from a global counter, so the very uneven row costs (a heavy
 // row scans ~|H|/32 D blocks, a light row handles a few dozen sparse edges) balance across the GPU.
@@ -399,50 +406,57 @@ constexpr int sc2_smem_bytes() { return SC2_WARPS * (96 * WPL + 32) * 4; }
 //       (or against row j's words);
 //   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
 constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
-constexpr int LIST_MAX = 64;
+constexpr int SC2_BLOCKS_PER_PAIR = 32;  // 256 warps stride over a pair's dense rows
+constexpr int SC2_CLAIM = 4;
 
-// |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned) against row i's bitmap in
-// shared memory; all list bytes are fetched with independent 16-byte loads first.
+// |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned, zero padded) against row
+// i's bitmap in shared memory.  Entries past len are zeros, so a chunk is processed whole and the pad's
+// bit 0 tests are subtracted once (row i's own bit 0 is read once).
 __device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len, const uint32_t* sr) {
+    const int nch = (len + 7) >> 3;
     uint4 v[LIST_MAX / 8];
 #pragma unroll
     for (int c = 0; c < LIST_MAX / 8; ++c)
-        v[c] = (c * 8 < len) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
     uint32_t cnt = 0;
 #pragma unroll
     for (int c = 0; c < LIST_MAX / 8; ++c) {
-        const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            if (c * 8 + e < len) {
-                const uint32_t k = (wv[e >> 1] >> (16 * (e & 1))) & 0xffffu;
-                cnt += (sr[k >> 5] >> (k & 31)) & 1u;
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t k0 = wv[e] & 0xffffu, k1 = wv[e] >> 16;
+                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
             }
         }
     }
-    return cnt;
+    return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws, int* counter, int maxn, int batch) {
+__global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws, int* counter, int maxn, int batch) {
     constexpr int G = 4;
-    // per warp: U_i words [32 WPL], exclusive prefix counts [32 WPL], full row i [32 WPL], L_i [LIST_MAX]
+    constexpr int QCAP = 32 * WPL;  // light-edge queue of a dense row (one entry per word is enough per round)
+    // per warp: U_i words [32 WPL], exclusive prefix counts [32 WPL], full row i [32 WPL], L_i [LIST_MAX],
+    // queue (j, rank) [QCAP]
     extern __shared__ uint32_t s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* su = s_dyn + warp * (96 * WPL + LIST_MAX / 2);
+    uint32_t* su = s_dyn + warp * sc2_warp_words<WPL>();
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
     uint16_t* sl = reinterpret_cast<uint16_t*>(su + 96 * WPL);
-    const int64_t total = (int64_t)maxn * batch;
-    while (true) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(counter, 1);
-        item = __shfl_sync(FULL, item, 0);
-        if (item >= total) break;
-        const int p = item / maxn, i = item % maxn;
-        const PairDesc d = ws.desc[p];
-        const int n = d.n;
-        if (i >= n) continue;
+    uint32_t* sq = su + 96 * WPL + LIST_MAX / 2;
+    (void)counter;
+    (void)maxn;
+    (void)batch;
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int nd = ws.st[p].n_dense;
+    const int nw = gridDim.x * SC2_WARPS;
+    for (int kq = blockIdx.x * SC2_WARPS + warp; kq < nd; kq += nw) {
+        const int i = ws.dense_list[p * ws.row_stride + kq];
         const int W = d.W;
         const int nchunks = (W + 31) >> 5;
         const uint32_t* bits = ws.bits + p * ws.bits_stride;
@@ -450,100 +464,96 @@ __global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws, int* counter, int
         const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
         const uint16_t* lists = ws.lists + p * ws.lists_stride;
         const int32_t* hpos = ws.hpos + p * ws.row_stride;
+        const int di = deg_full[i];
+        const int hi = hpos[i];
+        const bool ilist = di <= LIST_MAX;
+        uint32_t* erow = ws.edges + p * ws.edges_stride + tri_off(i, n);
         uint32_t reg[WPL];
-        int carry = 0;
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             const int w = lane + 32 * k;
             const uint32_t v = (w < W) ? ri[w] : 0u;
             reg[k] = v;
             sr[w] = v;
-            const uint32_t u = (w < W) ? upper_mask(v, w, i) : 0u;
-            const int cnt = __popc(u);
-            const int incl = warp_incl_scan(cnt);
-            su[w] = u;
-            sp[w] = carry + incl - cnt;
-            carry += __shfl_sync(FULL, incl, 31);
         }
-        const int di = deg_full[i];
-        const bool ilist = di <= LIST_MAX;
-        if (ilist) {
-            for (int t = lane; t < di; t += 32) sl[t] = lists[(int64_t)i * LIST_MAX + t];
-        }
-        __syncwarp();
-        uint32_t* erow = ws.edges + p * ws.edges_stride + tri_off(i, n);
-        const int hi = hpos[i];
-        if (hi >= 0) {
-            // (1) heavy-heavy edges: scan D row hi over heavy columns a > hi (a ascending ⇔ j ascending)
-            const int h = ws.st[p].heavy_h;
-            const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
-            const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
-            for (int a0 = hi + 1; a0 < h; a0 += 128) {
-                int jv[4];
-                uint32_t wv[4];
+        int carry = 0;
+        (void)ilist;
+        {
+            // dense (or heavy) row: U_i words and rank prefixes in shared memory
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int a = a0 + 32 * q + lane;
-                    jv[q] = (a < h) ? __ldg(hlist + a) : -1;
-                    wv[q] = (a < h) ? (uint32_t)__ldg(Drow + a) : 0u;
-                }
+            for (int k = 0; k < WPL; ++k) {
+                const int w = lane + 32 * k;
+                const uint32_t u = (w < W) ? upper_mask(reg[k], w, i) : 0u;
+                const int cnt = __popc(u);
+                const int incl = warp_incl_scan(cnt);
+                su[w] = u;
+                sp[w] = carry + incl - cnt;
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            __syncwarp();
+            if (hi >= 0) {
+                // (1) heavy-heavy edges: scan D row hi over heavy columns a > hi (a ascending ⇔ j ascending)
+                const int h = ws.st[p].heavy_h;
+                const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
+                const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
+                for (int a0 = hi + 1; a0 < h; a0 += 128) {
+                    int jv[4];
+                    uint32_t wv[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int j = jv[q];
-                    if (j >= 0) {
-                        const int w = j >> 5, b = j & 31;
-                        const uint32_t uw = su[w];
-                        if ((uw >> b) & 1u) erow[sp[w] + __popc(uw & ((1u << b) - 1u))] = ((uint32_t)j << 16) | wv[q];
+                    for (int q = 0; q < 4; ++q) {
+                        const int a = a0 + 32 * q + lane;
+                        jv[q] = (a < h) ? __ldg(hlist + a) : -1;
+                        wv[q] = (a < h) ? (uint32_t)__ldg(Drow + a) : 0u;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = jv[q];
+                        if (j >= 0) {
+                            const int w = j >> 5, b = j & 31;
+                            const uint32_t uw = su[w];
+                            if ((uw >> b) & 1u)
+                                erow[sp[w] + __popc(uw & ((1u << b) - 1u))] = ((uint32_t)j << 16) | wv[q];
+                        }
                     }
                 }
             }
-        }
-        if (ilist) {
-            // (2a) sparse row: its upper neighbours are L_i[lo..di); one edge per lane
-            int lo = 0;
-            for (int t = lane; t < di; t += 32) lo += (int)sl[t] <= i;
-            lo = __reduce_add_sync(FULL, (unsigned)lo);
-            for (int t = lo + lane; t < di; t += 32) {
-                const int j = sl[t];
-                const int hj = hpos[j];
-                if (hi >= 0 && hj >= 0) continue;  // from D
-                const int dj = deg_full[j];
-                uint32_t cnt = 0;
-                if (dj <= LIST_MAX) {  // |L_j ∩ N(i)|: L_j entries against row i's bitmap (shared memory)
-                    cnt = list_bitmap_count(lists + (int64_t)j * LIST_MAX, dj, sr);
-                } else {  // |L_i ∩ N(j)|: L_i entries against row j's words
-                    const uint32_t* rj = bits + (int64_t)j * W;
-                    for (int q = 0; q < di; ++q) {
-                        const int k = sl[q];
-                        cnt += (__ldg(rj + (k >> 5)) >> (k & 31)) & 1u;
-                    }
-                }
-                erow[t - lo] = ((uint32_t)j << 16) | cnt;
-            }
-        } else {
-            // dense row: enumerate U_i (minus heavy columns if i is heavy) lane-parallel
+            // remaining edges: queue sparse-neighbour edges, popcount dense-dense ones
             const uint32_t* hmask = ws.heavy_mask + p * (ws.bits_stride / ws.row_stride);
+            int nq = 0;  // queued sparse-neighbour edges (warp-uniform)
             for (int c = (i + 1) >> 10; c < nchunks; ++c) {
                 const int w = c * 32 + lane;
                 uint32_t u = (w < W) ? su[w] : 0u;
                 if (hi >= 0 && w < W) u &= ~__ldg(hmask + w);
                 const int rk = (w < W) ? sp[w] : 0;
-                const uint32_t uall = (w < W) ? su[w] : 0u;
+                const uint32_t uall = u | ((w < W) ? su[w] : 0u);
                 while (__any_sync(FULL, u != 0u)) {
                     const bool has = u != 0u;
                     int j = -1, myr = 0;
-                    bool dense_j = false;
+                    bool dense_j = false, sparse_j = false;
                     if (has) {
                         const int b = __ffs(u) - 1;
                         u &= u - 1u;
                         j = w * 32 + b;
                         myr = rk + __popc(uall & ((1u << b) - 1u));
-                        const int dj = deg_full[j];
-                        if (dj <= LIST_MAX) {  // (2b) |L_j ∩ N(i)| against row i's bitmap
-                            erow[myr] = ((uint32_t)j << 16) | list_bitmap_count(lists + (int64_t)j * LIST_MAX, dj, sr);
-                        } else {
-                            dense_j = true;
+                        dense_j = deg_full[j] > LIST_MAX;
+                        sparse_j = !dense_j;
+                    }
+                    const unsigned sb = __ballot_sync(FULL, sparse_j);
+                    if (sparse_j) {
+                        const int slot = nq + __popc(sb & ((1u << lane) - 1u));
+                        sq[slot] = ((uint32_t)j << 16) | (uint32_t)myr;  // rank < 65536 for n <= 32768
+                    }
+                    nq += __popc(sb);
+                    if (nq > QCAP - 32) {
+                        __syncwarp();
+                        for (int t = lane; t < nq; t += 32) {  // (2b) one queued edge per lane
+                            const uint32_t e = sq[t];
+                            const int jq = (int)(e >> 16);
+                            erow[e & 0xffffu] = ((uint32_t)jq << 16) |
+                                list_bitmap_count(lists + (int64_t)jq * LIST_MAX, deg_full[jq], sr);
                         }
+                        __syncwarp();
+                        nq = 0;
                     }
                     // (3) dense-dense: warp-cooperative popcount, G at a time
                     unsigned lb = __ballot_sync(FULL, dense_j);
@@ -582,10 +592,196 @@ __global__ void __launch_bounds__(SC2_WARPS * 32) k_sc2(WS ws, int* counter, int
                     }
                 }
             }
+            __syncwarp();
+            for (int t = lane; t < nq; t += 32) {  // (2b) remaining queued edges, one per lane
+                const uint32_t e = sq[t];
+                const int jq = (int)(e >> 16);
+                erow[e & 0xffffu] = ((uint32_t)jq << 16) | list_bitmap_count(lists + (int64_t)jq * LIST_MAX, deg_full[jq], sr);
+            }
         }
         if (lane == 0) ws.deg[p * ws.row_stride + i] = carry;
         __syncwarp();
     }
+}
+
+// Row classes for the SC^2 assembly: sparse rows (a list, not heavy) go to k_sc2_light, the rest to k_sc2.
+__global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    const int p = blockIdx.x;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int32_t* deg = ws.deg_full + p * ws.row_stride;
+    const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int32_t* L = ws.light_list + p * ws.row_stride;
+    int32_t* Dn = ws.dense_list + p * ws.row_stride;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (i < n && hpos[i] < 0 && deg[i] <= LIST_MAX) ? 1 : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) {
+            if (f) L[pos] = i;
+            else Dn[i - pos] = i;
+        }
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+    if (t == 0) { ws.st[p].n_light = s_carry; ws.st[p].n_dense = n - s_carry; }
+}
+
+// SC^2 edges of the sparse rows, packed for full lanes: a warp takes LG sparse rows (bitmaps and lists
+// staged in shared memory), enumerates all their upper edges, and pushes them into two queues — j sparse
+// (|L_j ∩ N(i)| against row i's bitmap) and j dense (|L_i ∩ N(j)| against row j's words) — each flushed
+// 32 edges at a time, one edge per lane.
+template <int WPL>
+constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
+template <int WPL>
+constexpr int light_warp_words() {
+    return light_rows<WPL>() * 32 * WPL + light_rows<WPL>() * (LIST_MAX / 2) + 64 + 64 + 4 * light_rows<WPL>();
+}
+template <int WPL>
+constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL>() * 4; }
+
+template <int WPL>
+__device__ __forceinline__ void light_flush(const WS& ws, int p, int n, int W, const uint32_t* bm, const uint16_t* ls,
+                                            const int32_t* meta, const uint32_t* q, int cnt, bool dense) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    if (lane < cnt) {
+        const uint32_t e = q[lane];
+        const int j = (int)(e & 0xffffu), t = (int)((e >> 16) & 63), r = (int)(e >> 22);
+        const int i = meta[4 * r], di = meta[4 * r + 1], lo = meta[4 * r + 2];
+        uint32_t c = 0;
+        if (!dense) {
+            c = list_bitmap_count(lists + (int64_t)j * LIST_MAX, deg_full[j], bm + r * 32 * WPL);
+        } else {
+            const uint32_t* rj = bits + (int64_t)j * W;
+            const uint16_t* Li = ls + r * LIST_MAX;
+            for (int k = 0; k < di; ++k) {
+                const int x = Li[k];
+                c += (__ldg(rj + (x >> 5)) >> (x & 31)) & 1u;
+            }
+        }
+        ws.edges[p * ws.edges_stride + tri_off(i, n) + (t - lo)] = ((uint32_t)j << 16) | c;
+    }
+}
+
+template <int WPL>
+__global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
+    constexpr int LG = light_rows<WPL>();
+    extern __shared__ uint32_t s_dyn[];
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nl = ws.st[p].n_light;
+    const int g0 = (blockIdx.x * 8 + warp) * LG;
+    if (g0 >= nl) return;
+    const int nr = min(LG, nl - g0);
+    uint32_t* bm = s_dyn + warp * light_warp_words<WPL>();
+    uint16_t* ls = reinterpret_cast<uint16_t*>(bm + LG * 32 * WPL);
+    uint32_t* qL = bm + LG * 32 * WPL + LG * (LIST_MAX / 2);
+    uint32_t* qD = qL + 64;
+    int32_t* meta = reinterpret_cast<int32_t*>(qD + 64);
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    const int32_t* light = ws.light_list + p * ws.row_stride;
+    // stage the group's bitmaps and lists; per-row meta (i, d, lo)
+    int my_i = 0, my_d = 0;
+    for (int r = 0; r < nr; ++r) {
+        const int i = light[g0 + r];
+        const uint32_t* ri = bits + (int64_t)i * W;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int w = lane + 32 * k;
+            bm[r * 32 * WPL + w] = (w < W) ? ri[w] : 0u;
+        }
+        const int di = deg_full[i];
+        if (lane < LIST_MAX / 8)
+            reinterpret_cast<uint4*>(ls + r * LIST_MAX)[lane] =
+                (lane * 8 < di) ? __ldg(reinterpret_cast<const uint4*>(lists + (int64_t)i * LIST_MAX) + lane) : make_uint4(0, 0, 0, 0);
+        if (lane == r) { my_i = i; my_d = di; }
+    }
+    __syncwarp();
+    int my_lo = 0;
+    for (int r = 0; r < nr; ++r) {
+        const int i = __shfl_sync(FULL, my_i, r), di = __shfl_sync(FULL, my_d, r);
+        int c = 0;
+        for (int t = lane; t < di; t += 32) c += (int)ls[r * LIST_MAX + t] <= i;
+        c = __reduce_add_sync(FULL, (unsigned)c);
+        if (lane == r) my_lo = c;
+    }
+    if (lane < nr) {
+        meta[4 * lane] = my_i; meta[4 * lane + 1] = my_d; meta[4 * lane + 2] = my_lo;
+        ws.deg[p * ws.row_stride + my_i] = my_d - my_lo;
+    }
+    // edge prefix over rows: pref(r) = Σ_{r' < r} (d − lo)
+    const int my_up = (lane < nr) ? my_d - my_lo : 0;
+    const int incl = warp_incl_scan(my_up);
+    const int my_pref = incl - my_up;
+    const int M = __shfl_sync(FULL, incl, 31);
+    if (lane < nr) meta[4 * lane + 3] = my_pref;
+    __syncwarp();
+    int nL = 0, nD = 0;
+    for (int e0 = 0; e0 < M; e0 += 32) {
+        const int e = e0 + lane;
+        bool isL = false, isD = false;
+        uint32_t packed = 0;
+        if (e < M) {
+            int r = 0;
+            for (int rr = 1; rr < nr; ++rr)
+                if (meta[4 * rr + 3] <= e) r = rr;
+            const int lo = meta[4 * r + 2];
+            const int pr = meta[4 * r + 3];
+            const int t = lo + (e - pr);
+            const int j = ls[r * LIST_MAX + t];
+            packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 22);
+            isL = deg_full[j] <= LIST_MAX;
+            isD = !isL;
+        }
+        const unsigned bL = __ballot_sync(FULL, isL), bD = __ballot_sync(FULL, isD);
+        const unsigned lt = (1u << lane) - 1u;
+        if (isL) qL[nL + __popc(bL & lt)] = packed;
+        if (isD) qD[nD + __popc(bD & lt)] = packed;
+        nL += __popc(bL);
+        nD += __popc(bD);
+        __syncwarp();
+        if (nL >= 32) {
+            light_flush<WPL>(ws, p, n, W, bm, ls, meta, qL, 32, false);
+            __syncwarp();
+            if (lane < nL - 32) qL[lane] = qL[32 + lane];
+            nL -= 32;
+            __syncwarp();
+        }
+        if (nD >= 32) {
+            light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, 32, true);
+            __syncwarp();
+            if (lane < nD - 32) qD[lane] = qD[32 + lane];
+            nD -= 32;
+            __syncwarp();
+        }
+    }
+    light_flush<WPL>(ws, p, n, W, bm, ls, meta, qL, nL, false);
+    light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, nD, true);
 }
 
 // Sorted neighbour lists (uint16) of the sparse rows (degree <= LIST_MAX), one warp per row.
@@ -615,6 +811,7 @@ __global__ void __launch_bounds__(256) k_lists(WS ws) {
             }
             carry += __shfl_sync(FULL, incl, 31);
         }
+        for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
     }
 }
 

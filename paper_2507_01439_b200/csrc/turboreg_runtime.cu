@@ -30,9 +30,11 @@ enum KernelId {
     KID_DEGREE,
     KID_HEAVY,
     KID_LISTS,
+    KID_ROWCLASS,
     KID_EXPAND,
     KID_SC2_MMA,
     KID_SC2,
+    KID_SC2_LIGHT,
     KID_HIST_HI,
     KID_HIST_LO,
     KID_SEL_COUNT,
@@ -44,12 +46,12 @@ enum KernelId {
     KID_FINALIZE,
     KID_COUNT
 };
-const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_lists",
-                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_hist_hi",     "k_hist_lo",
+const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_lists",       "k_rowclass",
+                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
                                        "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -96,7 +98,7 @@ struct turboreg_ctx {
     int32_t heavy_cap_alloc = 0;
     CUtensorMap tmX;
     bool tmX_ok = false;
-    int32_t opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
+    int32_t opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0, opt_sc2_variant = 0;
 };
 
 namespace {
@@ -151,7 +153,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -178,6 +180,8 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
         {sizeof(int) * 16, &p_ctr},
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
+        {sizeof(int32_t) * (size_t)(N * B), &p_ll},
+        {sizeof(int32_t) * (size_t)(N * B), &p_dl},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     size_t total = 0;
@@ -223,6 +227,8 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
+    w.light_list = static_cast<int32_t*>(p_ll);
+    w.dense_list = static_cast<int32_t*>(p_dl);
     // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle
     c->tmX_ok = false;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -248,6 +254,7 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.heavy_min_rows = c->opt_heavy_min_rows;
     c->ws.heavy_min_deg = c->opt_heavy_min_deg;
     c->ws.sc2_path = (c->opt_sc2_path == 0 && !c->tmX_ok) ? 1 : c->opt_sc2_path;
+    c->ws.sc2_variant = c->opt_sc2_variant;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -329,6 +336,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_LISTS, [&] { trk::k_lists<<<grow, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_ROWCLASS, [&] { trk::k_rowclass<<<B, 1024, 0, s>>>(ws); }));
     if (ws.sc2_path != 1) {
         CK(L.run(KID_EXPAND, [&] {
             const int64_t total = (int64_t)maxn_batch * Wb;
@@ -349,7 +357,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     {
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-        const dim3 gp((unsigned)(nsm * trk::SC2_PERSIST_BLOCKS_PER_SM));
+        (void)nsm;
+        const dim3 gp((unsigned)trk::SC2_BLOCKS_PER_PAIR, B);
         int* ctr = c->d_counters;
         CK(L.run(KID_SC2, [&] {
             if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws, ctr, maxn_batch, batch);
@@ -359,6 +368,17 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws, ctr, maxn_batch, batch);
             else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws, ctr, maxn_batch, batch);
             else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws, ctr, maxn_batch, batch);
+        }));
+        const int lgr = wpl >= 16 ? 2 : 8;  // trk::light_rows<WPL>()
+        const dim3 gl((unsigned)((maxn_batch + 8 * lgr - 1) / (8 * lgr)), B);
+        CK(L.run(KID_SC2_LIGHT, [&] {
+            if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), s>>>(ws);
+            else if (wpl <= 2) trk::k_sc2_light<2><<<gl, 256, trk::light_smem_bytes<2>(), s>>>(ws);
+            else if (wpl <= 4) trk::k_sc2_light<4><<<gl, 256, trk::light_smem_bytes<4>(), s>>>(ws);
+            else if (wpl <= 5) trk::k_sc2_light<5><<<gl, 256, trk::light_smem_bytes<5>(), s>>>(ws);
+            else if (wpl <= 8) trk::k_sc2_light<8><<<gl, 256, trk::light_smem_bytes<8>(), s>>>(ws);
+            else if (wpl <= 16) trk::k_sc2_light<16><<<gl, 256, trk::light_smem_bytes<16>(), s>>>(ws);
+            else trk::k_sc2_light<32><<<gl, 256, trk::light_smem_bytes<32>(), s>>>(ws);
         }));
     }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
@@ -442,6 +462,14 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
         cudaFuncSetAttribute(trk::k_sc2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<16>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2_light<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<5>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2_light<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<8>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2_light<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<16>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2_light<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<32>()) !=
             cudaSuccess) {
         cudaGetLastError();
         turboreg_destroy(c);
@@ -463,6 +491,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "heavy_min_degree") {
         if (value < 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_min_deg = (int32_t)value;
+    } else if (k == "sc2_variant") {
+        if (value < 0 || value > 3) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_sc2_variant = (int32_t)value;
     } else if (k == "heavy_cap") {
         if (value < 0 || value % 256 || value > c->heavy_cap_alloc) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_cap = (int32_t)value;
