@@ -60,6 +60,11 @@ struct WS {
     float4* src4;
     float4* dst4;
     int64_t pts_stride;
+    // point pairs for packed scoring: (x_2k, x_2k+1, y_2k, y_2k+1) and (z_2k, z_2k+1); stride pts_stride / 2
+    float4* srcP;
+    float2* srcZ;
+    float4* dstP;
+    float2* dstZ;
     uint32_t* bits;
     uint32_t* bits_base;
     int64_t bits_stride;
@@ -147,6 +152,19 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
         bad = !(isfinite(sx) && isfinite(sy) && isfinite(sz) && isfinite(tx) && isfinite(ty) && isfinite(tz));
         ws.src4[p * ws.pts_stride + k] = make_float4(sx, sy, sz, 0.f);
         ws.dst4[p * ws.pts_stride + k] = make_float4(tx, ty, tz, 0.f);
+    }
+    // paired layout (a pad point past n never scores: its target is at 3e38)
+    if (k < ((d.n + 1) & ~1)) {
+        const bool real = k < d.n;
+        const float sx = real ? d.src[3 * k] : 0.f, sy = real ? d.src[3 * k + 1] : 0.f, sz = real ? d.src[3 * k + 2] : 0.f;
+        const float tx = real ? d.dst[3 * k] : 3e38f, ty = real ? d.dst[3 * k + 1] : 3e38f, tz = real ? d.dst[3 * k + 2] : 3e38f;
+        const int64_t q = p * (ws.pts_stride / 2) + (k >> 1);
+        float* sp = reinterpret_cast<float*>(ws.srcP + q);
+        float* dp = reinterpret_cast<float*>(ws.dstP + q);
+        sp[k & 1] = sx; sp[2 + (k & 1)] = sy;
+        dp[k & 1] = tx; dp[2 + (k & 1)] = ty;
+        reinterpret_cast<float*>(ws.srcZ + q)[k & 1] = sz;
+        reinterpret_cast<float*>(ws.dstZ + q)[k & 1] = tz;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.st[p].nonfinite, 1);
 }
@@ -784,37 +802,6 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, nD, true);
 }
 
-// Sorted neighbour lists (uint16) of the sparse rows (degree <= LIST_MAX), one warp per row.
-__global__ void __launch_bounds__(256) k_lists(WS ws) {
-    const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    const int n = d.n;
-    if (n == 0) return;
-    const int W = d.W, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t* bits = ws.bits + p * ws.bits_stride;
-    uint16_t* lists = ws.lists + p * ws.lists_stride;
-    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
-    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
-        if (ws.deg_full[p * ws.row_stride + i] > LIST_MAX) continue;
-        uint16_t* L = lists + (int64_t)i * LIST_MAX;
-        int carry = 0;
-        for (int c = 0; c * 32 < W; ++c) {
-            const int w = c * 32 + lane;
-            uint32_t v = (w < W) ? bits[(int64_t)i * W + w] : 0u;
-            const int cnt = __popc(v);
-            const int incl = warp_incl_scan(cnt);
-            int pos = carry + incl - cnt;
-            while (v) {
-                const int b = __ffs(v) - 1;
-                v &= v - 1u;
-                L[pos++] = (uint16_t)(w * 32 + b);
-            }
-            carry += __shfl_sync(FULL, incl, 31);
-        }
-        for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
-    }
-}
-
 // Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4) and the
 // edge count E = Σ deg.
 __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
@@ -835,11 +822,16 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
         const int dg = ws.deg[p * ws.row_stride + i];
         my_edges += dg;
         const uint32_t* e = edges + tri_off(i, n);
-        for (int k = lane; k < dg; k += 32) {
-            const uint32_t w = e[k] & 0xffffu;
-            const int bin = (int)(w >> 7);
-            const unsigned m = __match_any_sync(__activemask(), w ? bin : -1);
-            if (w && lane == __ffs(m) - 1) atomicAdd(&s_hist[bin], __popc(m));
+        for (int k0 = 0; k0 < dg; k0 += 32) {
+            // weights of one row cluster in one bin: count the lanes sharing lane 0's bin with one
+            // ballot and one atomic, the (rare) others individually
+            const int k = k0 + lane;
+            const uint32_t w = (k < dg) ? (e[k] & 0xffffu) : 0u;
+            const int bin = w ? (int)(w >> 7) : -1;
+            const int b0 = __shfl_sync(FULL, bin, 0);
+            const unsigned same = __ballot_sync(FULL, bin == b0 && bin >= 0);
+            if (lane == 0 && same) atomicAdd(&s_hist[b0], __popc(same));
+            if (bin >= 0 && bin != b0) atomicAdd(&s_hist[bin], 1);
         }
     }
     if (lane == 0 && my_edges) atomicAdd(&s_edges, my_edges);
@@ -851,7 +843,8 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
 }
 
 // ------------------------------------------------------------------------------------------ a3 heavy split
-// Full degrees (popcount of each bit row) and their sum.
+// Full degrees (popcount of each bit row), their sum and maximum, and the sorted uint16 neighbour list of
+// every row with degree <= LIST_MAX (zero-padded to a 16-byte chunk); one warp per row.
 __global__ void __launch_bounds__(256) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
@@ -866,13 +859,28 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
     unsigned mine = 0;
     int mx = 0;
     const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    uint16_t* lists = ws.lists + p * ws.lists_stride;
     for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
-        unsigned c = 0;
-        for (int w = lane; w < W; w += 32) c += __popc(bits[(int64_t)i * W + w]);
-        c = __reduce_add_sync(FULL, c);
-        if (lane == 0) ws.deg_full[p * ws.row_stride + i] = (int)c;
-        mine += c;
-        mx = max(mx, (int)c);
+        uint16_t* L = lists + (int64_t)i * LIST_MAX;
+        int carry = 0;
+        for (int c = 0; c * 32 < W; ++c) {
+            const int w = c * 32 + lane;
+            uint32_t v = (w < W) ? bits[(int64_t)i * W + w] : 0u;
+            const int cnt = __popc(v);
+            const int incl = warp_incl_scan(cnt);
+            int pos = carry + incl - cnt;
+            while (v && pos < LIST_MAX) {
+                const int b = __ffs(v) - 1;
+                v &= v - 1u;
+                L[pos++] = (uint16_t)(w * 32 + b);
+            }
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+        if (carry <= LIST_MAX)
+            for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
+        if (lane == 0) ws.deg_full[p * ws.row_stride + i] = carry;
+        mine += carry;
+        mx = max(mx, carry);
     }
     if (lane == 0 && mine) { atomicAdd(&s_sum, (unsigned long long)mine); atomicMax(&s_max, mx); }
     __syncthreads();
@@ -937,51 +945,31 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     }
 }
 
-// X[a][k] = C[H_a][k] as uint8 0/1 for a < |H| rounded up to 256 (zero rows beyond |H|), k < 32 W.
+// X[a][k] = C[H_a][k] as uint8 0/1 for a < |H| rounded up to 256 (zero rows beyond |H|), k < 32 W: one warp
+// per X row, lane-strided words, each word → 32 bytes (two 16-byte stores, coalesced across the warp).
 __global__ void __launch_bounds__(256) k_expand(WS ws) {
-    const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    const int n = d.n;
-    if (n == 0) return;
-    const int h = ws.st[p].heavy_h;
-    if (h == 0) return;
-    const int W = d.W;
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // thread e → (source row i, word w); heavy rows land at X row hpos(i), light rows are skipped
-    const int64_t total = (int64_t)n * W;
-    if (e >= total) return;
-    const int i = (int)(e / W), w = (int)(e % W);
-    const int a = ws.hpos[p * ws.row_stride + i];
-    if (a < 0) return;
-    const uint32_t v = ws.bits[p * ws.bits_stride + (int64_t)i * W + w];
-    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap + 32 * w;
-    uint4 lo, hi4;
-    uint32_t b[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const uint32_t nib = (v >> (4 * q)) & 0xfu;
-        b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-    }
-    lo = make_uint4(b[0], b[1], b[2], b[3]);
-    hi4 = make_uint4(b[4], b[5], b[6], b[7]);
-    reinterpret_cast<uint4*>(X)[0] = lo;
-    reinterpret_cast<uint4*>(X)[1] = hi4;
-}
-
-// Zero rows [h, round_up(h, 256)) of X so the last MMA row tile reads zeros.
-__global__ void __launch_bounds__(256) k_expand_pad(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     if (d.n == 0) return;
     const int h = ws.st[p].heavy_h;
     if (h == 0) return;
     const int hp = (h + 255) / 256 * 256;
-    const int64_t rowbytes = (int64_t)d.W * 32;
-    const int64_t total = (int64_t)(hp - h) * rowbytes / 16;
-    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = h + e / (rowbytes / 16), c = e % (rowbytes / 16);
-        reinterpret_cast<uint4*>(X + r * ws.heavy_Kcap)[c] = make_uint4(0, 0, 0, 0);
+    const int a = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (a >= hp) return;
+    const int W = d.W;
+    const uint32_t* row = (a < h) ? ws.bits + p * ws.bits_stride + (int64_t)ws.heavy_list[p * ws.heavy_cap + a] * W : nullptr;
+    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
+    for (int w = lane; w < W; w += 32) {
+        const uint32_t v = row ? row[w] : 0u;
+        uint32_t b[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t nib = (v >> (4 * q)) & 0xfu;
+            b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
+        dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
+        dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
     }
 }
 
@@ -1426,80 +1414,119 @@ __global__ void __launch_bounds__(128) k_kabsch(WS ws) {
 // one thread stages into shared memory with two bulk async copies (cp.async.bulk, the TMA engine)
 // completing on an mbarrier; every thread then streams the chunk (broadcast LDS.128) through its own
 // (R, t) in the oracle's fixed fp32 FMA tree (reading r13) and adds its count atomically.
-constexpr int SCORE_HT = 128;
-constexpr int SCORE_PC = 1024;
+constexpr int SCORE_THREADS = 128;               // each thread scores two hypotheses
+constexpr int SCORE_HT = 2 * SCORE_THREADS;      // hypotheses per block
+constexpr int SCORE_PC = 512;                    // correspondences per pipeline stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(SCORE_HT) k_score(WS ws) {
-    __shared__ __align__(16) float4 s_src[SCORE_PC];
-    __shared__ __align__(16) float4 s_dst[SCORE_PC];
-    __shared__ __align__(8) unsigned long long s_bar;
-    const int q = blockIdx.z;
+// g(T) = inlier number.  A block owns 256 hypotheses of one pair (two per thread, packed as
+// f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and streams all N
+// correspondences through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
+// engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
+// Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
+__global__ void __launch_bounds__(SCORE_THREADS) k_score(WS ws) {
+    __shared__ __align__(16) float4 s_src[2][SCORE_PC];
+    __shared__ __align__(16) float4 s_dst[2][SCORE_PC];
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
     const int n = d.n;
     if (n == 0) return;
-    const int k0 = blockIdx.y * SCORE_PC;
-    if (k0 >= n) return;
-    const int kc = min(SCORE_PC, n - k0);
     const int K = ws.k1 * ws.k2;
-    const int h = blockIdx.x * SCORE_HT + threadIdx.x;
-    float* hp = ws.hyp + (q * ws.cl_stride + h) * 16;
-    bool valid = false;
-    float R[9], t[3];
-    if (h < K) {
-        const float4* h4 = reinterpret_cast<const float4*>(hp);
+    const int h0 = blockIdx.x * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
+    float R0[12], R1[12];
+    bool v0 = false, v1 = false;
+    float* hp0 = ws.hyp + (q * ws.cl_stride + h0) * 16;
+    float* hp1 = ws.hyp + (q * ws.cl_stride + h1) * 16;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) { R0[k] = 0.f; R1[k] = 0.f; }
+    if (h0 < K) {
+        const float4* h4 = reinterpret_cast<const float4*>(hp0);
         const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
-        valid = __float_as_int(e.y) == 0;
-        R[0] = a.x; R[1] = a.y; R[2] = a.z; R[3] = a.w; R[4] = b.x; R[5] = b.y; R[6] = b.z; R[7] = b.w;
-        R[8] = c.x; t[0] = c.y; t[1] = c.z; t[2] = c.w;
+        v0 = __float_as_int(e.y) == 0;
+        R0[0] = a.x; R0[1] = a.y; R0[2] = a.z; R0[3] = a.w; R0[4] = b.x; R0[5] = b.y; R0[6] = b.z; R0[7] = b.w;
+        R0[8] = c.x; R0[9] = c.y; R0[10] = c.z; R0[11] = c.w;
     }
-    if (!__syncthreads_or(valid)) return;
-    const uint32_t bar = smem_u32(&s_bar);
+    if (h1 < K) {
+        const float4* h4 = reinterpret_cast<const float4*>(hp1);
+        const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
+        v1 = __float_as_int(e.y) == 0;
+        R1[0] = a.x; R1[1] = a.y; R1[2] = a.z; R1[3] = a.w; R1[4] = b.x; R1[5] = b.y; R1[6] = b.z; R1[7] = b.w;
+        R1[8] = c.x; R1[9] = c.y; R1[10] = c.z; R1[11] = c.w;
+    }
+    if (!__syncthreads_or(v0 || v1)) return;
+    const uint32_t bar0 = smem_u32(&s_bar[0]), bar1 = smem_u32(&s_bar[1]);
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    const int nchunks = (n + SCORE_PC - 1) / SCORE_PC;
+    const float4* gs = ws.src4 + q * ws.pts_stride;
+    const float4* gd = ws.dst4 + q * ws.pts_stride;
+    auto issue = [&](int c) {  // thread 0: stage chunk c into buffer c & 1
+        const int st = c & 1;
+        const int kc = min(SCORE_PC, n - c * SCORE_PC);
         const uint32_t bytes = (uint32_t)kc * 16u;
+        const uint32_t bar = st ? bar1 : bar0;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * bytes) : "memory");
-        const float4* gs = ws.src4 + q * ws.pts_stride + k0;
-        const float4* gd = ws.dst4 + q * ws.pts_stride + k0;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(s_src)),
-                     "l"(gs), "r"(bytes), "r"(bar)
+                         smem_u32(s_src[st])),
+                     "l"(gs + c * SCORE_PC), "r"(bytes), "r"(bar)
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(s_dst)),
-                     "l"(gd), "r"(bytes), "r"(bar)
+                         smem_u32(s_dst[st])),
+                     "l"(gd + c * SCORE_PC), "r"(bytes), "r"(bar)
                      : "memory");
-    }
-    {
-        uint32_t done = 0;
-        while (!done) {
-            asm volatile(
-                "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0; selp.u32 %0, 1, 0, P; }"
-                : "=r"(done)
-                : "r"(bar)
-                : "memory");
+    };
+    if (threadIdx.x == 0) issue(0);
+    const uint32_t thr2b = __float_as_uint(__fmul_rn(ws.thr, ws.thr));
+    f2_t Rp[9], tp[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Rp[k] = f2_pack(R0[k], R1[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tp[k] = f2_pack(R0[9 + k], R1[9 + k]);
+    const f2_t mone = f2_pack(-1.0f, -1.0f);
+    int cnt0 = 0, cnt1 = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int st = c & 1;
+        if (threadIdx.x == 0 && c + 1 < nchunks) issue(c + 1);  // buffer st^1 was released by the barrier below
+        {
+            const uint32_t bar = st ? bar1 : bar0, parity = (uint32_t)((c >> 1) & 1);
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                    : "=r"(done)
+                    : "r"(bar), "r"(parity)
+                    : "memory");
+            }
         }
-    }
-    if (!valid) return;
-    const float thr2 = __fmul_rn(ws.thr, ws.thr);
-    int cnt = 0;
+        const int kc = min(SCORE_PC, n - c * SCORE_PC);
+        const float4* xs = s_src[st];
+        const float4* ys = s_dst[st];
 #pragma unroll 4
-    for (int k = 0; k < kc; ++k) {
-        const float4 x = s_src[k];
-        const float4 y = s_dst[k];
-        const float p0 = __fmaf_rn(R[2], x.z, __fmaf_rn(R[1], x.y, __fmaf_rn(R[0], x.x, t[0])));
-        const float p1 = __fmaf_rn(R[5], x.z, __fmaf_rn(R[4], x.y, __fmaf_rn(R[3], x.x, t[1])));
-        const float p2 = __fmaf_rn(R[8], x.z, __fmaf_rn(R[7], x.y, __fmaf_rn(R[6], x.x, t[2])));
-        const float e0 = __fsub_rn(p0, y.x), e1 = __fsub_rn(p1, y.y), e2 = __fsub_rn(p2, y.z);
-        const float s = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-        cnt += (s <= thr2);
+        for (int k = 0; k < kc; ++k) {
+            const float4 x = xs[k];
+            const float4 y = ys[k];
+            const f2_t X = f2_pack(x.x, x.x), Y = f2_pack(x.y, x.y), Z = f2_pack(x.z, x.z);
+            const f2_t p0 = f2_fma(Rp[2], Z, f2_fma(Rp[1], Y, f2_fma(Rp[0], X, tp[0])));
+            const f2_t p1 = f2_fma(Rp[5], Z, f2_fma(Rp[4], Y, f2_fma(Rp[3], X, tp[1])));
+            const f2_t p2 = f2_fma(Rp[8], Z, f2_fma(Rp[7], Y, f2_fma(Rp[6], X, tp[2])));
+            const f2_t e0 = f2_fma(f2_pack(y.x, y.x), mone, p0);  // p − y: exact negation, one rounding
+            const f2_t e1 = f2_fma(f2_pack(y.y, y.y), mone, p1);
+            const f2_t e2 = f2_fma(f2_pack(y.z, y.z), mone, p2);
+            const f2_t sq = f2_fma(e2, e2, f2_fma(e1, e1, f2_mul(e0, e0)));
+            // s >= 0, so integer order of the bit patterns is float order
+            cnt0 += f2_lo(sq) <= thr2b;
+            cnt1 += f2_hi(sq) <= thr2b;
+        }
+        __syncthreads();  // every thread is done with buffer st before it is refilled
     }
-    if (cnt) atomicAdd(reinterpret_cast<int*>(hp + 12), cnt);
+    if (v0 && cnt0) atomicAdd(reinterpret_cast<int*>(hp0 + 12), cnt0);
+    if (v1 && cnt1) atomicAdd(reinterpret_cast<int*>(hp1 + 12), cnt1);
 }
 
 // ------------------------------------------------------------------------------------------ a8 argmax

@@ -29,7 +29,6 @@ enum KernelId {
     KID_COMPAT,
     KID_DEGREE,
     KID_HEAVY,
-    KID_LISTS,
     KID_ROWCLASS,
     KID_EXPAND,
     KID_SC2_MMA,
@@ -46,12 +45,12 @@ enum KernelId {
     KID_FINALIZE,
     KID_COUNT
 };
-const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_lists",       "k_rowclass",
+const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
                                        "k_expand",   "k_sc2_mma",      "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
                                        "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -145,7 +144,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     const bool base = c->prm.tau_base > 0.f;
     struct Item { size_t bytes; void** dst; };
     trk::WS& w = c->ws;
-    w.pts_stride = N;
+    w.pts_stride = round_up(N, 32);  // even, so the paired arrays (stride / 2) stay 16-byte aligned
     w.bits_stride = N * W;
     w.row_stride = N;
     w.edges_stride = std::max<int64_t>(1, N * (N - 1) / 2);
@@ -153,13 +152,13 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_sP; void* p_sZ; void* p_dP; void* p_dZ;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
         {sizeof(trk::PairState) * B, &p_st},
-        {sizeof(float4) * N * B, &p_src4},
-        {sizeof(float4) * N * B, &p_dst4},
+        {sizeof(float4) * w.pts_stride * B, &p_src4},
+        {sizeof(float4) * w.pts_stride * B, &p_dst4},
         {sizeof(uint32_t) * N * W * B, &p_bits},
         {sizeof(int32_t) * N * B, &p_deg},
         {sizeof(int32_t) * N * B, &p_gt},
@@ -182,6 +181,10 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
         {sizeof(int32_t) * (size_t)(N * B), &p_ll},
         {sizeof(int32_t) * (size_t)(N * B), &p_dl},
+        {sizeof(float4) * (size_t)(w.pts_stride / 2 * B), &p_sP},
+        {sizeof(float2) * (size_t)(w.pts_stride / 2 * B), &p_sZ},
+        {sizeof(float4) * (size_t)(w.pts_stride / 2 * B), &p_dP},
+        {sizeof(float2) * (size_t)(w.pts_stride / 2 * B), &p_dZ},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     size_t total = 0;
@@ -228,6 +231,10 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
     w.light_list = static_cast<int32_t*>(p_ll);
+    w.srcP = static_cast<float4*>(p_sP);
+    w.srcZ = static_cast<float2*>(p_sZ);
+    w.dstP = static_cast<float4*>(p_dP);
+    w.dstZ = static_cast<float2*>(p_dZ);
     w.dense_list = static_cast<int32_t*>(p_dl);
     // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle
     c->tmX_ok = false;
@@ -335,13 +342,10 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
-    CK(L.run(KID_LISTS, [&] { trk::k_lists<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_ROWCLASS, [&] { trk::k_rowclass<<<B, 1024, 0, s>>>(ws); }));
     if (ws.sc2_path != 1) {
         CK(L.run(KID_EXPAND, [&] {
-            const int64_t total = (int64_t)maxn_batch * Wb;
-            trk::k_expand<<<dim3((unsigned)((total + 255) / 256), B), 256, 0, s>>>(ws);
-            trk::k_expand_pad<<<dim3(64, B), 256, 0, s>>>(ws);
+            trk::k_expand<<<dim3((unsigned)(ws.heavy_cap / 8), B), 256, 0, s>>>(ws);
         }));
         CK(L.run(KID_SC2_MMA, [&] {
             if (ws.sc2_path == 2) {
@@ -394,9 +398,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
-            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT),
-                         (unsigned)((maxn_batch + trk::SCORE_PC - 1) / trk::SCORE_PC), B);
-            trk::k_score<<<g, trk::SCORE_HT, 0, s>>>(ws);
+            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT), B);
+            trk::k_score<<<g, trk::SCORE_THREADS, 0, s>>>(ws);
         }));
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
     }
