@@ -116,7 +116,8 @@ const char* turboreg_status_string(turboreg_status s);
  *   TURBOREG_I_BITS      uint32 [n][W]  rows of C(τ), W = words per row (*needed / (4n))
  *   TURBOREG_I_BITS_BASE uint32 [n][W]  rows of C(τ_base) (only if tau_base > 0)
  *   TURBOREG_I_SC2       int32  [n][n]  Ĝ expanded to a dense symmetric matrix
- *   TURBOREG_I_PIVOTS    int32  [P][3]  (i, j, w) in (i, j) lexicographic order
+ *   TURBOREG_I_PIVOTS    int32  [P][3]  (i, j, w) in (w desc, i asc, j asc) order — (i, j) lexicographic
+ *                        order when more than 8192 edges reach the cut weight α_K1
  *   TURBOREG_I_CLIQUES   int32  [K1*K2][4] (i, j, z, S) per slot p*K2 + r; empty slots are (-1,-1,-1,0)
  *   TURBOREG_I_HYPS      float  [K1*K2][16]: R[9], t[3], count (int32 bits), flag (int32 bits:
  *                        0 valid, 1 degenerate, 2 empty slot), S (int32 bits), 0

@@ -5,8 +5,9 @@
 // pair's geometry from a PairDesc.  Data layout per pair:
 //   src4/dst4  float4[n]          correspondences (x, y, z, 0)
 //   bits       uint32[n][W]       rows of C(τ); bit c of word c/32 = C_rc; W = ceil(n/32) rounded up to 4
-//   edges      uint32[n(n-1)/2]   row i's upper edges (j > i) in increasing j at tri_off(i):
-//                                 (j << 16) | Ĝ_ij   ("rank-indexed" O2 weights, Def. 2)
+//   edges      uint32[E]          compact CSR of the O2 rows: row i's upper edges (j > i) in increasing j at
+//                                 rowptr[i]: (j << 16) | Ĝ_ij   ("rank-indexed" O2 weights, Def. 2)
+//   rowptr     int32[n+1]         exclusive scan of the upper degrees
 //   deg        int32[n]           upper degree of row i
 //   piv        int4[K1]           (i, j, Ĝ_ij, 0) in lexicographic order
 //   cliq       int4[K1*K2]        (i, j, z, S) per slot pivot*K2 + r; empty (-1,-1,-1,0)
@@ -49,7 +50,9 @@ struct PairState {
     int32_t deg_max;             // max_i deg(i)
     int32_t n_light;             // rows with a list and not heavy (k_sc2_light)
     int32_t n_dense;             // the other rows (k_sc2)
-    int32_t pad[3];
+    int32_t ncand;               // pivot candidates (weight >= α) collected
+    int32_t cand_overflow;       // ncand > PIV_CAP: the ordered count/scan/emit path selects instead
+    int32_t pad[1];
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
@@ -60,11 +63,6 @@ struct WS {
     float4* src4;
     float4* dst4;
     int64_t pts_stride;
-    // point pairs for packed scoring: (x_2k, x_2k+1, y_2k, y_2k+1) and (z_2k, z_2k+1); stride pts_stride / 2
-    float4* srcP;
-    float2* srcZ;
-    float4* dstP;
-    float2* dstZ;
     uint32_t* bits;
     uint32_t* bits_base;
     int64_t bits_stride;
@@ -76,8 +74,11 @@ struct WS {
     int64_t row_stride;
     uint32_t* edges;
     int64_t edges_stride;
+    int32_t* rowptr;      // [n+1] per pair, stride rp_stride
+    int64_t rp_stride;
     int4* piv;
     int64_t piv_stride;  // K1
+    unsigned long long* cand;  // [PIV_CAP] pivot candidate keys per pair
     int4* cliq;
     float* hyp;
     int64_t cl_stride;  // K1*K2
@@ -102,7 +103,6 @@ struct WS {
     int32_t k1, k2, mode;
 };
 
-__device__ __forceinline__ int64_t tri_off(int64_t i, int64_t n) { return i * n - (i * (i + 1)) / 2; }
 
 // Row i restricted to its upper part U_i = {c > i} (the O2 out-neighbourhood, Def. 2).
 __device__ __forceinline__ uint32_t upper_mask(uint32_t v, int w, int i) {
@@ -152,19 +152,6 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
         bad = !(isfinite(sx) && isfinite(sy) && isfinite(sz) && isfinite(tx) && isfinite(ty) && isfinite(tz));
         ws.src4[p * ws.pts_stride + k] = make_float4(sx, sy, sz, 0.f);
         ws.dst4[p * ws.pts_stride + k] = make_float4(tx, ty, tz, 0.f);
-    }
-    // paired layout (a pad point past n never scores: its target is at 3e38)
-    if (k < ((d.n + 1) & ~1)) {
-        const bool real = k < d.n;
-        const float sx = real ? d.src[3 * k] : 0.f, sy = real ? d.src[3 * k + 1] : 0.f, sz = real ? d.src[3 * k + 2] : 0.f;
-        const float tx = real ? d.dst[3 * k] : 3e38f, ty = real ? d.dst[3 * k + 1] : 3e38f, tz = real ? d.dst[3 * k + 2] : 3e38f;
-        const int64_t q = p * (ws.pts_stride / 2) + (k >> 1);
-        float* sp = reinterpret_cast<float*>(ws.srcP + q);
-        float* dp = reinterpret_cast<float*>(ws.dstP + q);
-        sp[k & 1] = sx; sp[2 + (k & 1)] = sy;
-        dp[k & 1] = tx; dp[2 + (k & 1)] = ty;
-        reinterpret_cast<float*>(ws.srcZ + q)[k & 1] = sz;
-        reinterpret_cast<float*>(ws.dstZ + q)[k & 1] = tz;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.st[p].nonfinite, 1);
 }
@@ -402,7 +389,7 @@ __global__ void __launch_bounds__(256) k_compat(WS ws) {
 //   * both endpoints heavy → Ĝ_ij was computed on the tensor cores: gather D[hpos i][hpos j];
 //   * otherwise (the sparse remainder) → popcount(row_i AND row_j): row_i in registers (lane-strided),
 //     G light edges at a time so G·WPL row_j loads are in flight, REDUX per edge.
-// The result (j << 16 | Ĝ_ij) goes to edges[tri_off(i) + rank]; positive weights feed a 256-bin histogram
+// The result (j << 16 | Ĝ_ij) goes to edges[rowptr(i) + rank]; positive weights feed a 256-bin histogram
 // of Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
 constexpr int SC2_WARPS = 8;
 constexpr int SC2_ROWS_PER_BLOCK = 64;
@@ -485,7 +472,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws, int* counter, 
         const int di = deg_full[i];
         const int hi = hpos[i];
         const bool ilist = di <= LIST_MAX;
-        uint32_t* erow = ws.edges + p * ws.edges_stride + tri_off(i, n);
+        uint32_t* erow = ws.edges + p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i];
         uint32_t reg[WPL];
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
@@ -617,7 +604,6 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws, int* counter, 
                 erow[e & 0xffffu] = ((uint32_t)jq << 16) | list_bitmap_count(lists + (int64_t)jq * LIST_MAX, deg_full[jq], sr);
             }
         }
-        if (lane == 0) ws.deg[p * ws.row_stride + i] = carry;
         __syncwarp();
     }
 }
@@ -659,6 +645,31 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
         __syncthreads();
     }
     if (t == 0) { ws.st[p].n_light = s_carry; ws.st[p].n_dense = n - s_carry; }
+    // compact CSR row pointers of the O2 edge lists: exclusive scan of the upper degrees
+    __syncthreads();
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    const int32_t* udeg = ws.deg + p * ws.row_stride;
+    int32_t* rp = ws.rowptr + p * ws.rp_stride;
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (i < n) ? udeg[i] : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) rp[i] = pos;
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+    if (t == 0) { rp[n] = s_carry; ws.st[p].edges = s_carry; }
 }
 
 // SC^2 edges of the sparse rows, packed for full lanes: a warp takes LG sparse rows (bitmaps and lists
@@ -696,7 +707,7 @@ __device__ __forceinline__ void light_flush(const WS& ws, int p, int n, int W, c
                 c += (__ldg(rj + (x >> 5)) >> (x & 31)) & 1u;
             }
         }
-        ws.edges[p * ws.edges_stride + tri_off(i, n) + (t - lo)] = ((uint32_t)j << 16) | c;
+        ws.edges[p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i] + (t - lo)] = ((uint32_t)j << 16) | c;
     }
 }
 
@@ -750,7 +761,6 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     }
     if (lane < nr) {
         meta[4 * lane] = my_i; meta[4 * lane + 1] = my_d; meta[4 * lane + 2] = my_lo;
-        ws.deg[p * ws.row_stride + my_i] = my_d - my_lo;
     }
     // edge prefix over rows: pref(r) = Σ_{r' < r} (d − lo)
     const int my_up = (lane < nr) ? my_d - my_lo : 0;
@@ -802,44 +812,34 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, nD, true);
 }
 
-// Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4) and the
-// edge count E = Σ deg.
+// The pivot passes stream the pair's compact O2 edge array (E words) with a grid stride: coalesced,
+// no per-row bookkeeping.
+constexpr int SEL_BLOCKS_PER_PAIR = 32;
+
+// Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4).
 __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
     __shared__ int s_hist[256];
-    __shared__ int s_edges;
     const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    const int n = d.n;
-    if (n == 0) return;
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
-    if (threadIdx.x == 0) s_edges = 0;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t* edges = ws.edges + p * ws.edges_stride;
-    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
-    int my_edges = 0;
-    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
-        const int dg = ws.deg[p * ws.row_stride + i];
-        my_edges += dg;
-        const uint32_t* e = edges + tri_off(i, n);
-        for (int k0 = 0; k0 < dg; k0 += 32) {
-            // weights of one row cluster in one bin: count the lanes sharing lane 0's bin with one
-            // ballot and one atomic, the (rare) others individually
-            const int k = k0 + lane;
-            const uint32_t w = (k < dg) ? (e[k] & 0xffffu) : 0u;
-            const int bin = w ? (int)(w >> 7) : -1;
-            const int b0 = __shfl_sync(FULL, bin, 0);
-            const unsigned same = __ballot_sync(FULL, bin == b0 && bin >= 0);
-            if (lane == 0 && same) atomicAdd(&s_hist[b0], __popc(same));
-            if (bin >= 0 && bin != b0) atomicAdd(&s_hist[bin], 1);
-        }
-    }
-    if (lane == 0 && my_edges) atomicAdd(&s_edges, my_edges);
-    __syncthreads();
+    if (ws.desc[p].n == 0) return;
     PairState* st = ws.st + p;
+    const int E = st->edges;
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
+    __syncthreads();
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int lane = threadIdx.x & 31;
+    for (int e0 = blockIdx.x * blockDim.x; e0 < E; e0 += gridDim.x * blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        // consecutive weights come from one row and cluster in one bin: lanes sharing lane 0's bin add once
+        const uint32_t w = (e < E) ? (__ldg(edges + e) & 0xffffu) : 0u;
+        const int bin = w ? (int)(w >> 7) : -1;
+        const int b0 = __shfl_sync(FULL, bin, 0);
+        const unsigned same = __ballot_sync(FULL, bin == b0 && bin >= 0);
+        if (lane == 0 && same) atomicAdd(&s_hist[b0], __popc(same));
+        if (bin >= 0 && bin != b0) atomicAdd(&s_hist[bin], 1);
+    }
+    __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x)
         if (s_hist[b]) atomicAdd(&st->hist_hi[b], s_hist[b]);
-    if (threadIdx.x == 0 && s_edges) atomicAdd(&st->edges, s_edges);
 }
 
 // ------------------------------------------------------------------------------------------ a3 heavy split
@@ -863,9 +863,11 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
     for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
         uint16_t* L = lists + (int64_t)i * LIST_MAX;
         int carry = 0;
+        unsigned ucnt = 0;
         for (int c = 0; c * 32 < W; ++c) {
             const int w = c * 32 + lane;
             uint32_t v = (w < W) ? bits[(int64_t)i * W + w] : 0u;
+            ucnt += __popc(upper_mask(v, w, i));
             const int cnt = __popc(v);
             const int incl = warp_incl_scan(cnt);
             int pos = carry + incl - cnt;
@@ -878,7 +880,8 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
         }
         if (carry <= LIST_MAX)
             for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
-        if (lane == 0) ws.deg_full[p * ws.row_stride + i] = carry;
+        ucnt = __reduce_add_sync(FULL, ucnt);
+        if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = carry; ws.deg[p * ws.row_stride + i] = (int)ucnt; }
         mine += carry;
         mx = max(mx, carry);
     }
@@ -1020,25 +1023,18 @@ __device__ void block_suffix_select(const int* hist, int nb, int K, int lowest, 
 __global__ void __launch_bounds__(256) k_hist_lo(WS ws) {
     __shared__ int s_lo[128];
     const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    const int n = d.n;
-    if (n == 0) return;
+    if (ws.desc[p].n == 0) return;
     PairState* st = ws.st + p;
     int b1, above, total;
     block_suffix_select(st->hist_hi, 256, ws.k1, 0, &b1, &above, &total);
     if (blockIdx.x == 0 && threadIdx.x == 0) { st->b1 = b1; st->above = above; st->epos = total; }
     for (int b = threadIdx.x; b < 128; b += blockDim.x) s_lo[b] = 0;
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int E = st->edges;
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
-    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
-    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
-        const int dg = ws.deg[p * ws.row_stride + i];
-        const uint32_t* e = edges + tri_off(i, n);
-        for (int k = lane; k < dg; k += 32) {
-            const uint32_t w = e[k] & 0xffffu;
-            if (w && (int)(w >> 7) == b1) atomicAdd(&s_lo[w & 127u], 1);
-        }
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const uint32_t w = __ldg(edges + e) & 0xffffu;
+        if (w && (int)(w >> 7) == b1) atomicAdd(&s_lo[w & 127u], 1);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < 128; b += blockDim.x)
@@ -1056,21 +1052,106 @@ __device__ void pivot_threshold(WS& ws, PairState* st, int* alpha, int* c_gt, in
     *need = ws.k1 - *c_gt;
 }
 
+// One block per pair: α, #(> α) and `need` into the pair state.
+__global__ void __launch_bounds__(256) k_alpha(WS ws) {
+    const int p = blockIdx.x;
+    if (ws.desc[p].n == 0) return;
+    PairState* st = ws.st + p;
+    int alpha, c_gt, need;
+    pivot_threshold(ws, st, &alpha, &c_gt, &need);
+    if (threadIdx.x == 0) { st->alpha = alpha; st->c_gt = c_gt; st->need = need; }
+}
+
+// Every edge with weight > α, or == α, is a pivot candidate: its key ((0x7fff − w) << 30 | i << 15 | j)
+// orders candidates by (w desc, i asc, j asc) (readings r4, r5).  Warp-aggregated append.
+constexpr int PIV_CAP = 8192;
+__global__ void __launch_bounds__(256) k_collect(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    const int alpha = st->alpha;
+    const int E = st->edges;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int32_t* rp = ws.rowptr + p * ws.rp_stride;
+    unsigned long long* cand = ws.cand + (int64_t)p * PIV_CAP;
+    const int lane = threadIdx.x & 31;
+    for (int e0 = blockIdx.x * blockDim.x; e0 < E; e0 += gridDim.x * blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        const uint32_t v = (e < E) ? __ldg(edges + e) : 0u;
+        const int w = (int)(v & 0xffffu);
+        const bool c = e < E && w >= alpha && w > 0;
+        const unsigned b = __ballot_sync(FULL, c);
+        if (!b) continue;
+        const int leader = __ffs(b) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&st->ncand, __popc(b));
+        base = __shfl_sync(FULL, base, leader);
+        if (c) {
+            int lo = 0, hi = n;  // row of edge e: rp[lo] <= e < rp[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(rp + mid) <= e) lo = mid; else hi = mid;
+            }
+            const int slot = base + __popc(b & ((1u << lane) - 1u));
+            if (slot < PIV_CAP)
+                cand[slot] = ((unsigned long long)(0x7fff - w) << 30) | ((unsigned long long)lo << 15) | (v >> 16);
+        }
+    }
+}
+
+// One block per pair: bitonic sort of the candidates, the first min(K1, #candidates) become the pivots.
+__global__ void __launch_bounds__(1024) k_pivot_sort(WS ws) {
+    extern __shared__ unsigned long long s_key[];
+    const int p = blockIdx.x;
+    if (ws.desc[p].n == 0) return;
+    PairState* st = ws.st + p;
+    const int m = st->ncand;
+    if (m > PIV_CAP) {
+        if (threadIdx.x == 0) st->cand_overflow = 1;
+        return;
+    }
+    int m2 = 1;
+    while (m2 < m) m2 <<= 1;
+    const unsigned long long* cand = ws.cand + (int64_t)p * PIV_CAP;
+    for (int k = threadIdx.x; k < m2; k += blockDim.x) s_key[k] = (k < m) ? cand[k] : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= m2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int k = threadIdx.x; k < m2 / 2; k += blockDim.x) {
+                const int lo = 2 * k - (k & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = s_key[lo], b = s_key[hi];
+                if ((a > b) == up) { s_key[lo] = b; s_key[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+    const int P = min(ws.k1, m);
+    int4* piv = ws.piv + p * ws.piv_stride;
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        const unsigned long long key = s_key[k];
+        piv[k] = make_int4((int)((key >> 15) & 0x7fff), (int)(key & 0x7fff), 0x7fff - (int)(key >> 30), 0);
+    }
+    if (threadIdx.x == 0) st->npiv = P;
+}
+
 __global__ void __launch_bounds__(256) k_select_count(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
     if (n == 0) return;
     PairState* st = ws.st + p;
-    int alpha, c_gt, need;
-    pivot_threshold(ws, st, &alpha, &c_gt, &need);
-    if (blockIdx.x == 0 && threadIdx.x == 0) { st->alpha = alpha; st->c_gt = c_gt; st->need = need; }
+    if (!st->cand_overflow) return;  // the candidate sort selected the pivots
+    const int alpha = st->alpha;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
     const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
     for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
         const int dg = ws.deg[p * ws.row_stride + i];
-        const uint32_t* e = edges + tri_off(i, n);
+        const uint32_t* e = edges + ws.rowptr[p * ws.rp_stride + i];
         int gt = 0, eq = 0;
         for (int k = lane; k < dg; k += 32) {
             const int w = (int)(e[k] & 0xffffu);
@@ -1096,6 +1177,7 @@ __global__ void __launch_bounds__(1024) k_select_scan(WS ws) {
     const int n = d.n;
     if (n == 0) return;
     PairState* st = ws.st + p;
+    if (!st->cand_overflow) return;
     const int need = st->need;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) { s_carry[0] = 0; s_carry[1] = 0; }
@@ -1151,6 +1233,7 @@ __global__ void __launch_bounds__(256) k_select_emit(WS ws) {
     const int n = d.n;
     if (n == 0) return;
     const PairState* st = ws.st + p;
+    if (!st->cand_overflow) return;
     const int alpha = st->alpha;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -1164,7 +1247,7 @@ __global__ void __launch_bounds__(256) k_select_emit(WS ws) {
         const int dg = ws.deg[ro];
         int pos = ws.row_off[ro];
         int eqseen = 0;
-        const uint32_t* e = edges + tri_off(i, n);
+        const uint32_t* e = edges + ws.rowptr[p * ws.rp_stride + i];
         for (int k0 = 0; k0 < dg; k0 += 32) {
             const int k = k0 + lane;
             const uint32_t v = (k < dg) ? e[k] : 0u;
@@ -1242,8 +1325,8 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const uint32_t* ri = bits + (int64_t)i * W;
     const uint32_t* rj = bits + (int64_t)j * W;
     const uint32_t* edges = ws.edges + q * ws.edges_stride;
-    const uint32_t* ei = edges + tri_off(i, n);
-    const uint32_t* ej = edges + tri_off(j, n);
+    const uint32_t* ei = edges + ws.rowptr[q * ws.rp_stride + i];
+    const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
     int emitted = 0;
     if (K2 <= PGS_KL) {
         unsigned long long top[PGS_KL];

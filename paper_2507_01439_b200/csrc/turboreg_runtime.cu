@@ -36,6 +36,9 @@ enum KernelId {
     KID_SC2_LIGHT,
     KID_HIST_HI,
     KID_HIST_LO,
+    KID_ALPHA,
+    KID_COLLECT,
+    KID_PIVOT_SORT,
     KID_SEL_COUNT,
     KID_SEL_SCAN,
     KID_SEL_EMIT,
@@ -46,11 +49,11 @@ enum KernelId {
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
-                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",
+                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
                                        "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -152,7 +155,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_sP; void* p_sZ; void* p_dP; void* p_dZ;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -181,10 +184,8 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
         {sizeof(int32_t) * (size_t)(N * B), &p_ll},
         {sizeof(int32_t) * (size_t)(N * B), &p_dl},
-        {sizeof(float4) * (size_t)(w.pts_stride / 2 * B), &p_sP},
-        {sizeof(float2) * (size_t)(w.pts_stride / 2 * B), &p_sZ},
-        {sizeof(float4) * (size_t)(w.pts_stride / 2 * B), &p_dP},
-        {sizeof(float2) * (size_t)(w.pts_stride / 2 * B), &p_dZ},
+        {sizeof(unsigned long long) * (size_t)(trk::PIV_CAP * B), &p_cand},
+        {sizeof(int32_t) * (size_t)((N + 1) * B), &p_rp},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     size_t total = 0;
@@ -231,10 +232,9 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
     w.light_list = static_cast<int32_t*>(p_ll);
-    w.srcP = static_cast<float4*>(p_sP);
-    w.srcZ = static_cast<float2*>(p_sZ);
-    w.dstP = static_cast<float4*>(p_dP);
-    w.dstZ = static_cast<float2*>(p_dZ);
+    w.cand = static_cast<unsigned long long*>(p_cand);
+    w.rowptr = static_cast<int32_t*>(p_rp);
+    w.rp_stride = N + 1;
     w.dense_list = static_cast<int32_t*>(p_dl);
     // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle
     c->tmX_ok = false;
@@ -386,8 +386,14 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         }));
     }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
-    CK(L.run(KID_HIST_HI, [&] { trk::k_hist_hi<<<gsel, 256, 0, s>>>(ws); }));
-    CK(L.run(KID_HIST_LO, [&] { trk::k_hist_lo<<<gsel, 256, 0, s>>>(ws); }));
+    const dim3 gflat(trk::SEL_BLOCKS_PER_PAIR, B);
+    CK(L.run(KID_HIST_HI, [&] { trk::k_hist_hi<<<gflat, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_HIST_LO, [&] { trk::k_hist_lo<<<gflat, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_ALPHA, [&] { trk::k_alpha<<<B, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_COLLECT, [&] { trk::k_collect<<<gflat, 256, 0, s>>>(ws); }));
+    CK(L.run(KID_PIVOT_SORT, [&] {
+        trk::k_pivot_sort<<<B, 1024, trk::PIV_CAP * sizeof(unsigned long long), s>>>(ws);
+    }));
     CK(L.run(KID_SEL_COUNT, [&] { trk::k_select_count<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_SCAN, [&] { trk::k_select_scan<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_EMIT, [&] { trk::k_select_emit<<<gsel, 256, 0, s>>>(ws); }));
@@ -466,6 +472,8 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
             cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_pivot_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             trk::PIV_CAP * (int)sizeof(unsigned long long)) != cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2_light<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<5>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2_light<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<8>()) !=
@@ -655,16 +663,15 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             if (needed) *needed = need;
             if (!dst) return TURBOREG_OK;
             if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
-            std::vector<int32_t> deg(n);
-            std::vector<uint32_t> e((size_t)n * (n - 1) / 2);
-            CK(cudaMemcpy(deg.data(), w.deg + pair * w.row_stride, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(e.data(), w.edges + pair * w.edges_stride, sizeof(uint32_t) * e.size(), cudaMemcpyDeviceToHost));
+            std::vector<int32_t> rp(n + 1);
+            CK(cudaMemcpy(rp.data(), w.rowptr + pair * w.rp_stride, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
+            std::vector<uint32_t> e(std::max(rp[n], 1));
+            if (rp[n]) CK(cudaMemcpy(e.data(), w.edges + pair * w.edges_stride, sizeof(uint32_t) * rp[n], cudaMemcpyDeviceToHost));
             int32_t* G = static_cast<int32_t*>(dst);
             std::memset(G, 0, need);
             for (int64_t i = 0; i < n; ++i) {
-                const int64_t off = i * n - i * (i + 1) / 2;
-                for (int k = 0; k < deg[i]; ++k) {
-                    const uint32_t v = e[off + k];
+                for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                    const uint32_t v = e[k];
                     const int64_t j = v >> 16;
                     const int32_t wt = (int32_t)(v & 0xffffu);
                     G[i * n + j] = wt;

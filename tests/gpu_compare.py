@@ -52,10 +52,11 @@ def compare_pair(tr, pair, src, dst, tau, k1, k2, thr, result=None, check_graph=
         diff = np.argwhere(g["C"] != ref["C"])
         assert len(diff) == 0, f"C differs at {len(diff)} entries, first {diff[:5].tolist()}"
         assert (g["G"] == ref["G"]).all(), f"SC2 differs at {int((g['G'] != ref['G']).sum())} entries"
-    # (i) pivots: the same set (oracle lists them in (w desc, i, j) order, the GPU lexicographically)
-    rp = sorted(map(tuple, ref["pivots"].tolist()), key=lambda x: (x[0], x[1]))
+    # (i) pivots: the same set; the GPU lists them in the oracle's (w desc, i, j) order unless > 8192 edges tie
+    # at the cut (then lexicographically)
+    rp = list(map(tuple, ref["pivots"].tolist()))
     gp = list(map(tuple, g["pivots"].tolist()))
-    assert gp == rp, f"pivots differ: {len(gp)} vs {len(rp)}"
+    assert sorted(gp) == sorted(rp), f"pivots differ: {len(gp)} vs {len(rp)}"
     # (i) cliques: the same set of (i, j, z, S)
     rc = sorted(map(tuple, ref["cliques"].tolist()))
     gc_order = np.lexsort(g["cliques"][:, ::-1].T)

@@ -113,7 +113,7 @@ def test_injected_adjacency_full_budget(tr_mod, density, seed):
     assert (G == oracle.sc2(C)).all()
     O = oracle.o2(oracle.sc2(C))
     piv = oracle.select_pivots(O, n * n)
-    assert sorted(map(tuple, piv.tolist())) == list(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
+    assert sorted(map(tuple, piv.tolist())) == sorted(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
     cl = tr.intermediate(0, I_CLIQUES)
     cl = cl[cl[:, 0] >= 0]
     assert sorted(map(tuple, cl[:, :3].tolist())) == sorted(py_triangles(C))
@@ -131,7 +131,7 @@ def test_injected_adjacency_budgets(tr_mod, k1, k2):
 
     O = oracle.o2(oracle.sc2(C))
     piv = oracle.select_pivots(O, k1)
-    assert sorted(map(tuple, piv.tolist())) == list(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
+    assert list(map(tuple, piv.tolist())) == list(map(tuple, tr.intermediate(0, I_PIVOTS).tolist()))
     ref, _ = oracle.pgs(O, piv, k2)
     cl = tr.intermediate(0, I_CLIQUES)
     cl = cl[cl[:, 0] >= 0]
@@ -148,10 +148,28 @@ def test_complete_graph_all_ties(tr_mod):
 
     piv = tr.intermediate(0, I_PIVOTS)
     lex = [(i, j) for i in range(n) for j in range(i + 1, n)][:100]
-    assert list(map(tuple, piv[:, :2].tolist())) == lex and (piv[:, 2] == n - 2).all()
+    assert list(map(tuple, piv[:, :2].tolist())) == lex and (piv[:, 2] == n - 2).all()  # (w desc, i, j) order
     cl = tr.intermediate(0, I_CLIQUES)
     O = oracle.o2(oracle.sc2(C))
     ref, _ = oracle.pgs(O, oracle.select_pivots(O, 100), 3)
+    assert sorted(map(tuple, cl[cl[:, 0] >= 0].tolist())) == sorted(map(tuple, ref.tolist()))
+
+
+@pytest.mark.parametrize("n,k1", [(70, 100), (200, 300), (200, 20000)])
+def test_complete_graph_tie_paths(tr_mod, n, k1):
+    # all weights tie: <= 8192 candidates use the candidate sort, more use the ordered count/scan/emit path;
+    # both must pick the lexicographically first K1 edges
+    C = (1 - np.eye(n)).astype(np.uint8)
+    tr = tr_mod(0.01, k1, 2, 0.1, max_n=n)
+    tr.pgs_from_adjacency(C)
+    from paper_2507_01439_b200._binding import I_CLIQUES, I_PIVOTS
+
+    piv = tr.intermediate(0, I_PIVOTS)
+    lex = [(i, j) for i in range(n) for j in range(i + 1, n)][:k1]
+    assert sorted(map(tuple, piv[:, :2].tolist())) == lex and (piv[:, 2] == n - 2).all()
+    O = oracle.o2(oracle.sc2(C))
+    ref, _ = oracle.pgs(O, oracle.select_pivots(O, k1), 2)
+    cl = tr.intermediate(0, I_CLIQUES)
     assert sorted(map(tuple, cl[cl[:, 0] >= 0].tolist())) == sorted(map(tuple, ref.tolist()))
 
 
