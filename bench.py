@@ -34,7 +34,6 @@ UNIT = "registrations/s"
 CFG = synth.CONFIGS["E"]
 PAIRS_PER_GPU = 203  # ceil(1623 / 8): the 3DMatch pair count split over the 8-GPU box
 L2_FLUSH_BYTES = 256 << 20
-POPC_PER_CLK_PER_SM = 16  # CUDA C Programming Guide arithmetic-instruction throughput table
 SMS = 148
 
 
@@ -60,7 +59,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -115,18 +114,51 @@ def make_inputs(rank, pairs, n=None, world=1):
     return src, dst, gts
 
 
-def algorithmic_work(tr, pairs):
-    """Per-kernel algorithmic units of the last call, summed over its pairs."""
+def algorithmic_work(tr, res, pairs):
+    """Algorithmic work of the last call, summed over its pairs: compat pair tests, the
+    dense tensor-core block's int8 MACs, scoring residual tests."""
     from paper_2507_01439_b200._binding import I_STATE
 
-    edges = words = tests = resid = 0
+    tests = mma_ops = edges = 0
     for p in range(pairs):
         st = tr.intermediate(p, I_STATE)
-        n = st["n"]
-        edges += st["edges"]
-        words += st["edges"] * ((n + 31) // 32)
+        n, W, h = st["n"], st["W"], st["heavy_h"]
         tests += n * (n - 1) // 2
-    return {"sc2_word_ops": words, "compat_pair_tests": tests, "edges": edges}
+        edges += st["edges"]
+        if h:
+            hp = -(-h // 256) * 256
+            tiles = sum(hp // 256 - rb // 2 for rb in range(hp // 128))
+            mma_ops += tiles * 2 * 128 * 256 * 32 * W
+    score_tests = int(sum(int(r["hypotheses_evaluated"]) for r in res)) * CFG.n
+    return {"compat_tests": tests, "mma_ops": mma_ops, "score_tests": score_tests, "edges": edges}
+
+
+def rooflines(kern, work, steps, pk, pairs):
+    """Per-kernel roofline entries (achieved algorithmic rate ÷ peak) from CUDA-event kernel times."""
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    fp32_peak = SMS * 128 * sm_max * 1e6 / 1e12  # Tops/s, one fp32 op per lane per clock
+    int8_peak = 2.0 * float(pk.get("bf16_tflops", 1590.0))  # guide's nominal int8/bf16 ratio 4.5/2.25
+    out = {}
+
+    def entry(name, bound, units, peak, unit, per_unit):
+        ms, launches = kern.get(name, (0.0, 0))
+        if not launches or not ms:
+            return
+        t = ms / launches / 1000.0
+        ach = units / t / 1e12
+        tr = ncu_traffic(name)
+        out[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                     "measured_ms_per_launch": t * 1000, "per_unit": per_unit,
+                     "traffic": (tr["dram_bytes_per_pair"] * pairs) if tr else None,
+                     "traffic_source": (tr["source"] + " (ncu --set full dram read+write per pair x pairs)") if tr else None}
+
+    entry("k_compat", "alu", work["compat_tests"] * 20, fp32_peak, "Tops/s (fp32)",
+          "20 fp32 ops of the Eq. 1 tree per pair test; N(N-1)/2 tests per pair")
+    entry("k_sc2_mma", "tensor", work["mma_ops"], int8_peak, "TOPS (int8)",
+          "2*128*256*K ops per upper MMA tile of the dense block, K = 32W")
+    entry("k_score", "alu", work["score_tests"] * 24, 2 * fp32_peak, "TFLOP/s (fp32, FMA = 2)",
+          "24 flops per residual test (12 FMA-equivalents); hypotheses x N tests per pair")
+    return out
 
 
 def cpu_sample(seconds=12.0, min_pairs=2):
@@ -292,30 +324,12 @@ def run_cuda(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    work = algorithmic_work(tr, pairs)
+    work = algorithmic_work(tr, res, pairs)
     pk = peaks()
-    sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    # dominant kernel by measured time
-    dom = max(kern.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_launches) = dom
-    avg_launch_s = dom_ms / max(dom_launches, 1) / 1000.0
-    roof = None
-    if dom_name == "k_sc2":
-        peak = POPC_PER_CLK_PER_SM * SMS * sm_max * 1e6 / 1e12  # Tword-ops/s
-        achieved = work["sc2_word_ops"] / avg_launch_s / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (32-bit AND+POPC word ops)",
-                "frac": achieved / peak, "kernel": dom_name,
-                "per_unit": "ceil(N/32) word ops per O2 edge; units per launch = Σ_pairs E_p",
-                "peak_source": f"POPC {POPC_PER_CLK_PER_SM}/clk/SM x {SMS} SMs x {sm_max:.0f} MHz (DESIGN.md)"}
-    elif dom_name == "k_compat":
-        ops_per_test = 2  # two sqrt.rn on the MUFU-fed path; see DESIGN.md
-        peak = SMS * 16 * sm_max * 1e6 / 1e12 / ops_per_test
-        achieved = work["compat_pair_tests"] / avg_launch_s / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Ttests/s", "frac": achieved / peak,
-                "kernel": dom_name}
-    if roof is not None:
-        roof["traffic"] = ncu_traffic(dom_name)
-        roof["measured_ms_per_launch"] = avg_launch_s * 1000
+    roofs = rooflines(kern, work, args.steps, pk, pairs)
+    # the roofline line describes the dominant kernel (by measured time) among those with a defined bound
+    dom_name = max(roofs, key=lambda k: kern[k][0]) if roofs else None
+    roof = dict(roofs[dom_name], kernel=dom_name) if dom_name else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -329,6 +343,7 @@ def run_cuda(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(pairs * RESULT_DTYPE.itemsize)},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "roofline_kernels": roofs,
         "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "single_pair_latency_ms": float(np.median(lat)),
         "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{pairs * world}",
@@ -341,7 +356,7 @@ def run_cuda(args, rank, world, local_rank):
 
 
 def ncu_traffic(kernel):
-    """dram bytes per launch from the committed ncu --set full summary (profiles/), or None."""
+    """{dram_bytes_per_pair, source} of `kernel` from the newest committed ncu --set full summary, or None."""
     import glob
 
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")), reverse=True):
@@ -357,7 +372,7 @@ def ncu_traffic(kernel):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--pairs", type=int, default=PAIRS_PER_GPU)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
