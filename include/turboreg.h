@@ -154,6 +154,9 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "heavy_min_rows"   minimum |H| for the dense block to be used (default 128)
  *   "heavy_min_degree" minimum degree of a heavy row (default 32)
  *   "heavy_cap"        maximum |H| (multiple of 256, <= the allocated capacity)
+ *   "sc2_variant"      bit 0: static row striding in the dense-row assembly; bit 1: warp-cooperative
+ *                      dense-neighbour counts; bit 2: tensor-core block over the non-sparse columns only,
+ *                      sparse columns added by a correction pass (default 0)
  * Returns TURBOREG_ERR_INVALID_ARGUMENT for unknown names or values. */
 turboreg_status turboreg_set_option(turboreg_ctx* ctx, const char* name, int64_t value);
 

@@ -96,7 +96,7 @@ struct WS {
     int64_t heavy_X_stride;
     int32_t heavy_Kcap;
     int32_t heavy_cap;    // max |H| (multiple of 256)
-    uint16_t* heavy_D;    // [cap][cap] X X^T
+    uint16_t* heavy_D;    // [cap][cap] X X^T (+ sparse-column correction)
     int64_t heavy_D_stride;
     int32_t heavy_min_rows, heavy_min_deg, sc2_path, sc2_variant;
     float tau, tau_base, thr;
@@ -341,7 +341,7 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
 
 // Block b of a pair owns block-rows I = b and I = T-1-b (equal work: T+1 tiles); its 8 warps sweep J.
 template <bool BASE>
-__global__ void __launch_bounds__(256) k_compat(WS ws) {
+__global__ void __launch_bounds__(256, 4) k_compat(WS ws) {
     __shared__ float4 s_rs[32];
     __shared__ float4 s_rd[32];
     __shared__ float4 s_pxy[16];
@@ -396,6 +396,7 @@ constexpr int SC2_ROWS_PER_BLOCK = 64;
 constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 64;
 constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
+constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
 template <int WPL>
 constexpr int sc2_warp_words() { return 96 * WPL + LIST_MAX / 2 + 32 * WPL; }
 template <int WPL>
@@ -948,8 +949,10 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     }
 }
 
-// X[a][k] = C[H_a][k] as uint8 0/1 for a < |H| rounded up to 256 (zero rows beyond |H|), k < 32 W: one warp
-// per X row, lane-strided words, each word → 32 bytes (two 16-byte stores, coalesced across the warp).
+// X[a][k] = C[H_a][k] as uint8 0/1 over all columns (default), or — with sc2_variant bit 2 — over
+// Kset = the non-sparse columns only (dense_list, k' < round_up(|Kset|, 128), zero columns beyond; the
+// sparse columns then come from k_light_corr).  Rows a in [|H|, round_up(|H|, 256)) are zero.  One warp
+// per X row.
 __global__ void __launch_bounds__(256) k_expand(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
@@ -961,18 +964,82 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
     if (a >= hp) return;
     const int W = d.W;
     const uint32_t* row = (a < h) ? ws.bits + p * ws.bits_stride + (int64_t)ws.heavy_list[p * ws.heavy_cap + a] * W : nullptr;
-    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
-    for (int w = lane; w < W; w += 32) {
-        const uint32_t v = row ? row[w] : 0u;
-        uint32_t b[8];
+    if (!(ws.sc2_variant & 4)) {  // full K: every column, 32 bytes per bit word (two 16-byte stores)
+        uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
+        for (int w = lane; w < W; w += 32) {
+            const uint32_t v = row ? row[w] : 0u;
+            uint32_t b[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t nib = (v >> (4 * q)) & 0xfu;
-            b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t nib = (v >> (4 * q)) & 0xfu;
+                b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
+            dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
+            dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
         }
-        uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
-        dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
-        dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
+        return;
+    }
+    const int nk = ws.st[p].n_dense, kp = (nk + MMA_BK_ - 1) / MMA_BK_ * MMA_BK_;
+    const int32_t* kset = ws.dense_list + p * ws.row_stride;
+    uint32_t* X = reinterpret_cast<uint32_t*>(ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap);
+    for (int q = lane; q < kp / 4; q += 32) {  // 4 columns per 32-bit store
+        uint32_t out = 0u;
+        if (row) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int kk = 4 * q + e;
+                if (kk < nk) {
+                    const int c = __ldg(kset + kk);
+                    out |= ((__ldg(row + (c >> 5)) >> (c & 31)) & 1u) << (8 * e);
+                }
+            }
+        }
+        X[q] = out;
+    }
+}
+
+// Σ_k C_ak C_bk over the sparse columns k the tensor-core block skipped: each sparse row k adds 1 to
+// D[hpos x][hpos y] for every pair x < y of heavy vertices in its neighbour list.  One thread per sparse row:
+// independent 16-byte list loads, the heavy positions staged in shared memory, then the pair atomics.
+constexpr int CORR_THREADS = 128;
+__global__ void __launch_bounds__(CORR_THREADS) k_light_corr(WS ws) {
+    __shared__ int16_t s_h[CORR_THREADS][LIST_MAX];
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    if (d.n == 0) return;
+    const int h = ws.st[p].heavy_h;
+    if (h == 0 || !(ws.sc2_variant & 4)) return;
+    const int kq = blockIdx.x * CORR_THREADS + threadIdx.x;
+    if (kq >= ws.st[p].n_light) return;
+    const int k = ws.light_list[p * ws.row_stride + kq];
+    const int dk = ws.deg_full[p * ws.row_stride + k];
+    const uint4* L4 = reinterpret_cast<const uint4*>(ws.lists + p * ws.lists_stride + (int64_t)k * LIST_MAX);
+    const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int16_t* mine = s_h[threadIdx.x];
+    int m = 0;
+    const int nch = (dk + 7) >> 3;
+    for (int c = 0; c < nch; ++c) {
+        const uint4 v = __ldg(L4 + c);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        int hx[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int t = 8 * c + e;
+            hx[e] = (t < dk) ? __ldg(hpos + ((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu)) : -1;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (hx[e] >= 0) mine[m++] = (int16_t)hx[e];
+    }
+    // D is uint16: add to a half of the aligned 32-bit word (entries stay < 2^15, so no carry crosses halves)
+    uint16_t* D = ws.heavy_D + p * ws.heavy_D_stride;
+    for (int x = 0; x + 1 < m; ++x) {
+        uint16_t* row = D + (int64_t)mine[x] * ws.heavy_cap;
+        for (int y = x + 1; y < m; ++y) {  // hpos ascending along L
+            const uintptr_t a = reinterpret_cast<uintptr_t>(row + mine[y]);
+            atomicAdd(reinterpret_cast<unsigned int*>(a & ~(uintptr_t)3), (a & 2) ? 0x10000u : 1u);
+        }
     }
 }
 
@@ -1303,6 +1370,42 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
     }
 }
 
+// Per-lane sorted top-KL lists (KL >= K2) merged by K2 warp argmax rounds.
+template <int KL>
+__device__ __forceinline__ int pgs_topk_list(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
+                                             const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long top[KL];
+#pragma unroll
+    for (int r = 0; r < KL; ++r) top[r] = 0ull;
+    pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
+        if (key > top[KL - 1]) {  // sorted insertion, descending
+            unsigned long long k = key;
+#pragma unroll
+            for (int r = 0; r < KL; ++r) {
+                if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
+            }
+        }
+    });
+    int emitted = 0;
+    for (int r = 0; r < K2; ++r) {
+        const unsigned long long head = top[0];
+        const unsigned long long best = warp_max_u64(head);
+        if (best == 0ull) break;
+        if (head == best) {  // keys are unique (distinct z), exactly one lane pops
+#pragma unroll
+            for (int s2 = 0; s2 < KL - 1; ++s2) top[s2] = top[s2 + 1];
+            top[KL - 1] = 0ull;
+        }
+        if (lane == 0) {
+            const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
+            out[r] = make_int4(i, j, z, (int)(best >> 32));
+        }
+        ++emitted;
+    }
+    return emitted;
+}
+
 __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
@@ -1328,34 +1431,12 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const uint32_t* ei = edges + ws.rowptr[q * ws.rp_stride + i];
     const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
     int emitted = 0;
-    if (K2 <= PGS_KL) {
-        unsigned long long top[PGS_KL];
-#pragma unroll
-        for (int r = 0; r < PGS_KL; ++r) top[r] = 0ull;
-        pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
-            if (key > top[PGS_KL - 1]) {  // sorted insertion, descending
-                unsigned long long k = key;
-#pragma unroll
-                for (int r = 0; r < PGS_KL; ++r) {
-                    if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
-                }
-            }
-        });
-        for (int r = 0; r < K2; ++r) {
-            const unsigned long long head = top[0];
-            const unsigned long long best = warp_max_u64(head);
-            if (best == 0ull) break;
-            if (head == best) {  // keys are unique (distinct z), exactly one lane pops
-#pragma unroll
-                for (int s = 0; s < PGS_KL - 1; ++s) top[s] = top[s + 1];
-                top[PGS_KL - 1] = 0ull;
-            }
-            if (lane == 0) {
-                const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
-                out[r] = make_int4(i, j, z, (int)(best >> 32));
-            }
-            ++emitted;
-        }
+    if (K2 <= 2) {
+        emitted = pgs_topk_list<2>(ri, rj, W, i, j, ei, ej, wij, K2, out);
+    } else if (K2 <= 4) {
+        emitted = pgs_topk_list<4>(ri, rj, W, i, j, ei, ej, wij, K2, out);
+    } else if (K2 <= PGS_KL) {
+        emitted = pgs_topk_list<PGS_KL>(ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else {
         unsigned long long thr = ~0ull;
         for (int r = 0; r < K2; ++r) {
@@ -1508,7 +1589,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // correspondences through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
-__global__ void __launch_bounds__(SCORE_THREADS) k_score(WS ws) {
+__global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
     __shared__ __align__(16) float4 s_src[2][SCORE_PC];
     __shared__ __align__(16) float4 s_dst[2][SCORE_PC];
     __shared__ __align__(8) unsigned long long s_bar[2];

@@ -32,6 +32,7 @@ enum KernelId {
     KID_ROWCLASS,
     KID_EXPAND,
     KID_SC2_MMA,
+    KID_LIGHT_CORR,
     KID_SC2,
     KID_SC2_LIGHT,
     KID_HIST_HI,
@@ -49,11 +50,11 @@ enum KernelId {
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
-                                       "k_expand",   "k_sc2_mma",      "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
+                                       "k_expand",   "k_sc2_mma",      "k_light_corr",  "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
                                        "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -356,6 +357,10 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
                                  s>>>(c->tmX, ws);
             }
         }));
+        if (ws.sc2_variant & 4) CK(L.run(KID_LIGHT_CORR, [&] {
+            trk::k_light_corr<<<dim3((unsigned)((maxn_batch + trk::CORR_THREADS - 1) / trk::CORR_THREADS), B),
+                                trk::CORR_THREADS, 0, s>>>(ws);
+        }));
     }
     const int wpl = (Wb + 31) / 32;
     {
@@ -503,7 +508,7 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
         if (value < 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_min_deg = (int32_t)value;
     } else if (k == "sc2_variant") {
-        if (value < 0 || value > 3) return TURBOREG_ERR_INVALID_ARGUMENT;
+        if (value < 0 || value > 7) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_sc2_variant = (int32_t)value;
     } else if (k == "heavy_cap") {
         if (value < 0 || value % 256 || value > c->heavy_cap_alloc) return TURBOREG_ERR_INVALID_ARGUMENT;

@@ -5,7 +5,7 @@
 //   X = C[H, :] as uint8 0/1 (K-major, [h][K]),  D = X · X^T  (exact: int32 accumulate, K <= 32768)
 // with tcgen05.mma kind::i8 (M=128, N=256, K=32 per instruction), operands staged by TMA
 // (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline, the accumulator in TMEM
-// (256 columns) and a 4-warp epilogue (tcgen05.ld 32x32b) that stores D as uint16 for the assemble pass.
+// (256 columns) and a 4-warp epilogue (tcgen05.ld 32x32b) that stores D as uint16 for the assembly pass.
 // Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..5 =
 // epilogue.  Which rows are heavy only changes speed, never the result (Σ_k splits exactly).
 // =====================================================================================================
@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     const int hp = (h + MMA_BN - 1) / MMA_BN * MMA_BN;
     int rb, cb;
     if (!mma_tile_coords(blockIdx.x, hp, &rb, &cb)) return;
-    const int KB = d.W * 32 / MMA_BK;  // W is a multiple of 4 ⇒ K = 32 W is a multiple of 128
+    // K = every column (32 W, a multiple of 128), or the non-sparse columns padded to 128 (sc2_variant bit 2)
+    const int KB = (ws.sc2_variant & 4) ? (ws.st[p].n_dense + MMA_BK - 1) / MMA_BK : d.W * 32 / MMA_BK;
 
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t tiles = (base + 1023u) & ~1023u;  // 1024-byte aligned for the 128B swizzle
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) k_sc2_dp4a(WS ws) {
     const int h = ws.st[p].heavy_h;
     const int a0 = blockIdx.y * 64, b0 = blockIdx.x * 64;
     if (a0 >= h || b0 >= h || b0 + 63 < a0) return;
-    const int K = d.W * 32;
+    const int K = (ws.sc2_variant & 4) ? (ws.st[p].n_dense + MMA_BK - 1) / MMA_BK * MMA_BK : d.W * 32;
     const uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     uint32_t acc[4][4] = {};

@@ -290,3 +290,16 @@ def test_compat_adversarial_threshold_ties(tr_mod, scale, tau):
     assert near > 100  # the case really is adversarial
     got = tr.bits(0)
     assert (got == ref).all(), int((got != ref).sum())
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 7])
+@pytest.mark.parametrize("key,n", [("B", 2500), ("C", 3000), ("D", 1800)])
+def test_sc2_variants_agree_with_oracle(tr_mod, variant, key, n):
+    # static striding, warp-cooperative dense counts, K-restricted tensor-core block + sparse-column correction
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=2, n=n)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n)
+    tr.set_option("sc2_variant", variant)
+    tr.set_option("heavy_min_rows", 1)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
