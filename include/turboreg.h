@@ -157,6 +157,8 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "sc2_variant"      bit 0: static row striding in the dense-row assembly; bit 1: warp-cooperative
  *                      dense-neighbour counts; bit 2: tensor-core block over the non-sparse columns only,
  *                      sparse columns added by a correction pass (default 0)
+ *   "compat_variant"   compat-graph tiling: 0 = row pairs in f32x2 lanes x 2 column tiles per warp
+ *                      (default); 1 = column pairs x 2 tiles; 2 = row pairs x 1 column tile
  * Returns TURBOREG_ERR_INVALID_ARGUMENT for unknown names or values. */
 turboreg_status turboreg_set_option(turboreg_ctx* ctx, const char* name, int64_t value);
 

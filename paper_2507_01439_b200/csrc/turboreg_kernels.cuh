@@ -157,10 +157,11 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
 }
 
 // ------------------------------------------------------------------------------------------ a2 compat
-// Eq. 1 on 32×32 tiles of the upper block triangle.  One warp per tile (I ≤ J): lane l owns
-// column point J*32+l; the 32 row points I*32+r are staged in shared memory and read as broadcasts.  Each
-// test is evaluated once: the ballot over lanes is row word (I*32+r, J), the lane's own bit accumulation
-// the mirrored column word (J*32+l, I) — exact because IEEE subtraction is antisymmetric.
+// Eq. 1 on 32×32 tiles of the upper block triangle.  One warp per pair of adjacent tiles
+// (I, J), (I, J+1), J >= I: lane l owns column points J*32+l and J*32+32+l; the 32 row points I*32+r are
+// staged in shared memory and read as broadcasts.  Each test is evaluated once: the lane's own bit
+// accumulation is the column word (c, I), its warp transpose the row word (I*32+r, J) — exact because
+// IEEE subtraction is antisymmetric.
 //
 // The decision must equal the oracle's float32 tree bit for bit: a = sqrt.rn((dx*dx + dy*dy) + dz*dz),
 // b likewise, edge ⇔ |a - b| <= τ (readings r1, r2).  Two correctly rounded square roots per test are
@@ -200,6 +201,8 @@ __device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
 }
 __device__ __forceinline__ uint32_t f2_lo(f2_t v) { return (uint32_t)v; }
 __device__ __forceinline__ uint32_t f2_hi(f2_t v) { return (uint32_t)(v >> 32); }
+__device__ __forceinline__ float lo_f(f2_t v) { return __uint_as_float(f2_lo(v)); }
+__device__ __forceinline__ float hi_f(f2_t v) { return __uint_as_float(f2_hi(v)); }
 
 // Warp-level 32×32 bit-matrix transpose: lane l holds row l (bit b = column b); returns column l.
 __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
@@ -215,12 +218,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
     return x;
 }
 
-// One 32×32 tile (I, J >= I) by one warp; the block's 32 row points are staged in shared memory, packed
-// as row pairs (x_{2k}, x_{2k+1}, y_{2k}, y_{2k+1}) / (z_{2k}, z_{2k+1}) so one f32x2 op serves two tests.
-template <bool BASE>
-__device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, int T, int I, int J,
-                                            const float4* s_rs, const float4* s_rd, const float4* s_pxy,
-                                            const float2* s_pz, const float4* s_qxy, const float2* s_qz) {
+// One 32×32 tile (I, J >= I) by one warp, with the optional τ_base plane (r19): both planes need the exact
+// tree value of |a − b|, so this path evaluates it directly (lane = column, rows broadcast from shared memory).
+__device__ __forceinline__ void compat_tile_base(const WS& ws, int p, int n, int W, int T, int I, int J,
+                                                 const float4* s_rs, const float4* s_rd) {
     const int lane = threadIdx.x & 31;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
     const float4* d4 = ws.dst4 + p * ws.pts_stride;
@@ -239,83 +240,18 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
     uint32_t okr = rv ? cvb : 0u;
     if (I == J) { okc &= ~(1u << lane); okr &= ~(1u << lane); }
     uint32_t colw = 0, roww = 0, colb = 0, rowb = 0;
-    if (!BASE) {
-        const float t2 = __fmul_rn(tau, tau);
-        const f2_t t2x2 = f2_pack(t2, t2);
-        const float m2t2 = -2.0f * t2;
-        const float t4 = __fmul_rn(t2, t2);
-        const f2_t m2t2x2 = f2_pack(m2t2, m2t2), t4x2 = f2_pack(t4, t4);
-        const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), c19 = f2_pack(0x1p-19f, 0x1p-19f);
-        const f2_t mone = f2_pack(-1.0f, -1.0f);
-        const f2_t ncx = f2_pack(-cs.x, -cs.x), ncy = f2_pack(-cs.y, -cs.y), ncz = f2_pack(-cs.z, -cs.z);
-        const f2_t ndx = f2_pack(-cd.x, -cd.x), ndy = f2_pack(-cd.y, -cd.y), ndz = f2_pack(-cd.z, -cd.z);
-        const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
-        const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
-        const f2_t nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
-        // Sign-bit algebra per test (bit 31 of each float word):
-        //   a = S − s_lo  (< 0 ⇔ sure edge),  c = s_hi − S  (< 0 ⇔ S > s_hi),
-        //   b = |q| − Tq  computed as (−Tq) + |q| ... sign set ⇔ |q| < Tq, so sure_q ⇔ ~b & c,
-        //   edge = a | (sure_q & q<0),  all-sure accumulator &= a | sure_q.
-        uint32_t sacc = 0xffffffffu;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const float4 P = s_pxy[k];
-            const float2 Pz = s_pz[k];
-            const float4 Q = s_qxy[k];
-            const float2 Qz = s_qz[k];
-            const f2_t dx = f2_add(f2_pack(P.x, P.y), ncx), dy = f2_add(f2_pack(P.z, P.w), ncy);
-            const f2_t dz = f2_add(f2_pack(Pz.x, Pz.y), ncz);
-            const f2_t ex = f2_add(f2_pack(Q.x, Q.y), ndx), ey = f2_add(f2_pack(Q.z, Q.w), ndy);
-            const f2_t ez = f2_add(f2_pack(Qz.x, Qz.y), ndz);
-            const f2_t A = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
-            const f2_t B = f2_fma(ez, ez, f2_fma(ey, ey, f2_mul(ex, ex)));
-            const f2_t S = f2_add(A, B);
-            const f2_t D = f2_fma(B, mone, A);
-            const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
-            const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
-            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
-            const f2_t a = f2_add(S, ns_lo2);
-            const f2_t cc = f2_fma(S, mone, s_hi2);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t av = h ? f2_hi(a) : f2_lo(a), bv = h ? f2_hi(b) : f2_lo(b);
-                const uint32_t cv2 = h ? f2_hi(cc) : f2_lo(cc), qv = h ? f2_hi(q) : f2_lo(q);
-                const uint32_t sq = ~bv & cv2;        // sure_q in bit 31 (|q| > Tq and S > s_hi)
-                const uint32_t e = av | (sq & qv);    // edge in bit 31
-                sacc &= av | sq;                      // bit 31 stays set while every test is decided
-                colw = __funnelshift_l(e, colw, 1);   // colw = colw << 1 | e >> 31 (bit-reversed order)
-            }
-        }
-        colw = __brev(colw);
-        const bool unsure_any = (int32_t)sacc >= 0;
-        if (__any_sync(FULL, unsure_any)) {  // rare: redo this lane's 32 tests with the exact tree
-            if (unsure_any) {
-                colw = 0u;
-                for (int r = 0; r < 32; ++r) {
-                    const float4 ps = s_rs[r];
-                    const float4 pd = s_rd[r];
-                    const float a = f32_dist(ps.x, ps.y, ps.z, cs.x, cs.y, cs.z);
-                    const float b = f32_dist(pd.x, pd.y, pd.z, cd.x, cd.y, cd.z);
-                    colw |= (fabsf(__fsub_rn(a, b)) <= tau) ? (1u << r) : 0u;
-                }
-            }
-        }
-        roww = transpose32(colw);
-    } else {
-        for (int r = 0; r < 32; ++r) {
-            const float4 ps = s_rs[r];
-            const float4 pd = s_rd[r];
-            const float a = f32_dist(ps.x, ps.y, ps.z, cs.x, cs.y, cs.z);
-            const float b = f32_dist(pd.x, pd.y, pd.z, cd.x, cd.y, cd.z);
-            const float delta = fabsf(__fsub_rn(a, b));
-            const bool e = delta <= tau, eb = delta <= taub;
-            colw |= e ? (1u << r) : 0u;
-            colb |= eb ? (1u << r) : 0u;
-            const uint32_t bal = __ballot_sync(FULL, e), balb = __ballot_sync(FULL, eb);
-            roww = (lane == r) ? bal : roww;
-            rowb = (lane == r) ? balb : rowb;
-        }
+    for (int r = 0; r < 32; ++r) {
+        const float4 ps = s_rs[r];
+        const float4 pd = s_rd[r];
+        const float a = f32_dist(ps.x, ps.y, ps.z, cs.x, cs.y, cs.z);
+        const float b = f32_dist(pd.x, pd.y, pd.z, cd.x, cd.y, cd.z);
+        const float delta = fabsf(__fsub_rn(a, b));
+        const bool e = delta <= tau, eb = delta <= taub;
+        colw |= e ? (1u << r) : 0u;
+        colb |= eb ? (1u << r) : 0u;
+        const uint32_t bal = __ballot_sync(FULL, e), balb = __ballot_sync(FULL, eb);
+        roww = (lane == r) ? bal : roww;
+        rowb = (lane == r) ? balb : rowb;
     }
     colw &= okc;
     roww &= okr;
@@ -324,7 +260,7 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
     if (cv) bits[(int64_t)c * W + I] = colw;
     if (I == J && rv)
         for (int w = T; w < W; ++w) bits[(int64_t)r0 * W + w] = 0u;
-    if (BASE) {
+    {
         colb &= okc;
         rowb &= okr;
         uint32_t* bb = ws.bits_base + p * ws.bits_stride;
@@ -340,14 +276,242 @@ __device__ __forceinline__ void compat_tile(const WS& ws, int p, int n, int W, i
 }
 
 // Block b of a pair owns block-rows I = b and I = T-1-b (equal work: T+1 tiles); its 8 warps sweep J.
-template <bool BASE>
-__global__ void __launch_bounds__(256, 4) k_compat(WS ws) {
-    __shared__ float4 s_rs[32];
-    __shared__ float4 s_rd[32];
-    __shared__ float4 s_pxy[16];
-    __shared__ float2 s_pz[16];
-    __shared__ float4 s_qxy[16];
-    __shared__ float2 s_qz[16];
+// Two adjacent 32×32 tiles (I, J) and (I, J+1) by one warp, J >= I: lane l owns column points
+// c0 = J*32+l and c1 = c0+32, packed as one f32x2 lane pair, so each row point (a shared-memory broadcast,
+// stored negated) serves two tests per f32x2 op and the row loads are amortised over 64 columns.  The
+// arithmetic per test is the same op for op in every tiling (same FMAs, same rounding): only the packing
+// differs, so DESIGN.md §6.1's proof covers all of them.
+template <int NP, int UNR>
+__device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, int T, int I, int J,
+                                             const float4* s_rs, const float4* s_rd, const float4* s_nr,
+                                             const float4* s_nd, f2_t* s_col) {
+    constexpr int NT = 2 * NP;  // tiles (I, J) .. (I, J+NT-1); lane column k: (J+k)*32 + lane
+    const int lane = threadIdx.x & 31;
+    const float4* s4 = ws.src4 + p * ws.pts_stride;
+    const float4* d4 = ws.dst4 + p * ws.pts_stride;
+    const int r0 = I * 32 + lane;
+    const bool rv = r0 < n;
+    const float tau = ws.tau;
+    const int rmax = min(32, n - I * 32);
+    const uint32_t rmask = rmax >= 32 ? 0xffffffffu : ((1u << rmax) - 1u);
+    // the column pairs (k = 2m, 2m+1) go through the warp's shared-memory slot so each arrives as one
+    // 64-bit load and stays an aligned register pair for the whole loop (ptxas re-packs scalar-built pairs
+    // on every use)
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+        const int c = (J + k) * 32 + lane;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 cs = c < n ? s4[c] : z4, cd = c < n ? d4[c] : z4;
+        float* sc = reinterpret_cast<float*>(s_col) + (k & 1);
+        sc[2 * ((0 * NP + (k >> 1)) * 32 + lane)] = cs.x;
+        sc[2 * ((1 * NP + (k >> 1)) * 32 + lane)] = cs.y;
+        sc[2 * ((2 * NP + (k >> 1)) * 32 + lane)] = cs.z;
+        sc[2 * ((3 * NP + (k >> 1)) * 32 + lane)] = cd.x;
+        sc[2 * ((4 * NP + (k >> 1)) * 32 + lane)] = cd.y;
+        sc[2 * ((5 * NP + (k >> 1)) * 32 + lane)] = cd.z;
+    }
+    __syncwarp();
+    f2_t CX[NP], CY[NP], CZ[NP], DX[NP], DY[NP], DZ[NP];
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+        CX[m] = s_col[(0 * NP + m) * 32 + lane];
+        CY[m] = s_col[(1 * NP + m) * 32 + lane];
+        CZ[m] = s_col[(2 * NP + m) * 32 + lane];
+        DX[m] = s_col[(3 * NP + m) * 32 + lane];
+        DY[m] = s_col[(4 * NP + m) * 32 + lane];
+        DZ[m] = s_col[(5 * NP + m) * 32 + lane];
+    }
+    const float t2 = __fmul_rn(tau, tau);
+    const float t4 = __fmul_rn(t2, t2);
+    const f2_t t2x2 = f2_pack(t2, t2), m2t2x2 = f2_pack(-2.0f * t2, -2.0f * t2), t4x2 = f2_pack(t4, t4);
+    const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
+    const f2_t mone = f2_pack(-1.0f, -1.0f);
+    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
+    const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
+    // per test, in bit 31:  a: S < s_lo (sure edge);  cc: S > s_hi (q decides);  b: |q| < Tq (q unsure);
+    // q: q < 0.  decided x = a | (~b & cc);  edge e = x & (a | q);  sacc keeps bit 31 while all decided.
+    uint32_t colw[NT], sacc = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) colw[k] = 0u;
+#pragma unroll UNR
+    for (int r = 0; r < 32; ++r) {
+        const float4 R = s_nr[r];
+        const float4 Q = s_nd[r];
+#pragma unroll
+        for (int m = 0; m < NP; ++m) {
+            const f2_t dx = f2_add(CX[m], f2_pack(R.x, R.x)), dy = f2_add(CY[m], f2_pack(R.y, R.y));
+            const f2_t dz = f2_add(CZ[m], f2_pack(R.z, R.z));
+            const f2_t ex = f2_add(DX[m], f2_pack(Q.x, Q.x)), ey = f2_add(DY[m], f2_pack(Q.y, Q.y));
+            const f2_t ez = f2_add(DZ[m], f2_pack(Q.z, Q.z));
+            const f2_t A = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+            const f2_t B = f2_fma(ez, ez, f2_fma(ey, ey, f2_mul(ex, ex)));
+            const f2_t S = f2_add(A, B);
+            const f2_t D = f2_fma(B, mone, A);
+            const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
+            const f2_t absD = D & 0x7fffffff7fffffffull;
+            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
+            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
+            const f2_t a = f2_add(S, ns_lo2), cc = f2_fma(S, mone, s_hi2);
+            const uint32_t a0 = f2_lo(a), a1 = f2_hi(a), k0 = f2_lo(cc), k1 = f2_hi(cc);
+            const uint32_t x0 = a0 | (~f2_lo(b) & k0), x1 = a1 | (~f2_hi(b) & k1);
+            colw[2 * m] = __funnelshift_l(x0 & (a0 | f2_lo(q)), colw[2 * m], 1);
+            colw[2 * m + 1] = __funnelshift_l(x1 & (a1 | f2_hi(q)), colw[2 * m + 1], 1);
+            sacc &= x0 & x1;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NT; ++k) colw[k] = __brev(colw[k]);
+    const bool unsure_any = (int32_t)sacc >= 0;
+    if (__any_sync(FULL, unsure_any)) {  // rare: redo this lane's tests with the exact tree
+        if (unsure_any) {
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+                uint32_t w0 = 0u, w1 = 0u;
+                for (int r = 0; r < 32; ++r) {
+                    const float4 ps = s_rs[r];
+                    const float4 pd = s_rd[r];
+                    const float a0 = f32_dist(ps.x, ps.y, ps.z, lo_f(CX[m]), lo_f(CY[m]), lo_f(CZ[m]));
+                    const float b0 = f32_dist(pd.x, pd.y, pd.z, lo_f(DX[m]), lo_f(DY[m]), lo_f(DZ[m]));
+                    const float a1 = f32_dist(ps.x, ps.y, ps.z, hi_f(CX[m]), hi_f(CY[m]), hi_f(CZ[m]));
+                    const float b1 = f32_dist(pd.x, pd.y, pd.z, hi_f(DX[m]), hi_f(DY[m]), hi_f(DZ[m]));
+                    w0 |= (fabsf(__fsub_rn(a0, b0)) <= tau) ? (1u << r) : 0u;
+                    w1 |= (fabsf(__fsub_rn(a1, b1)) <= tau) ? (1u << r) : 0u;
+                }
+                colw[2 * m] = w0;
+                colw[2 * m + 1] = w1;
+            }
+        }
+    }
+    uint32_t* bits = ws.bits + p * ws.bits_stride;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+        const int c = (J + k) * 32 + lane;
+        const bool cv = c < n;
+        uint32_t okc = cv ? rmask : 0u;
+        const uint32_t cvb = __ballot_sync(FULL, cv);  // every lane votes (never inside a conditional)
+        uint32_t okr = rv ? cvb : 0u;
+        if (I == J + k) { okc &= ~(1u << lane); okr &= ~(1u << lane); }
+        const uint32_t cw = colw[k] & okc;
+        const uint32_t rw = transpose32(cw) & okr;
+        if (rv && J + k < T) bits[(int64_t)r0 * W + J + k] = rw;
+        if (cv) bits[(int64_t)c * W + I] = cw;
+    }
+    if (I == J && rv)
+        for (int w = T; w < W; ++w) bits[(int64_t)r0 * W + w] = 0u;
+}
+
+// Row-pair packing: the f32x2 lanes hold two row points (2k, 2k+1) of tile row I (negated, from shared
+// memory, one LDS.128 + one LDS.64 per coordinate triple), each lane's NC column points are scalar
+// broadcast operands held in registers.  Same per-test arithmetic as compat_tiles.
+template <int NC, int UNR>
+__device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int W, int T, int I, int J,
+                                                const float4* s_rs, const float4* s_rd, const float4* s_pxy,
+                                                const float2* s_pz, const float4* s_qxy, const float2* s_qz) {
+    const int lane = threadIdx.x & 31;
+    const float4* s4 = ws.src4 + p * ws.pts_stride;
+    const float4* d4 = ws.dst4 + p * ws.pts_stride;
+    const int r0 = I * 32 + lane;
+    const bool rv = r0 < n;
+    const float tau = ws.tau;
+    const int rmax = min(32, n - I * 32);
+    const uint32_t rmask = rmax >= 32 ? 0xffffffffu : ((1u << rmax) - 1u);
+    float4 cs[NC], cd[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const int c = (J + k) * 32 + lane;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        cs[k] = c < n ? s4[c] : z4;
+        cd[k] = c < n ? d4[c] : z4;
+    }
+    const float t2 = __fmul_rn(tau, tau);
+    const float t4 = __fmul_rn(t2, t2);
+    const f2_t t2x2 = f2_pack(t2, t2), m2t2x2 = f2_pack(-2.0f * t2, -2.0f * t2), t4x2 = f2_pack(t4, t4);
+    const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
+    const f2_t mone = f2_pack(-1.0f, -1.0f);
+    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
+    const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
+    uint32_t colw[NC], sacc = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) colw[k] = 0u;
+#pragma unroll UNR
+    for (int kk = 0; kk < 16; ++kk) {
+        const float4 P = s_pxy[kk];
+        const float2 Pz = s_pz[kk];
+        const float4 Q = s_qxy[kk];
+        const float2 Qz = s_qz[kk];
+        const f2_t px = f2_pack(P.x, P.y), py = f2_pack(P.z, P.w), pz = f2_pack(Pz.x, Pz.y);
+        const f2_t qx = f2_pack(Q.x, Q.y), qy = f2_pack(Q.z, Q.w), qz = f2_pack(Qz.x, Qz.y);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            const f2_t dx = f2_add(px, f2_pack(cs[k].x, cs[k].x)), dy = f2_add(py, f2_pack(cs[k].y, cs[k].y));
+            const f2_t dz = f2_add(pz, f2_pack(cs[k].z, cs[k].z));
+            const f2_t ex = f2_add(qx, f2_pack(cd[k].x, cd[k].x)), ey = f2_add(qy, f2_pack(cd[k].y, cd[k].y));
+            const f2_t ez = f2_add(qz, f2_pack(cd[k].z, cd[k].z));
+            const f2_t A = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+            const f2_t B = f2_fma(ez, ez, f2_fma(ey, ey, f2_mul(ex, ex)));
+            const f2_t S = f2_add(A, B);
+            const f2_t D = f2_fma(B, mone, A);
+            const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
+            const f2_t absD = D & 0x7fffffff7fffffffull;
+            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
+            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
+            const f2_t a = f2_add(S, ns_lo2), cc = f2_fma(S, mone, s_hi2);
+            const uint32_t a0 = f2_lo(a), a1 = f2_hi(a), k0 = f2_lo(cc), k1 = f2_hi(cc);
+            const uint32_t x0 = a0 | (~f2_lo(b) & k0), x1 = a1 | (~f2_hi(b) & k1);
+            colw[k] = __funnelshift_l(x0 & (a0 | f2_lo(q)), colw[k], 1);
+            colw[k] = __funnelshift_l(x1 & (a1 | f2_hi(q)), colw[k], 1);
+            sacc &= x0 & x1;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) colw[k] = __brev(colw[k]);
+    const bool unsure_any = (int32_t)sacc >= 0;
+    if (__any_sync(FULL, unsure_any)) {  // rare: redo this lane's tests with the exact tree
+        if (unsure_any) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                uint32_t w0 = 0u;
+                for (int r = 0; r < 32; ++r) {
+                    const float4 ps = s_rs[r];
+                    const float4 pd = s_rd[r];
+                    const float a0 = f32_dist(ps.x, ps.y, ps.z, cs[k].x, cs[k].y, cs[k].z);
+                    const float b0 = f32_dist(pd.x, pd.y, pd.z, cd[k].x, cd[k].y, cd[k].z);
+                    w0 |= (fabsf(__fsub_rn(a0, b0)) <= tau) ? (1u << r) : 0u;
+                }
+                colw[k] = w0;
+            }
+        }
+    }
+    uint32_t* bits = ws.bits + p * ws.bits_stride;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        const int c = (J + k) * 32 + lane;
+        const bool cv = c < n;
+        uint32_t okc = cv ? rmask : 0u;
+        const uint32_t cvb = __ballot_sync(FULL, cv);  // every lane votes (never inside a conditional)
+        uint32_t okr = rv ? cvb : 0u;
+        if (I == J + k) { okc &= ~(1u << lane); okr &= ~(1u << lane); }
+        const uint32_t cw = colw[k] & okc;
+        const uint32_t rw = transpose32(cw) & okr;
+        if (rv && J + k < T) bits[(int64_t)r0 * W + J + k] = rw;
+        if (cv) bits[(int64_t)c * W + I] = cw;
+    }
+    if (I == J && rv)
+        for (int w = T; w < W; ++w) bits[(int64_t)r0 * W + w] = 0u;
+}
+
+template <bool BASE, int MINB = 4, int UNR = 8, int NP = 1>
+__global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
+    __shared__ float4 s_rs[64];
+    __shared__ float4 s_rd[64];
+    __shared__ float4 s_pxy[2][16];
+    __shared__ float2 s_pz[2][16];
+    __shared__ float4 s_qxy[2][16];
+    __shared__ float2 s_qz[2][16];
+    __shared__ float4 s_nr[64];
+    __shared__ float4 s_nd[64];
+    __shared__ f2_t s_col[8][6 * 32 * (NP > 0 ? NP : 1)];
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -359,26 +523,61 @@ __global__ void __launch_bounds__(256, 4) k_compat(WS ws) {
     const int warp = threadIdx.x >> 5;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
     const float4* d4 = ws.dst4 + p * ws.pts_stride;
-    for (int half = 0; half < 2; ++half) {
-        const int I = half == 0 ? b : T - 1 - b;
-        if (half == 1 && I == b) break;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int t = threadIdx.x, r0 = I * 32 + t;
+    if constexpr (BASE) {
+        for (int half = 0; half < 2; ++half) {
+            const int I = half == 0 ? b : T - 1 - b;
+            if (half == 1 && I == b) break;
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const int t = threadIdx.x, r0 = I * 32 + t;
+                const float4 a = r0 < n ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 q = r0 < n ? d4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
+                s_rs[t] = a;
+                s_rd[t] = q;
+            }
+            __syncthreads();
+            for (int J = I + warp; J < T; J += 8)
+                compat_tile_base(ws, p, n, W, T, I, J, s_rs, s_rd);
+        }
+    } else {
+        // block-rows I0 = b and I1 = T-1-b (T+1 tiles together, so every block has the same work) are
+        // staged at once and their tile pairs dealt to the 8 warps as one list: no barrier between them
+        const int I0 = b, I1 = T - 1 - b;
+        if (threadIdx.x < 64) {
+            const int t = threadIdx.x, I = t < 32 ? I0 : I1, r0 = I * 32 + (t & 31);
             const float4 a = r0 < n ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
             const float4 q = r0 < n ? d4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
             s_rs[t] = a;
             s_rd[t] = q;
-            float* pxy = reinterpret_cast<float*>(s_pxy) + 4 * (t >> 1) + (t & 1);
-            float* qxy = reinterpret_cast<float*>(s_qxy) + 4 * (t >> 1) + (t & 1);
-            pxy[0] = a.x; pxy[2] = a.y;
-            qxy[0] = q.x; qxy[2] = q.y;
-            reinterpret_cast<float*>(s_pz)[t] = a.z;
-            reinterpret_cast<float*>(s_qz)[t] = q.z;
+            s_nr[t] = make_float4(-a.x, -a.y, -a.z, 0.f);
+            s_nd[t] = make_float4(-q.x, -q.y, -q.z, 0.f);
+            const int h = t >> 5, u = t & 31;
+            float* pxy = reinterpret_cast<float*>(s_pxy[h]) + 4 * (u >> 1) + (u & 1);
+            float* qxy = reinterpret_cast<float*>(s_qxy[h]) + 4 * (u >> 1) + (u & 1);
+            pxy[0] = -a.x; pxy[2] = -a.y;
+            qxy[0] = -q.x; qxy[2] = -q.y;
+            reinterpret_cast<float*>(s_pz[h])[u] = -a.z;
+            reinterpret_cast<float*>(s_qz[h])[u] = -q.z;
         }
         __syncthreads();
-        for (int J = I + warp; J < T; J += 8)
-            compat_tile<BASE>(ws, p, n, W, T, I, J, s_rs, s_rd, s_pxy, s_pz, s_qxy, s_qz);
+        if constexpr (NP < 0) {
+            constexpr int NC = -NP;
+            const int P0 = (T - I0 + NC - 1) / NC, P1 = (I1 != I0) ? (T - I1 + NC - 1) / NC : 0;
+            for (int t = warp; t < P0 + P1; t += 8) {
+                const bool second = t >= P0;
+                const int I = second ? I1 : I0, J = I + NC * (second ? t - P0 : t), o = second ? 32 : 0, h = second;
+                compat_tiles_rp<NC, UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_pxy[h], s_pz[h], s_qxy[h],
+                                         s_qz[h]);
+            }
+            return;
+        }
+        constexpr int NT = 2 * (NP > 0 ? NP : 1);
+        const int P0 = (T - I0 + NT - 1) / NT, P1 = (I1 != I0) ? (T - I1 + NT - 1) / NT : 0;
+        for (int t = warp; t < P0 + P1; t += 8) {
+            const bool second = t >= P0;
+            const int I = second ? I1 : I0, J = I + NT * (second ? t - P0 : t), o = second ? 32 : 0;
+            compat_tiles<(NP > 0 ? NP : 1), UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_nr + o, s_nd + o, s_col[warp]);
+        }
     }
 }
 
@@ -818,6 +1017,20 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
 constexpr int SEL_BLOCKS_PER_PAIR = 32;
 
 // Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4).
+// The three edge passes below stream the pair's compact O2 edge array (edges_stride is a multiple of 4
+// words) as uint4: EDGE_VEC edges per thread per round, all loads issued before any is consumed.
+constexpr int EDGE_VEC = 8;
+__device__ __forceinline__ void load_edges8(const uint32_t* edges, int e, int E, uint32_t (&v)[EDGE_VEC]) {
+    if (e + EDGE_VEC <= E) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(edges + e));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(edges + e) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) v[k] = (e + k < E) ? __ldg(edges + e + k) : 0u;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
     __shared__ int s_hist[256];
     const int p = blockIdx.y;
@@ -827,16 +1040,23 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
     for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
     __syncthreads();
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
-    const int lane = threadIdx.x & 31;
-    for (int e0 = blockIdx.x * blockDim.x; e0 < E; e0 += gridDim.x * blockDim.x) {
-        const int e = e0 + threadIdx.x;
-        // consecutive weights come from one row and cluster in one bin: lanes sharing lane 0's bin add once
-        const uint32_t w = (e < E) ? (__ldg(edges + e) & 0xffffu) : 0u;
-        const int bin = w ? (int)(w >> 7) : -1;
-        const int b0 = __shfl_sync(FULL, bin, 0);
-        const unsigned same = __ballot_sync(FULL, bin == b0 && bin >= 0);
-        if (lane == 0 && same) atomicAdd(&s_hist[b0], __popc(same));
-        if (bin >= 0 && bin != b0) atomicAdd(&s_hist[bin], 1);
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; e < E; e += gridDim.x * blockDim.x * EDGE_VEC) {
+        uint32_t v[EDGE_VEC];
+        load_edges8(edges, e, E, v);
+        // consecutive weights come from one row and cluster in one bin: add runs, not single edges
+        int run_bin = -1, run = 0;
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) {
+            const uint32_t w = v[k] & 0xffffu;
+            const int bin = w ? (int)(w >> 7) : -1;
+            if (bin != run_bin) {
+                if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
+                run_bin = bin;
+                run = 0;
+            }
+            ++run;
+        }
+        if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x)
@@ -846,6 +1066,7 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
 // ------------------------------------------------------------------------------------------ a3 heavy split
 // Full degrees (popcount of each bit row), their sum and maximum, and the sorted uint16 neighbour list of
 // every row with degree <= LIST_MAX (zero-padded to a 16-byte chunk); one warp per row.
+constexpr int DEG_GROUP = 8;
 __global__ void __launch_bounds__(256) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
@@ -863,21 +1084,34 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
     uint16_t* lists = ws.lists + p * ws.lists_stride;
     for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
         uint16_t* L = lists + (int64_t)i * LIST_MAX;
+        const uint32_t* ri = bits + (int64_t)i * W;
         int carry = 0;
         unsigned ucnt = 0;
-        for (int c = 0; c * 32 < W; ++c) {
-            const int w = c * 32 + lane;
-            uint32_t v = (w < W) ? bits[(int64_t)i * W + w] : 0u;
-            ucnt += __popc(upper_mask(v, w, i));
-            const int cnt = __popc(v);
-            const int incl = warp_incl_scan(cnt);
-            int pos = carry + incl - cnt;
-            while (v && pos < LIST_MAX) {
-                const int b = __ffs(v) - 1;
-                v &= v - 1u;
-                L[pos++] = (uint16_t)(w * 32 + b);
+        // DEG_GROUP words per lane are loaded before any is used, so a warp keeps a whole row (n <= 8192)
+        // in flight instead of one dependent 128-byte load per round
+        for (int c0 = 0; c0 * 32 < W; c0 += DEG_GROUP) {
+            uint32_t vv[DEG_GROUP];
+#pragma unroll
+            for (int k = 0; k < DEG_GROUP; ++k) {
+                const int w = (c0 + k) * 32 + lane;
+                vv[k] = (w < W) ? __ldg(ri + w) : 0u;
             }
-            carry += __shfl_sync(FULL, incl, 31);
+#pragma unroll
+            for (int k = 0; k < DEG_GROUP; ++k) {
+                if ((c0 + k) * 32 >= W) break;
+                const int w = (c0 + k) * 32 + lane;
+                uint32_t v = vv[k];
+                ucnt += __popc(upper_mask(v, w, i));
+                const int cnt = __popc(v);
+                const int incl = warp_incl_scan(cnt);
+                int pos = carry + incl - cnt;
+                while (v && pos < LIST_MAX) {
+                    const int b = __ffs(v) - 1;
+                    v &= v - 1u;
+                    L[pos++] = (uint16_t)(w * 32 + b);
+                }
+                carry += __shfl_sync(FULL, incl, 31);
+            }
         }
         if (carry <= LIST_MAX)
             for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
@@ -1099,9 +1333,14 @@ __global__ void __launch_bounds__(256) k_hist_lo(WS ws) {
     __syncthreads();
     const int E = st->edges;
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        const uint32_t w = __ldg(edges + e) & 0xffffu;
-        if (w && (int)(w >> 7) == b1) atomicAdd(&s_lo[w & 127u], 1);
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; e < E; e += gridDim.x * blockDim.x * EDGE_VEC) {
+        uint32_t v[EDGE_VEC];
+        load_edges8(edges, e, E, v);
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) {
+            const uint32_t w = v[k] & 0xffffu;
+            if (w && (int)(w >> 7) == b1) atomicAdd(&s_lo[w & 127u], 1);
+        }
     }
     __syncthreads();
     for (int b = threadIdx.x; b < 128; b += blockDim.x)
@@ -1144,26 +1383,36 @@ __global__ void __launch_bounds__(256) k_collect(WS ws) {
     const int32_t* rp = ws.rowptr + p * ws.rp_stride;
     unsigned long long* cand = ws.cand + (int64_t)p * PIV_CAP;
     const int lane = threadIdx.x & 31;
-    for (int e0 = blockIdx.x * blockDim.x; e0 < E; e0 += gridDim.x * blockDim.x) {
-        const int e = e0 + threadIdx.x;
-        const uint32_t v = (e < E) ? __ldg(edges + e) : 0u;
-        const int w = (int)(v & 0xffffu);
-        const bool c = e < E && w >= alpha && w > 0;
-        const unsigned b = __ballot_sync(FULL, c);
-        if (!b) continue;
-        const int leader = __ffs(b) - 1;
+    for (int e0 = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; __any_sync(FULL, e0 < E);
+         e0 += gridDim.x * blockDim.x * EDGE_VEC) {
+        uint32_t v[EDGE_VEC];
+        load_edges8(edges, e0, E, v);  // zero past E: weight 0 never qualifies
+        unsigned m = 0;
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) {
+            const int w = (int)(v[k] & 0xffffu);
+            m |= (w >= alpha && w > 0) ? (1u << k) : 0u;
+        }
+        const int cnt = __popc(m);
+        const int incl = warp_incl_scan(cnt);
+        const int tot = __shfl_sync(FULL, incl, 31);
+        if (tot == 0) continue;
         int base = 0;
-        if (lane == leader) base = atomicAdd(&st->ncand, __popc(b));
-        base = __shfl_sync(FULL, base, leader);
-        if (c) {
+        if (lane == 0) base = atomicAdd(&st->ncand, tot);
+        base = __shfl_sync(FULL, base, 0) + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) {
+            if (!((m >> k) & 1u)) continue;
+            const int e = e0 + k;
             int lo = 0, hi = n;  // row of edge e: rp[lo] <= e < rp[hi]
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
                 if (__ldg(rp + mid) <= e) lo = mid; else hi = mid;
             }
-            const int slot = base + __popc(b & ((1u << lane) - 1u));
+            const int slot = base++;
             if (slot < PIV_CAP)
-                cand[slot] = ((unsigned long long)(0x7fff - w) << 30) | ((unsigned long long)lo << 15) | (v >> 16);
+                cand[slot] = ((unsigned long long)(0x7fff - (int)(v[k] & 0xffffu)) << 30) |
+                             ((unsigned long long)lo << 15) | (v[k] >> 16);
         }
     }
 }

@@ -101,7 +101,7 @@ struct turboreg_ctx {
     int32_t heavy_cap_alloc = 0;
     CUtensorMap tmX;
     bool tmX_ok = false;
-    int32_t opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0, opt_sc2_variant = 0;
+    int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0, opt_sc2_variant = 0;
 };
 
 namespace {
@@ -151,7 +151,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.pts_stride = round_up(N, 32);  // even, so the paired arrays (stride / 2) stay 16-byte aligned
     w.bits_stride = N * W;
     w.row_stride = N;
-    w.edges_stride = std::max<int64_t>(1, N * (N - 1) / 2);
+    w.edges_stride = round_up(std::max<int64_t>(1, N * (N - 1) / 2), 4);  // uint4-aligned per pair
     w.piv_stride = K1;
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
@@ -337,7 +337,9 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         CK(L.run(KID_COMPAT, [&] {
             const dim3 g((unsigned)((T + 1) / 2), B);
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws);
-            else trk::k_compat<false><<<g, 256, 0, s>>>(ws);
+            else if (c->opt_compat_variant == 1) trk::k_compat<false, 4, 8, 1><<<g, 256, 0, s>>>(ws);
+            else if (c->opt_compat_variant == 2) trk::k_compat<false, 4, 16, -1><<<g, 256, 0, s>>>(ws);
+            else trk::k_compat<false, 3, 8, -2><<<g, 256, 0, s>>>(ws);
         }));
     }
     const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
@@ -510,6 +512,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "sc2_variant") {
         if (value < 0 || value > 7) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_sc2_variant = (int32_t)value;
+    } else if (k == "compat_variant") {
+        if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_compat_variant = (int32_t)value;
     } else if (k == "heavy_cap") {
         if (value < 0 || value % 256 || value > c->heavy_cap_alloc) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_cap = (int32_t)value;

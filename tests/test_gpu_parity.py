@@ -303,3 +303,15 @@ def test_sc2_variants_agree_with_oracle(tr_mod, variant, key, n):
     tr.set_option("heavy_min_rows", 1)
     res = tr.register(inst["src"], inst["dst"])
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("key,n", [("B", 2100), ("D", 1337)])
+def test_compat_variants_agree_with_oracle(tr_mod, variant, key, n):
+    # compat tilings: row pairs x 2 columns (default), column pairs x 2 tiles, row pairs x 1 column
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=3, n=n)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n)
+    tr.set_option("compat_variant", variant)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
