@@ -92,6 +92,7 @@ struct WS {
     int32_t* dense_list;  // [n] all other rows, index order
     int64_t lists_stride;
     uint32_t* heavy_mask; // [W] bitset of H
+    uint32_t* light_mask; // [W] bitset of the sparse rows (k_sc2_light's rows)
     uint8_t* heavy_X;     // [cap][Kcap] uint8 rows of C restricted to H
     int64_t heavy_X_stride;
     int32_t heavy_Kcap;
@@ -597,19 +598,21 @@ constexpr int SEL_ROWS_PER_BLOCK = 64;
 constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
 constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
 template <int WPL>
-constexpr int sc2_warp_words() { return 96 * WPL + LIST_MAX / 2 + 32 * WPL; }
+constexpr int sc2_warp_words() { return 96 * WPL + 32 * WPL; }  // U_i, rank prefix, row i, queue
 template <int WPL>
-constexpr int sc2_smem_bytes() { return SC2_WARPS * sc2_warp_words<WPL>() * 4; }
+constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 3 * 32 * WPL) * 4; }
 
-// Persistent: warps claim (pair, row) items from a global counter, so the very uneven row costs (a heavy
-// row scans ~|H|/32 D blocks, a light row handles a few dozen sparse edges) balance across the GPU.
-//
-// Per row i the edges j > i (O2, Def. 2) are assembled in rank order from three sources:
-//   (1) i, j both heavy: D[hpos i][hpos j] from the tensor-core block (scan of D row hpos(i));
-//   (2) i or j sparse (degree <= LIST_MAX, compact sorted neighbour list L): Ĝ_ij = |L_j ∩ N(i)| (or
-//       |L_i ∩ N(j)|), one edge per lane, testing list entries against the row bitmap in shared memory
-//       (or against row j's words);
+// Dense rows (not sparse: heavy, or degree > LIST_MAX), one warp per row i, SC2_BLOCKS_PER_PAIR blocks of
+// warps striding over the pair's dense rows.  Row i's edges come from three sources:
+//   (1) i, j both heavy: Ĝ_ij = D[hpos i][hpos j] from the tensor-core block.  The warp walks the heavy
+//       bits of U_i word-parallel; hpos j = (heavy columns in earlier words) + (heavy bits below j in its
+//       word), both from the pair's heavy mask in shared memory, so no index list is read;
+//   (2) j sparse (degree <= LIST_MAX, sorted neighbour list L_j), on EITHER side of i:
+//       Ĝ_ij = |L_j ∩ N(i)|, one edge per lane, list entries tested against row i's bitmap in shared
+//       memory.  For j > i the result goes to row i's slot; for j < i to row j's slot, whose rank
+//       (entries of L_j below i, minus those up to j) falls out of the same pass over L_j;
 //   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
+// Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
 constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
 constexpr int SC2_BLOCKS_PER_PAIR = 32;  // 256 warps stride over a pair's dense rows
 constexpr int SC2_CLAIM = 4;
@@ -638,172 +641,217 @@ __device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
+
+// As list_bitmap_count, for an edge (j, i) with j < i stored in row j: also returns the rank of i among
+// the entries of L_j above j (= #{x in L_j : j < x < i}).
+__device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, int len, const uint32_t* sr, int i,
+                                                           int j, int* rank) {
+    const int nch = (len + 7) >> 3;
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+    int r = 0;
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+                r += (k0 > j && k0 < i) + (k1 > j && k1 < i);  // pads are 0 <= j: never counted
+            }
+        }
+    }
+    *rank = r;
+    return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
+}
+
+// Edge between dense row i (bitmap sr, U_i words su, rank prefix sp in shared memory) and sparse row j.
+__device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
+                                                const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
+                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr, int i,
+                                                int j) {
+    const uint16_t* L = lists + (int64_t)j * LIST_MAX;
+    if (j > i) {
+        const uint32_t c = list_bitmap_count(L, deg_full[j], sr);
+        const int wj = j >> 5;
+        erow[sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u))] = ((uint32_t)j << 16) | c;
+    } else {
+        int rank;
+        const uint32_t c = list_bitmap_count_rank(L, deg_full[j], sr, i, j, &rank);
+        edges[rowptr[j] + rank] = ((uint32_t)i << 16) | c;
+    }
+}
+
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws, int* counter, int maxn, int batch) {
+__global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
     constexpr int G = 4;
-    constexpr int QCAP = 32 * WPL;  // light-edge queue of a dense row (one entry per word is enough per round)
-    // per warp: U_i words [32 WPL], exclusive prefix counts [32 WPL], full row i [32 WPL], L_i [LIST_MAX],
-    // queue (j, rank) [QCAP]
+    constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* su = s_dyn + warp * sc2_warp_words<WPL>();
+    // block: heavy mask, its exclusive word prefix, sparse mask; per warp: U_i, rank prefix, row i, queue
+    uint32_t* hm = s_dyn;
+    int32_t* hp = reinterpret_cast<int32_t*>(s_dyn + 32 * WPL);
+    uint32_t* lm = s_dyn + 64 * WPL;
+    uint32_t* su = s_dyn + 96 * WPL + warp * sc2_warp_words<WPL>();
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
-    uint16_t* sl = reinterpret_cast<uint16_t*>(su + 96 * WPL);
-    uint32_t* sq = su + 96 * WPL + LIST_MAX / 2;
-    (void)counter;
-    (void)maxn;
-    (void)batch;
+    uint32_t* sq = su + 96 * WPL;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
     if (n == 0) return;
     const int nd = ws.st[p].n_dense;
+    const int W = d.W;
+    const int nchunks = (W + 31) >> 5;
+    const int mstride = ws.bits_stride / ws.row_stride;
+    if (warp == 0) {
+        int carry = 0;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int w = lane + 32 * k;
+            const uint32_t h = (w < W) ? ws.heavy_mask[p * mstride + w] : 0u;
+            hm[w] = h;
+            lm[w] = (w < W) ? ws.light_mask[p * mstride + w] : 0u;
+            const int c = __popc(h);
+            const int incl = warp_incl_scan(c);
+            hp[w] = carry + incl - c;
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+    }
+    __syncthreads();
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    const int32_t* rowptr = ws.rowptr + p * ws.rp_stride;
+    uint32_t* edges = ws.edges + p * ws.edges_stride;
     const int nw = gridDim.x * SC2_WARPS;
     for (int kq = blockIdx.x * SC2_WARPS + warp; kq < nd; kq += nw) {
         const int i = ws.dense_list[p * ws.row_stride + kq];
-        const int W = d.W;
-        const int nchunks = (W + 31) >> 5;
-        const uint32_t* bits = ws.bits + p * ws.bits_stride;
         const uint32_t* ri = bits + (int64_t)i * W;
-        const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
-        const uint16_t* lists = ws.lists + p * ws.lists_stride;
-        const int32_t* hpos = ws.hpos + p * ws.row_stride;
-        const int di = deg_full[i];
         const int hi = hpos[i];
-        const bool ilist = di <= LIST_MAX;
-        uint32_t* erow = ws.edges + p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i];
+        uint32_t* erow = edges + rowptr[i];
         uint32_t reg[WPL];
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
             const int w = lane + 32 * k;
-            const uint32_t v = (w < W) ? ri[w] : 0u;
-            reg[k] = v;
-            sr[w] = v;
+            reg[k] = (w < W) ? ri[w] : 0u;
         }
-        int carry = 0;
-        (void)ilist;
         {
-            // dense (or heavy) row: U_i words and rank prefixes in shared memory
+            int carry = 0;
 #pragma unroll
             for (int k = 0; k < WPL; ++k) {
                 const int w = lane + 32 * k;
                 const uint32_t u = (w < W) ? upper_mask(reg[k], w, i) : 0u;
                 const int cnt = __popc(u);
                 const int incl = warp_incl_scan(cnt);
+                sr[w] = reg[k];
                 su[w] = u;
                 sp[w] = carry + incl - cnt;
                 carry += __shfl_sync(FULL, incl, 31);
             }
-            __syncwarp();
-            if (hi >= 0) {
-                // (1) heavy-heavy edges: scan D row hi over heavy columns a > hi (a ascending ⇔ j ascending)
-                const int h = ws.st[p].heavy_h;
-                const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
-                const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
-                for (int a0 = hi + 1; a0 < h; a0 += 128) {
-                    int jv[4];
-                    uint32_t wv[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int a = a0 + 32 * q + lane;
-                        jv[q] = (a < h) ? __ldg(hlist + a) : -1;
-                        wv[q] = (a < h) ? (uint32_t)__ldg(Drow + a) : 0u;
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int j = jv[q];
-                        if (j >= 0) {
-                            const int w = j >> 5, b = j & 31;
-                            const uint32_t uw = su[w];
-                            if ((uw >> b) & 1u)
-                                erow[sp[w] + __popc(uw & ((1u << b) - 1u))] = ((uint32_t)j << 16) | wv[q];
-                        }
-                    }
-                }
-            }
-            // remaining edges: queue sparse-neighbour edges, popcount dense-dense ones
-            const uint32_t* hmask = ws.heavy_mask + p * (ws.bits_stride / ws.row_stride);
-            int nq = 0;  // queued sparse-neighbour edges (warp-uniform)
+        }
+        __syncwarp();
+        // (1) heavy-heavy edges: walk the heavy bits of U_i, up to 4 per lane per round (gathers first)
+        if (hi >= 0) {
+            const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
             for (int c = (i + 1) >> 10; c < nchunks; ++c) {
                 const int w = c * 32 + lane;
-                uint32_t u = (w < W) ? su[w] : 0u;
-                if (hi >= 0 && w < W) u &= ~__ldg(hmask + w);
-                const int rk = (w < W) ? sp[w] : 0;
-                const uint32_t uall = u | ((w < W) ? su[w] : 0u);
+                const uint32_t suw = (w < W) ? su[w] : 0u, hmw = (w < W) ? hm[w] : 0u;
+                const int hpw = (w < W) ? hp[w] : 0, spw = (w < W) ? sp[w] : 0;
+                uint32_t u = suw & hmw;
                 while (__any_sync(FULL, u != 0u)) {
-                    const bool has = u != 0u;
-                    int j = -1, myr = 0;
-                    bool dense_j = false, sparse_j = false;
-                    if (has) {
-                        const int b = __ffs(u) - 1;
-                        u &= u - 1u;
-                        j = w * 32 + b;
-                        myr = rk + __popc(uall & ((1u << b) - 1u));
-                        dense_j = deg_full[j] > LIST_MAX;
-                        sparse_j = !dense_j;
-                    }
-                    const unsigned sb = __ballot_sync(FULL, sparse_j);
-                    if (sparse_j) {
-                        const int slot = nq + __popc(sb & ((1u << lane) - 1u));
-                        sq[slot] = ((uint32_t)j << 16) | (uint32_t)myr;  // rank < 65536 for n <= 32768
-                    }
-                    nq += __popc(sb);
-                    if (nq > QCAP - 32) {
-                        __syncwarp();
-                        for (int t = lane; t < nq; t += 32) {  // (2b) one queued edge per lane
-                            const uint32_t e = sq[t];
-                            const int jq = (int)(e >> 16);
-                            erow[e & 0xffffu] = ((uint32_t)jq << 16) |
-                                list_bitmap_count(lists + (int64_t)jq * LIST_MAX, deg_full[jq], sr);
-                        }
-                        __syncwarp();
-                        nq = 0;
-                    }
-                    // (3) dense-dense: warp-cooperative popcount, G at a time
-                    unsigned lb = __ballot_sync(FULL, dense_j);
-                    while (lb) {
-                        int jj[G], rr[G];
+                    int bq[4];
+                    uint32_t dv[4];
 #pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            int src = -1;
-                            if (lb) {
-                                src = __ffs(lb) - 1;
-                                lb &= lb - 1u;
+                    for (int q = 0; q < 4; ++q) {
+                        bq[q] = -1;
+                        dv[q] = 0u;
+                        if (u) {
+                            const int b = __ffs(u) - 1;
+                            u &= u - 1u;
+                            bq[q] = b;
+                            dv[q] = __ldg(Drow + hpw + __popc(hmw & ((1u << b) - 1u)));
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (bq[q] >= 0)
+                            erow[spw + __popc(suw & ((1u << bq[q]) - 1u))] = ((uint32_t)(w * 32 + bq[q]) << 16) | dv[q];
+                }
+            }
+        }
+        // (2) sparse neighbours on both sides (queued, one edge per lane) and (3) dense-dense upper
+        // neighbours that are not both heavy (warp-cooperative popcount)
+        int nq = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int w = c * 32 + lane;
+            const uint32_t lmw = (w < W) ? lm[w] : 0u;
+            uint32_t ul = ((w < W) ? sr[w] : 0u) & lmw;
+            uint32_t ud = ((w < W) ? su[w] : 0u) & ~lmw;
+            if (hi >= 0 && w < W) ud &= ~hm[w];
+            while (__any_sync(FULL, (ul | ud) != 0u)) {
+                int jl = -1, jd = -1;
+                if (ul) {
+                    jl = w * 32 + __ffs(ul) - 1;
+                    ul &= ul - 1u;
+                } else if (ud) {
+                    jd = w * 32 + __ffs(ud) - 1;
+                    ud &= ud - 1u;
+                }
+                const unsigned sb = __ballot_sync(FULL, jl >= 0);
+                if (jl >= 0) sq[nq + __popc(sb & ((1u << lane) - 1u))] = (uint32_t)jl;
+                nq += __popc(sb);
+                if (nq > QCAP - 32) {
+                    __syncwarp();
+                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
+                    __syncwarp();
+                    nq = 0;
+                }
+                unsigned lb = __ballot_sync(FULL, jd >= 0);
+                while (lb) {
+                    int jj[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        int src = -1;
+                        if (lb) {
+                            src = __ffs(lb) - 1;
+                            lb &= lb - 1u;
+                        }
+                        jj[g] = __shfl_sync(FULL, jd, src < 0 ? 0 : src);
+                        if (src < 0) jj[g] = -1;
+                    }
+                    uint32_t part[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        part[g] = 0u;
+                        if (jj[g] >= 0) {
+                            const uint32_t* rj = bits + (int64_t)jj[g] * W;
+#pragma unroll
+                            for (int k = 0; k < WPL; ++k) {
+                                const int wk = lane + 32 * k;
+                                if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
                             }
-                            jj[g] = __shfl_sync(FULL, j, src < 0 ? 0 : src);
-                            rr[g] = __shfl_sync(FULL, myr, src < 0 ? 0 : src);
-                            if (src < 0) jj[g] = -1;
                         }
-                        uint32_t part[G];
+                    }
 #pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            part[g] = 0u;
-                            if (jj[g] >= 0) {
-                                const uint32_t* rj = bits + (int64_t)jj[g] * W;
-#pragma unroll
-                                for (int k = 0; k < WPL; ++k) {
-                                    const int wk = lane + 32 * k;
-                                    if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            if (jj[g] < 0) break;
-                            const uint32_t tot = __reduce_add_sync(FULL, part[g]);
-                            if (lane == g) erow[rr[g]] = ((uint32_t)jj[g] << 16) | tot;
+                    for (int g = 0; g < G; ++g) {
+                        if (jj[g] < 0) break;
+                        const uint32_t tot = __reduce_add_sync(FULL, part[g]);
+                        if (lane == g) {
+                            const int j = jj[g], wj = j >> 5;
+                            erow[sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u))] = ((uint32_t)j << 16) | tot;
                         }
                     }
                 }
             }
-            __syncwarp();
-            for (int t = lane; t < nq; t += 32) {  // (2b) remaining queued edges, one per lane
-                const uint32_t e = sq[t];
-                const int jq = (int)(e >> 16);
-                erow[e & 0xffffu] = ((uint32_t)jq << 16) | list_bitmap_count(lists + (int64_t)jq * LIST_MAX, deg_full[jq], sr);
-            }
         }
+        __syncwarp();
+        for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
         __syncwarp();
     }
 }
@@ -840,6 +888,9 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
             if (f) L[pos] = i;
             else Dn[i - pos] = i;
         }
+        const unsigned fb = __ballot_sync(FULL, f);
+        if (lane == 0 && ((r0 + warp * 32) >> 5) < d.W)
+            ws.light_mask[p * (ws.bits_stride / ws.row_stride) + ((r0 + warp * 32) >> 5)] = fb;
         __syncthreads();
         if (t == 1023) s_carry = pos + f;
         __syncthreads();
@@ -886,27 +937,16 @@ template <int WPL>
 constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL>() * 4; }
 
 template <int WPL>
-__device__ __forceinline__ void light_flush(const WS& ws, int p, int n, int W, const uint32_t* bm, const uint16_t* ls,
-                                            const int32_t* meta, const uint32_t* q, int cnt, bool dense) {
+__device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t* bm, const int32_t* meta,
+                                            const uint32_t* q, int cnt) {
     const int lane = threadIdx.x & 31;
-    const uint32_t* bits = ws.bits + p * ws.bits_stride;
     const uint16_t* lists = ws.lists + p * ws.lists_stride;
     const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
     if (lane < cnt) {
         const uint32_t e = q[lane];
         const int j = (int)(e & 0xffffu), t = (int)((e >> 16) & 63), r = (int)(e >> 22);
-        const int i = meta[4 * r], di = meta[4 * r + 1], lo = meta[4 * r + 2];
-        uint32_t c = 0;
-        if (!dense) {
-            c = list_bitmap_count(lists + (int64_t)j * LIST_MAX, deg_full[j], bm + r * 32 * WPL);
-        } else {
-            const uint32_t* rj = bits + (int64_t)j * W;
-            const uint16_t* Li = ls + r * LIST_MAX;
-            for (int k = 0; k < di; ++k) {
-                const int x = Li[k];
-                c += (__ldg(rj + (x >> 5)) >> (x & 31)) & 1u;
-            }
-        }
+        const int i = meta[4 * r], lo = meta[4 * r + 2];
+        const uint32_t c = list_bitmap_count(lists + (int64_t)j * LIST_MAX, deg_full[j], bm + r * 32 * WPL);
         ws.edges[p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i] + (t - lo)] = ((uint32_t)j << 16) | c;
     }
 }
@@ -969,10 +1009,12 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int M = __shfl_sync(FULL, incl, 31);
     if (lane < nr) meta[4 * lane + 3] = my_pref;
     __syncwarp();
-    int nL = 0, nD = 0;
+    const int mstride = ws.bits_stride / ws.row_stride;
+    const uint32_t* lmask = ws.light_mask + p * mstride;
+    int nL = 0;
     for (int e0 = 0; e0 < M; e0 += 32) {
         const int e = e0 + lane;
-        bool isL = false, isD = false;
+        bool isL = false;
         uint32_t packed = 0;
         if (e < M) {
             int r = 0;
@@ -983,33 +1025,21 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
             const int t = lo + (e - pr);
             const int j = ls[r * LIST_MAX + t];
             packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 22);
-            isL = deg_full[j] <= LIST_MAX;
-            isD = !isL;
+            isL = (__ldg(lmask + (j >> 5)) >> (j & 31)) & 1u;  // sparse j; dense j is k_sc2's edge
         }
-        const unsigned bL = __ballot_sync(FULL, isL), bD = __ballot_sync(FULL, isD);
-        const unsigned lt = (1u << lane) - 1u;
-        if (isL) qL[nL + __popc(bL & lt)] = packed;
-        if (isD) qD[nD + __popc(bD & lt)] = packed;
+        const unsigned bL = __ballot_sync(FULL, isL);
+        if (isL) qL[nL + __popc(bL & ((1u << lane) - 1u))] = packed;
         nL += __popc(bL);
-        nD += __popc(bD);
         __syncwarp();
         if (nL >= 32) {
-            light_flush<WPL>(ws, p, n, W, bm, ls, meta, qL, 32, false);
+            light_flush<WPL>(ws, p, bm, meta, qL, 32);
             __syncwarp();
             if (lane < nL - 32) qL[lane] = qL[32 + lane];
             nL -= 32;
             __syncwarp();
         }
-        if (nD >= 32) {
-            light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, 32, true);
-            __syncwarp();
-            if (lane < nD - 32) qD[lane] = qD[32 + lane];
-            nD -= 32;
-            __syncwarp();
-        }
     }
-    light_flush<WPL>(ws, p, n, W, bm, ls, meta, qL, nL, false);
-    light_flush<WPL>(ws, p, n, W, bm, ls, meta, qD, nD, true);
+    light_flush<WPL>(ws, p, bm, meta, qL, nL);
 }
 
 // The pivot passes stream the pair's compact O2 edge array (E words) with a grid stride: coalesced,

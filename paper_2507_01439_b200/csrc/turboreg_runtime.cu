@@ -156,7 +156,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -181,6 +181,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(uint16_t) * (size_t)(cap * cap * B), &p_D},
         {sizeof(int32_t) * (size_t)(cap * B), &p_hl},
         {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
+        {sizeof(uint32_t) * (size_t)(W * B), &p_lm},
         {sizeof(int) * 16, &p_ctr},
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
         {sizeof(int32_t) * (size_t)(N * B), &p_ll},
@@ -229,6 +230,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_D_stride = cap * cap;
     w.heavy_list = static_cast<int32_t*>(p_hl);
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
+    w.light_mask = static_cast<uint32_t*>(p_lm);
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
@@ -366,19 +368,15 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     const int wpl = (Wb + 31) / 32;
     {
-        int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-        (void)nsm;
         const dim3 gp((unsigned)trk::SC2_BLOCKS_PER_PAIR, B);
-        int* ctr = c->d_counters;
         CK(L.run(KID_SC2, [&] {
-            if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws, ctr, maxn_batch, batch);
-            else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws, ctr, maxn_batch, batch);
-            else if (wpl <= 4) trk::k_sc2<4><<<gp, 256, trk::sc2_smem_bytes<4>(), s>>>(ws, ctr, maxn_batch, batch);
-            else if (wpl <= 5) trk::k_sc2<5><<<gp, 256, trk::sc2_smem_bytes<5>(), s>>>(ws, ctr, maxn_batch, batch);
-            else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws, ctr, maxn_batch, batch);
-            else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws, ctr, maxn_batch, batch);
-            else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws, ctr, maxn_batch, batch);
+            if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws);
+            else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws);
+            else if (wpl <= 4) trk::k_sc2<4><<<gp, 256, trk::sc2_smem_bytes<4>(), s>>>(ws);
+            else if (wpl <= 5) trk::k_sc2<5><<<gp, 256, trk::sc2_smem_bytes<5>(), s>>>(ws);
+            else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws);
+            else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws);
+            else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws);
         }));
         const int lgr = wpl >= 16 ? 2 : 8;  // trk::light_rows<WPL>()
         const dim3 gl((unsigned)((maxn_batch + 8 * lgr - 1) / (8 * lgr)), B);
