@@ -154,9 +154,6 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "heavy_min_rows"   minimum |H| for the dense block to be used (default 128)
  *   "heavy_min_degree" minimum degree of a heavy row (default 32)
  *   "heavy_cap"        maximum |H| (multiple of 256, <= the allocated capacity)
- *   "sc2_variant"      bit 0: static row striding in the dense-row assembly; bit 1: warp-cooperative
- *                      dense-neighbour counts; bit 2: tensor-core block over the non-sparse columns only,
- *                      sparse columns added by a correction pass (default 0)
  *   "compat_variant"   compat-graph tiling: 0 = row pairs in f32x2 lanes x 2 column tiles per warp
  *                      (default); 1 = column pairs x 2 tiles; 2 = row pairs x 1 column tile
  * Returns TURBOREG_ERR_INVALID_ARGUMENT for unknown names or values. */

@@ -93,13 +93,15 @@ struct WS {
     int64_t lists_stride;
     uint32_t* heavy_mask; // [W] bitset of H
     uint32_t* light_mask; // [W] bitset of the sparse rows (k_sc2_light's rows)
+    uint2* heavy_UP;      // [cap][W] per heavy row a: (U_{H_a} word, exclusive prefix popcount of U_{H_a})
+    int64_t heavy_UP_stride;
     uint8_t* heavy_X;     // [cap][Kcap] uint8 rows of C restricted to H
     int64_t heavy_X_stride;
     int32_t heavy_Kcap;
     int32_t heavy_cap;    // max |H| (multiple of 256)
     uint16_t* heavy_D;    // [cap][cap] X X^T (+ sparse-column correction)
     int64_t heavy_D_stride;
-    int32_t heavy_min_rows, heavy_min_deg, sc2_path, sc2_variant;
+    int32_t heavy_min_rows, heavy_min_deg, sc2_path;
     float tau, tau_base, thr;
     int32_t k1, k2, mode;
 };
@@ -600,13 +602,11 @@ constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_B
 template <int WPL>
 constexpr int sc2_warp_words() { return 96 * WPL + 32 * WPL; }  // U_i, rank prefix, row i, queue
 template <int WPL>
-constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 3 * 32 * WPL) * 4; }
+constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
 
 // Dense rows (not sparse: heavy, or degree > LIST_MAX), one warp per row i, SC2_BLOCKS_PER_PAIR blocks of
 // warps striding over the pair's dense rows.  Row i's edges come from three sources:
-//   (1) i, j both heavy: Ĝ_ij = D[hpos i][hpos j] from the tensor-core block.  The warp walks the heavy
-//       bits of U_i word-parallel; hpos j = (heavy columns in earlier words) + (heavy bits below j in its
-//       word), both from the pair's heavy mask in shared memory, so no index list is read;
+//   (1) i, j both heavy: written by the tensor-core epilogue (k_sc2_mma) or k_emit_hh, not here;
 //   (2) j sparse (degree <= LIST_MAX, sorted neighbour list L_j), on EITHER side of i:
 //       Ĝ_ij = |L_j ∩ N(i)|, one edge per lane, list entries tested against row i's bitmap in shared
 //       memory.  For j > i the result goes to row i's slot; for j < i to row j's slot, whose rank
@@ -692,11 +692,10 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
     constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // block: heavy mask, its exclusive word prefix, sparse mask; per warp: U_i, rank prefix, row i, queue
+    // block: heavy mask, sparse mask; per warp: U_i, rank prefix, row i, queue
     uint32_t* hm = s_dyn;
-    int32_t* hp = reinterpret_cast<int32_t*>(s_dyn + 32 * WPL);
-    uint32_t* lm = s_dyn + 64 * WPL;
-    uint32_t* su = s_dyn + 96 * WPL + warp * sc2_warp_words<WPL>();
+    uint32_t* lm = s_dyn + 32 * WPL;
+    uint32_t* su = s_dyn + 64 * WPL + warp * sc2_warp_words<WPL>();
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
     uint32_t* sq = su + 96 * WPL;
@@ -708,19 +707,9 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
     const int W = d.W;
     const int nchunks = (W + 31) >> 5;
     const int mstride = ws.bits_stride / ws.row_stride;
-    if (warp == 0) {
-        int carry = 0;
-#pragma unroll
-        for (int k = 0; k < WPL; ++k) {
-            const int w = lane + 32 * k;
-            const uint32_t h = (w < W) ? ws.heavy_mask[p * mstride + w] : 0u;
-            hm[w] = h;
-            lm[w] = (w < W) ? ws.light_mask[p * mstride + w] : 0u;
-            const int c = __popc(h);
-            const int incl = warp_incl_scan(c);
-            hp[w] = carry + incl - c;
-            carry += __shfl_sync(FULL, incl, 31);
-        }
+    for (int w = threadIdx.x; w < 32 * WPL; w += blockDim.x) {
+        hm[w] = (w < W) ? ws.heavy_mask[p * mstride + w] : 0u;
+        lm[w] = (w < W) ? ws.light_mask[p * mstride + w] : 0u;
     }
     __syncthreads();
     const uint32_t* bits = ws.bits + p * ws.bits_stride;
@@ -756,35 +745,6 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
             }
         }
         __syncwarp();
-        // (1) heavy-heavy edges: walk the heavy bits of U_i, up to 4 per lane per round (gathers first)
-        if (hi >= 0) {
-            const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)hi * ws.heavy_cap;
-            for (int c = (i + 1) >> 10; c < nchunks; ++c) {
-                const int w = c * 32 + lane;
-                const uint32_t suw = (w < W) ? su[w] : 0u, hmw = (w < W) ? hm[w] : 0u;
-                const int hpw = (w < W) ? hp[w] : 0, spw = (w < W) ? sp[w] : 0;
-                uint32_t u = suw & hmw;
-                while (__any_sync(FULL, u != 0u)) {
-                    int bq[4];
-                    uint32_t dv[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        bq[q] = -1;
-                        dv[q] = 0u;
-                        if (u) {
-                            const int b = __ffs(u) - 1;
-                            u &= u - 1u;
-                            bq[q] = b;
-                            dv[q] = __ldg(Drow + hpw + __popc(hmw & ((1u << b) - 1u)));
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (bq[q] >= 0)
-                            erow[spw + __popc(suw & ((1u << bq[q]) - 1u))] = ((uint32_t)(w * 32 + bq[q]) << 16) | dv[q];
-                }
-            }
-        }
         // (2) sparse neighbours on both sides (queued, one edge per lane) and (3) dense-dense upper
         // neighbours that are not both heavy (warp-cooperative popcount)
         int nq = 0;
@@ -1213,10 +1173,9 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     }
 }
 
-// X[a][k] = C[H_a][k] as uint8 0/1 over all columns (default), or — with sc2_variant bit 2 — over
-// Kset = the non-sparse columns only (dense_list, k' < round_up(|Kset|, 128), zero columns beyond; the
-// sparse columns then come from k_light_corr).  Rows a in [|H|, round_up(|H|, 256)) are zero.  One warp
-// per X row.
+// X[a][k] = C[H_a][k] as uint8 0/1 over all columns (rows a in [|H|, round_up(|H|, 256)) are zero), and
+// for a < |H| the upper words of row H_a with their exclusive prefix popcounts (UP), from which the
+// tensor-core epilogue reads the O2 test and the edge-list rank of every (H_a, H_b).  One warp per X row.
 __global__ void __launch_bounds__(256) k_expand(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
@@ -1227,11 +1186,15 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
     const int a = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (a >= hp) return;
     const int W = d.W;
-    const uint32_t* row = (a < h) ? ws.bits + p * ws.bits_stride + (int64_t)ws.heavy_list[p * ws.heavy_cap + a] * W : nullptr;
-    if (!(ws.sc2_variant & 4)) {  // full K: every column, 32 bytes per bit word (two 16-byte stores)
-        uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
-        for (int w = lane; w < W; w += 32) {
-            const uint32_t v = row ? row[w] : 0u;
+    const int ia = (a < h) ? ws.heavy_list[p * ws.heavy_cap + a] : -1;
+    const uint32_t* row = (a < h) ? ws.bits + p * ws.bits_stride + (int64_t)ia * W : nullptr;
+    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
+    uint2* up = ws.heavy_UP + p * ws.heavy_UP_stride + (int64_t)a * W;
+    int carry = 0;
+    for (int w0 = 0; w0 < W; w0 += 32) {  // 32 bytes per bit word (two 16-byte stores)
+        const int w = w0 + lane;
+        const uint32_t v = (row && w < W) ? row[w] : 0u;
+        if (w < W) {
             uint32_t b[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -1242,70 +1205,16 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
             dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
             dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
         }
-        return;
-    }
-    const int nk = ws.st[p].n_dense, kp = (nk + MMA_BK_ - 1) / MMA_BK_ * MMA_BK_;
-    const int32_t* kset = ws.dense_list + p * ws.row_stride;
-    uint32_t* X = reinterpret_cast<uint32_t*>(ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap);
-    for (int q = lane; q < kp / 4; q += 32) {  // 4 columns per 32-bit store
-        uint32_t out = 0u;
         if (row) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int kk = 4 * q + e;
-                if (kk < nk) {
-                    const int c = __ldg(kset + kk);
-                    out |= ((__ldg(row + (c >> 5)) >> (c & 31)) & 1u) << (8 * e);
-                }
-            }
+            const uint32_t u = (w < W) ? upper_mask(v, w, ia) : 0u;
+            const int cnt = __popc(u);
+            const int incl = warp_incl_scan(cnt);
+            if (w < W) up[w] = make_uint2(u, (uint32_t)(carry + incl - cnt));
+            carry += __shfl_sync(FULL, incl, 31);
         }
-        X[q] = out;
     }
 }
 
-// Σ_k C_ak C_bk over the sparse columns k the tensor-core block skipped: each sparse row k adds 1 to
-// D[hpos x][hpos y] for every pair x < y of heavy vertices in its neighbour list.  One thread per sparse row:
-// independent 16-byte list loads, the heavy positions staged in shared memory, then the pair atomics.
-constexpr int CORR_THREADS = 128;
-__global__ void __launch_bounds__(CORR_THREADS) k_light_corr(WS ws) {
-    __shared__ int16_t s_h[CORR_THREADS][LIST_MAX];
-    const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    if (d.n == 0) return;
-    const int h = ws.st[p].heavy_h;
-    if (h == 0 || !(ws.sc2_variant & 4)) return;
-    const int kq = blockIdx.x * CORR_THREADS + threadIdx.x;
-    if (kq >= ws.st[p].n_light) return;
-    const int k = ws.light_list[p * ws.row_stride + kq];
-    const int dk = ws.deg_full[p * ws.row_stride + k];
-    const uint4* L4 = reinterpret_cast<const uint4*>(ws.lists + p * ws.lists_stride + (int64_t)k * LIST_MAX);
-    const int32_t* hpos = ws.hpos + p * ws.row_stride;
-    int16_t* mine = s_h[threadIdx.x];
-    int m = 0;
-    const int nch = (dk + 7) >> 3;
-    for (int c = 0; c < nch; ++c) {
-        const uint4 v = __ldg(L4 + c);
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-        int hx[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int t = 8 * c + e;
-            hx[e] = (t < dk) ? __ldg(hpos + ((wv[e >> 1] >> (16 * (e & 1))) & 0xffffu)) : -1;
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (hx[e] >= 0) mine[m++] = (int16_t)hx[e];
-    }
-    // D is uint16: add to a half of the aligned 32-bit word (entries stay < 2^15, so no carry crosses halves)
-    uint16_t* D = ws.heavy_D + p * ws.heavy_D_stride;
-    for (int x = 0; x + 1 < m; ++x) {
-        uint16_t* row = D + (int64_t)mine[x] * ws.heavy_cap;
-        for (int y = x + 1; y < m; ++y) {  // hpos ascending along L
-            const uintptr_t a = reinterpret_cast<uintptr_t>(row + mine[y]);
-            atomicAdd(reinterpret_cast<unsigned int*>(a & ~(uintptr_t)3), (a & 2) ? 0x10000u : 1u);
-        }
-    }
-}
 
 // ------------------------------------------------------------------------------------------ a4 pivots
 // Eq. 4: α_K1 = K1-th largest O2 weight; all edges > α plus the lexicographically first

@@ -32,7 +32,7 @@ enum KernelId {
     KID_ROWCLASS,
     KID_EXPAND,
     KID_SC2_MMA,
-    KID_LIGHT_CORR,
+    KID_EMIT_HH,
     KID_SC2,
     KID_SC2_LIGHT,
     KID_HIST_HI,
@@ -50,7 +50,7 @@ enum KernelId {
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
-                                       "k_expand",   "k_sc2_mma",      "k_light_corr",  "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
+                                       "k_expand",   "k_sc2_mma",      "k_emit_hh",     "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
                                        "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
@@ -60,12 +60,6 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
 constexpr int HEAVY_CAP_MAX = 2048;
 
-int mma_tiles_for(int cap) {
-    const int RB = cap / trk::MMA_BM, CB = cap / trk::MMA_BN;
-    int t = 0;
-    for (int rb = 0; rb < RB; ++rb) t += CB - rb / 2;
-    return t;
-}
 
 }  // namespace
 
@@ -101,7 +95,8 @@ struct turboreg_ctx {
     int32_t heavy_cap_alloc = 0;
     CUtensorMap tmX;
     bool tmX_ok = false;
-    int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0, opt_sc2_variant = 0;
+    int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
+    int num_sms = 148;
 };
 
 namespace {
@@ -156,7 +151,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -182,6 +177,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(int32_t) * (size_t)(cap * B), &p_hl},
         {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
         {sizeof(uint32_t) * (size_t)(W * B), &p_lm},
+        {sizeof(uint2) * (size_t)(cap * W * B), &p_up},
         {sizeof(int) * 16, &p_ctr},
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
         {sizeof(int32_t) * (size_t)(N * B), &p_ll},
@@ -231,6 +227,8 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_list = static_cast<int32_t*>(p_hl);
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
     w.light_mask = static_cast<uint32_t*>(p_lm);
+    w.heavy_UP = static_cast<uint2*>(p_up);
+    w.heavy_UP_stride = cap * W;
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
@@ -264,7 +262,6 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.heavy_min_rows = c->opt_heavy_min_rows;
     c->ws.heavy_min_deg = c->opt_heavy_min_deg;
     c->ws.sc2_path = (c->opt_sc2_path == 0 && !c->tmX_ok) ? 1 : c->opt_sc2_path;
-    c->ws.sc2_variant = c->opt_sc2_variant;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -352,19 +349,19 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         CK(L.run(KID_EXPAND, [&] {
             trk::k_expand<<<dim3((unsigned)(ws.heavy_cap / 8), B), 256, 0, s>>>(ws);
         }));
-        CK(L.run(KID_SC2_MMA, [&] {
-            if (ws.sc2_path == 2) {
+        if (ws.sc2_path == 2) {
+            CK(L.run(KID_SC2_MMA, [&] {
                 const unsigned g = (unsigned)(ws.heavy_cap / 64);
                 trk::k_sc2_dp4a<<<dim3(g, g, B), 256, 0, s>>>(ws);
-            } else {
-                trk::k_sc2_mma<<<dim3((unsigned)mma_tiles_for(ws.heavy_cap), B), trk::MMA_THREADS, trk::MMA_SMEM_BYTES,
-                                 s>>>(c->tmX, ws);
-            }
-        }));
-        if (ws.sc2_variant & 4) CK(L.run(KID_LIGHT_CORR, [&] {
-            trk::k_light_corr<<<dim3((unsigned)((maxn_batch + trk::CORR_THREADS - 1) / trk::CORR_THREADS), B),
-                                trk::CORR_THREADS, 0, s>>>(ws);
-        }));
+            }));
+            CK(L.run(KID_EMIT_HH, [&] {
+                trk::k_emit_hh<<<dim3((unsigned)(ws.heavy_cap / 8), B), 256, 0, s>>>(ws);
+            }));
+        } else {
+            CK(L.run(KID_SC2_MMA, [&] {
+                trk::k_sc2_mma<<<c->num_sms, trk::MMA_THREADS, trk::MMA_SMEM_BYTES, s>>>(c->tmX, ws, B);
+            }));
+        }
     }
     const int wpl = (Wb + 31) / 32;
     {
@@ -459,6 +456,7 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreate(&c->own_stream) != cudaSuccess) {
         st = TURBOREG_ERR_CUDA;
     }
+    if (st == TURBOREG_OK) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (st == TURBOREG_OK) st = alloc_ws(c);
     if (st == TURBOREG_OK) {
         if (cudaMallocHost(&c->h_desc, sizeof(trk::PairDesc) * max_batch) != cudaSuccess ||
@@ -507,9 +505,6 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "heavy_min_degree") {
         if (value < 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_min_deg = (int32_t)value;
-    } else if (k == "sc2_variant") {
-        if (value < 0 || value > 7) return TURBOREG_ERR_INVALID_ARGUMENT;
-        c->opt_sc2_variant = (int32_t)value;
     } else if (k == "compat_variant") {
         if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_compat_variant = (int32_t)value;

@@ -4,10 +4,14 @@
 // C·C over H is a dense binary contraction, so it runs on the 5th-gen tensor cores:
 //   X = C[H, :] as uint8 0/1 (K-major, [h][K]),  D = X · X^T  (exact: int32 accumulate, K <= 32768)
 // with tcgen05.mma kind::i8 (M=128, N=256, K=32 per instruction), operands staged by TMA
-// (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline, the accumulator in TMEM
-// (256 columns) and a 4-warp epilogue (tcgen05.ld 32x32b) that stores D as uint16 for the assembly pass.
-// Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..5 =
-// epilogue.  Which rows are heavy only changes speed, never the result (Σ_k splits exactly).
+// (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline.
+// Persistent: one CTA per SM walks the (pair, tile) list of the whole batch; the accumulator is double
+// buffered in TMEM (2 × 256 columns) so the epilogue of tile t overlaps the MMAs of tile t+1.
+// The epilogue (4 warps, tcgen05.ld 32x32b, thread = output row a) does not store D: it keeps the entries
+// that are O2 edges — b > a and C[H_a][H_b] = 1, tested on row H_a's upper words — and writes each
+// straight to its slot in the compact edge list, rowptr(H_a) + rank of H_b in U_{H_a} (prefix counts
+// per word from k_expand).  Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread
+// MMA issuer, warps 2..5 = epilogue.  Which rows are heavy only changes speed, never the result.
 // =====================================================================================================
 #pragma once
 #include <cuda.h>
@@ -22,8 +26,11 @@ constexpr int MMA_STAGES = 4;
 constexpr int MMA_A_BYTES = MMA_BM * MMA_BK;  // 16 KB
 constexpr int MMA_B_BYTES = MMA_BN * MMA_BK;  // 32 KB
 constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
-constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int MMA_THREADS = 192;
+constexpr int MMA_EPI_WARPS = 8;  // 2 per TMEM lane quarter, each draining half of the 256 columns
+constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larger batches loop over it)
+constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 32 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
+constexpr int MMA_THREADS = 64 + 32 * MMA_EPI_WARPS;
 
 // Instruction descriptor: c_format S32 (bits 4-5 = 2), a/b format u8 (0), both K-major, N>>3 at bit 17,
 // M>>4 at bit 24 (CUTLASS UMMA::InstrDescriptor layout).
@@ -70,38 +77,63 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// Per-pair heavy-set bookkeeping lives in PairState (heavy_h); tile (rb, cb) enumeration over the blocks
-// that touch the strict upper triangle (some b > a): cb >= rb/2.
-__device__ __forceinline__ bool mma_tile_coords(int t, int hp, int* rb_out, int* cb_out) {
+// Tiles (rb, cb) of one pair: the 128×256 blocks that touch the strict upper triangle (some b > a):
+// cb >= rb/2.  Count for a padded heavy count hp (multiple of 256).
+__device__ __forceinline__ int mma_tile_count(int hp) {
+    const int RB = hp / MMA_BM, CB = hp / MMA_BN;
+    int t = 0;
+    for (int rb = 0; rb < RB; ++rb) t += CB - rb / 2;
+    return t;
+}
+__device__ __forceinline__ void mma_tile_coords(int t, int hp, int* rb_out, int* cb_out) {
     const int RB = hp / MMA_BM, CB = hp / MMA_BN;
     for (int rb = 0; rb < RB; ++rb) {
         const int c0 = rb / 2;
         const int cnt = CB - c0;
-        if (t < cnt) { *rb_out = rb; *cb_out = c0 + t; return true; }
+        if (t < cnt) { *rb_out = rb; *cb_out = c0 + t; return; }
         t -= cnt;
     }
-    return false;
+    *rb_out = *cb_out = 0;
+}
+// Global tile g of the batch -> (pair, rb, cb): linear walk over pairs with a running prefix (each role
+// walks its own tiles in increasing g, so the cursor only moves forward).
+struct TileCursor {
+    int p = 0, base = 0, cnt = -1;
+    __device__ bool locate(const WS& ws, int batch, int g, int* pp, int* rb, int* cb, int* h) {
+        for (;;) {
+            if (p >= batch) return false;
+            if (cnt < 0) {
+                const int hh = (ws.desc[p].n == 0) ? 0 : ws.st[p].heavy_h;
+                cnt = hh ? mma_tile_count((hh + MMA_BN - 1) / MMA_BN * MMA_BN) : 0;
+            }
+            if (g < base + cnt) break;
+            base += cnt;
+            cnt = -1;
+            ++p;
+        }
+        *pp = p;
+        *h = ws.st[p].heavy_h;
+        mma_tile_coords(g - base, (*h + MMA_BN - 1) / MMA_BN * MMA_BN, rb, cb);
+        return true;
+    }
+};
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-__global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constant__ CUtensorMap tmX, WS ws) {
+__global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constant__ CUtensorMap tmX, WS ws, int batch) {
     extern __shared__ uint8_t smem_raw[];
-    const int p = blockIdx.y;
-    const PairDesc d = ws.desc[p];
-    if (d.n == 0) return;
-    const int h = ws.st[p].heavy_h;
-    if (h == 0) return;
-    const int hp = (h + MMA_BN - 1) / MMA_BN * MMA_BN;
-    int rb, cb;
-    if (!mma_tile_coords(blockIdx.x, hp, &rb, &cb)) return;
-    // K = every column (32 W, a multiple of 128), or the non-sparse columns padded to 128 (sc2_variant bit 2)
-    const int KB = (ws.sc2_variant & 4) ? (ws.st[p].n_dense + MMA_BK - 1) / MMA_BK : d.W * 32 / MMA_BK;
-
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t tiles = (base + 1023u) & ~1023u;  // 1024-byte aligned for the 128B swizzle
     const uint32_t bars = tiles + MMA_STAGES * MMA_STAGE_BYTES;
-    // barriers: full[s] at bars + 8s, empty[s] at bars + 64 + 8s, accum at bars + 128; tmem ptr at bars + 192
-    const uint32_t full0 = bars, empty0 = bars + 64, accum = bars + 128, tptr = bars + 192;
+    // barriers: full[s] at bars + 8s, empty[s] at bars + 64 + 8s, tmem_full[2] at bars + 128,
+    // tmem_empty[2] at bars + 144; tmem ptr at bars + 192
+    const uint32_t full0 = bars, empty0 = bars + 64, tfull0 = bars + 128, tempty0 = bars + 144, tptr = bars + 192;
     uint8_t* gen_tptr = smem_raw + (tptr - base);
+    int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
+    uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [8][32][34] (Ĝ < 65536)
+    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 32 * 34);   // [8][32] edge-list bases
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -109,12 +141,15 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
-        mbar_init(accum, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, MMA_EPI_WARPS);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     }
-    if (warp == 1) {  // TMEM: 256 columns × 128 lanes of 32-bit = one M128×N256 int32 accumulator
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tptr));
+    if (warp == 1) {  // TMEM: 2 × 256 columns × 128 lanes of 32-bit = two M128×N256 int32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tptr));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -124,74 +159,129 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % MMA_STAGES;
-                const int round = kb / MMA_STAGES;
-                if (round > 0) mbar_wait(empty0 + 8 * s, (round - 1) & 1);
-                const uint32_t a_dst = tiles + s * MMA_STAGE_BYTES;
-                const uint32_t b_dst = a_dst + MMA_A_BYTES;
-                mbar_expect_tx(full0 + 8 * s, MMA_STAGE_BYTES);
-                tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, p);
-                tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN, p);
-                tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN + 128, p);
+            TileCursor cur;
+            int it = 0;
+            int p, rb, cb, h;
+            for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x) {
+                const int KB = ws.desc[p].W * 32 / MMA_BK;
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % MMA_STAGES;
+                    const int round = it / MMA_STAGES;
+                    if (round > 0) mbar_wait(empty0 + 8 * s, (round - 1) & 1);
+                    const uint32_t a_dst = tiles + s * MMA_STAGE_BYTES;
+                    const uint32_t b_dst = a_dst + MMA_A_BYTES;
+                    mbar_expect_tx(full0 + 8 * s, MMA_STAGE_BYTES);
+                    tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, p);
+                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN, p);
+                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN + 128, p);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % MMA_STAGES;
-                mbar_wait(full0 + 8 * s, (kb / MMA_STAGES) & 1);
+            TileCursor cur;
+            int it = 0, lt = 0;
+            int p, rb, cb, h;
+            for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x, ++lt) {
+                const int KB = ws.desc[p].W * 32 / MMA_BK;
+                const int acc = lt & 1;
+                if (lt >= 2) mbar_wait(tempty0 + 8 * acc, ((lt >> 1) - 1) & 1);  // epilogue drained it
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a_src = tiles + s * MMA_STAGE_BYTES;
-                const uint32_t b_src = a_src + MMA_A_BYTES;
+                const uint32_t tacc = tmem + (uint32_t)(acc * MMA_BN);
+                for (int kb = 0; kb < KB; ++kb, ++it) {
+                    const int s = it % MMA_STAGES;
+                    mbar_wait(full0 + 8 * s, (it / MMA_STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a_src = tiles + s * MMA_STAGE_BYTES;
+                    const uint32_t b_src = a_src + MMA_A_BYTES;
 #pragma unroll
-                for (int k = 0; k < MMA_BK / 32; ++k) {
-                    umma_i8(tmem, umma_desc_sw128(a_src + 32 * k), umma_desc_sw128(b_src + 32 * k), MMA_IDESC,
-                            (kb | k) ? 1u : 0u);
+                    for (int k = 0; k < MMA_BK / 32; ++k) {
+                        umma_i8(tacc, umma_desc_sw128(a_src + 32 * k), umma_desc_sw128(b_src + 32 * k), MMA_IDESC,
+                                (kb | k) ? 1u : 0u);
+                    }
+                    umma_commit(empty0 + 8 * s);  // frees the smem stage once these MMAs completed
                 }
-                umma_commit(empty0 + 8 * s);  // frees the smem stage once these MMAs completed
+                umma_commit(tfull0 + 8 * acc);  // accumulator complete
             }
-            umma_commit(accum);
         }
-    } else {  // epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    } else {  // epilogue: warp w owns TMEM lane quarter w % 4 and column half (w - 2) / 4
         const int q = warp & 3;
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int a = rb * MMA_BM + q * 32 + lane;  // output row = TMEM lane
-        uint16_t* D = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)a * ws.heavy_cap;
-#pragma unroll 1
-        for (int c = 0; c < MMA_BN / 32; ++c) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (a < h) {
-                uint4* dst = reinterpret_cast<uint4*>(D + cb * MMA_BN + c * 32);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uint4 o;
-                    o.x = (v[8 * k + 0] & 0xffffu) | (v[8 * k + 1] << 16);
-                    o.y = (v[8 * k + 2] & 0xffffu) | (v[8 * k + 3] << 16);
-                    o.z = (v[8 * k + 4] & 0xffffu) | (v[8 * k + 5] << 16);
-                    o.w = (v[8 * k + 6] & 0xffffu) | (v[8 * k + 7] << 16);
-                    dst[k] = o;
-                }
+        const int ew = warp - 2;           // 0..7
+        const int half = ew >> 2;
+        const int et = threadIdx.x - 64;  // 0..255
+        TileCursor cur;
+        int lt = 0;
+        int p, rb, cb, h;
+        for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            int32_t* hl = s_hl + acc * MMA_BN;
+            const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
+            for (int k = et; k < MMA_BN; k += 32 * MMA_EPI_WARPS) {
+                const int b = cb * MMA_BN + k;
+                hl[k] = (b < h) ? __ldg(hlist + b) : -1;
             }
+            named_bar(1, 32 * MMA_EPI_WARPS);  // heavy ids of this tile's columns visible to all epilogue warps
+            const int a = rb * MMA_BM + q * 32 + lane;  // this thread's TMEM lane = output row
+            const int W = ws.desc[p].W;
+            const bool arow = a < h;
+            const int ja = arow ? __ldg(hlist + a) : 0;
+            s_eb[ew * 32 + lane] = arow ? __ldg(ws.rowptr + p * ws.rp_stride + ja) : -1;
+            const uint2* up0 = ws.heavy_UP + p * ws.heavy_UP_stride;
+            uint32_t* edges = ws.edges + p * ws.edges_stride;
+            uint16_t* vt = s_vt + ew * 32 * 34;  // this warp's 32×32 transpose buffer
+            const int bt = cb * MMA_BN;
+            mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c = half * (MMA_BN / 64); c < (half + 1) * (MMA_BN / 64); ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * MMA_BN + c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c == (half + 1) * (MMA_BN / 64) - 1) {  // my half drained: hand it back to the MMA issuer
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
+                }
+                // transpose through shared memory: afterwards lane = column, loop over the warp's 32 rows, so
+                // the UP reads and edge stores of one row are coalesced
+#pragma unroll
+                for (int k = 0; k < 32; ++k) vt[lane * 34 + k] = (uint16_t)v[k];
+                __syncwarp();
+                const int b = bt + c * 32 + lane;
+                const int jb = hl[c * 32 + lane];
+                const uint32_t bit = 1u << (jb & 31);
+                const int wb = jb >> 5;
+                const int a0 = rb * MMA_BM + q * 32;
+                uint2 u[32];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {  // all 32 rows' words in flight at once
+                    const bool ok = s_eb[ew * 32 + r] >= 0 && jb >= 0 && b > a0 + r;
+                    u[r] = ok ? __ldg(up0 + (int64_t)(a0 + r) * W + wb) : make_uint2(0u, 0u);
+                }
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                    if (u[r].x & bit)
+                        edges[s_eb[ew * 32 + r] + (int)u[r].y + __popc(u[r].x & (bit - 1u))] =
+                            ((uint32_t)jb << 16) | vt[r * 34 + lane];
+                __syncwarp();
+            }
+            named_bar(1, 32 * MMA_EPI_WARPS);  // everyone done with hl[acc] before it is refilled two tiles later
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
@@ -205,7 +295,7 @@ __global__ void __launch_bounds__(256) k_sc2_dp4a(WS ws) {
     const int h = ws.st[p].heavy_h;
     const int a0 = blockIdx.y * 64, b0 = blockIdx.x * 64;
     if (a0 >= h || b0 >= h || b0 + 63 < a0) return;
-    const int K = (ws.sc2_variant & 4) ? (ws.st[p].n_dense + MMA_BK - 1) / MMA_BK * MMA_BK : d.W * 32;
+    const int K = d.W * 32;
     const uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     uint32_t acc[4][4] = {};
@@ -229,6 +319,29 @@ __global__ void __launch_bounds__(256) k_sc2_dp4a(WS ws) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             D[(int64_t)(a0 + ty * 4 + i) * ws.heavy_cap + b0 + tx * 4 + j] = (uint16_t)acc[i][j];
+}
+
+// Edge emission from D for the CUDA-core path: one warp per heavy row a, lanes over the columns b > a
+// (same test and slot as the tensor-core epilogue).
+__global__ void __launch_bounds__(256) k_emit_hh(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    if (d.n == 0) return;
+    const int h = ws.st[p].heavy_h;
+    const int a = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (a >= h) return;
+    const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
+    const int ja = hlist[a];
+    const int ebase = ws.rowptr[p * ws.rp_stride + ja];
+    const uint2* up = ws.heavy_UP + p * ws.heavy_UP_stride + (int64_t)a * d.W;
+    const uint16_t* Drow = ws.heavy_D + p * ws.heavy_D_stride + (int64_t)a * ws.heavy_cap;
+    uint32_t* edges = ws.edges + p * ws.edges_stride;
+    for (int b = a + 1 + lane; b < h; b += 32) {
+        const int jb = hlist[b];
+        const uint2 u = up[jb >> 5];
+        const uint32_t bit = 1u << (jb & 31);
+        if (u.x & bit) edges[ebase + (int)u.y + __popc(u.x & (bit - 1u))] = ((uint32_t)jb << 16) | Drow[b];
+    }
 }
 
 }  // namespace trk

@@ -292,14 +292,14 @@ def test_compat_adversarial_threshold_ties(tr_mod, scale, tau):
     assert (got == ref).all(), int((got != ref).sum())
 
 
-@pytest.mark.parametrize("variant", [1, 2, 4, 7])
+@pytest.mark.parametrize("path", [0, 2])
 @pytest.mark.parametrize("key,n", [("B", 2500), ("C", 3000), ("D", 1800)])
-def test_sc2_variants_agree_with_oracle(tr_mod, variant, key, n):
-    # static striding, warp-cooperative dense counts, K-restricted tensor-core block + sparse-column correction
+def test_heavy_block_paths_agree_with_oracle(tr_mod, path, key, n):
+    # every row eligible for the dense block: tensor-core epilogue emission vs CUDA-core D + k_emit_hh
     cfg = synth.CONFIGS[key]
     inst = synth.workload_instance(cfg, pair=2, n=n)
     tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n)
-    tr.set_option("sc2_variant", variant)
+    tr.set_option("sc2_path", path)
     tr.set_option("heavy_min_rows", 1)
     res = tr.register(inst["src"], inst["dst"])
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
@@ -315,3 +315,24 @@ def test_compat_variants_agree_with_oracle(tr_mod, variant, key, n):
     tr.set_option("compat_variant", variant)
     res = tr.register(inst["src"], inst["dst"])
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+def test_heavy_block_batch_mixed(tr_mod):
+    # the persistent tensor-core kernel walks one (pair, tile) list across pairs with different |H|,
+    # including pairs with no dense block (tiny / empty) between them
+    cfg = synth.CONFIGS["B"]
+    sizes = [1500, 40, 2200, 0, 900, 2600]
+    srcs, dsts = [], []
+    for p, n in enumerate(sizes):
+        inst = synth.workload_instance(synth.CONFIGS["BCD"[p % 3]], pair=30 + p, n=max(n, 1))
+        srcs.append(inst["src"][:n])
+        dsts.append(inst["dst"][:n])
+    n = np.array(sizes, np.int32)
+    off = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=max(sizes), max_batch=len(sizes))
+    tr.set_option("heavy_min_rows", 1)
+    res = tr.register_batch(np.concatenate(srcs), np.concatenate(dsts), off, n)
+    for p in range(len(sizes)):
+        if sizes[p] >= 3:
+            r = {k: res[p][k] for k in res.dtype.names}
+            compare_pair(tr, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
