@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
 """Summarise an ncu report for profiles/: per kernel launch duration, DRAM bytes, SM/tensor/L2 throughput,
-occupancy, IPC.  usage: python tools/ncu_summary.py report.ncu-rep out_prefix"""
+occupancy, IPC.  usage: python tools/ncu_summary.py report.ncu-rep out_prefix [pairs_per_launch]
+With pairs_per_launch, also writes <dir of out_prefix>/ncu_traffic.json (DRAM bytes per pair per kernel),
+which bench.py reads for the roofline "traffic" field."""
 import csv
 import io
 import json
@@ -71,3 +73,14 @@ with open(out + ".txt", "w") as f:
                 f"occ {v.get('occupancy_pct', 0):5.1f}%  ipc {v.get('ipc', 0):4.2f}  regs {v.get('registers', 0):.0f}"
                 + (f"  int8 {v['tensor_int8_ops']/1e9:.1f} Gop" if v.get("tensor_int8_ops") else "") + "\n")
 print(open(out + ".txt").read())
+
+if len(sys.argv) > 3:
+    import os
+
+    pairs = int(sys.argv[3])
+    tr = {}
+    for k, v in summary.items():
+        name = k.split("<")[0].split("(")[0].replace("void ", "").strip()
+        tr[name] = {"dram_bytes_per_pair": v["dram_bytes"] / pairs, "pairs_in_capture": pairs,
+                    "source": os.path.relpath(out + ".json", os.path.dirname(os.path.dirname(os.path.abspath(out))) + "/..")}
+    json.dump(tr, open(os.path.join(os.path.dirname(out), "ncu_traffic.json"), "w"), indent=1, sort_keys=True)
