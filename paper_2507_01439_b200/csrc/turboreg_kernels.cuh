@@ -1056,7 +1056,27 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
 // ------------------------------------------------------------------------------------------ a3 heavy split
 // Full degrees (popcount of each bit row), their sum and maximum, and the sorted uint16 neighbour list of
 // every row with degree <= LIST_MAX (zero-padded to a 16-byte chunk); one warp per row.
-constexpr int DEG_GROUP = 8;
+// Degrees and the sorted lists of sparse rows.  Lane l owns 8 consecutive words [g + 8l, g + 8l + 8) of a
+// 256-word group (two 16-byte loads), so lane order is column order and one warp scan of the per-lane
+// counts places every lane's entries; only rows with degree <= LIST_MAX extract their set bits.
+__device__ __forceinline__ void deg_load8(const uint32_t* ri, int w0, int W, uint32_t (&v)[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint4 q = (w0 + 4 * h < W) ? __ldg(reinterpret_cast<const uint4*>(ri + w0 + 4 * h)) : make_uint4(0, 0, 0, 0);
+        v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
+    }
+}
+__device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int pos, uint16_t* L) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint32_t x = v[k];
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1u;
+            L[pos++] = (uint16_t)((w0 + k) * 32 + b);
+        }
+    }
+}
 __global__ void __launch_bounds__(256) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
@@ -1072,43 +1092,66 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
     int mx = 0;
     const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
-    for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+    auto finish_row = [&](int i, int deg, int ucnt) {
         uint16_t* L = lists + (int64_t)i * LIST_MAX;
-        const uint32_t* ri = bits + (int64_t)i * W;
-        int carry = 0;
-        unsigned ucnt = 0;
-        // DEG_GROUP words per lane are loaded before any is used, so a warp keeps a whole row (n <= 8192)
-        // in flight instead of one dependent 128-byte load per round
-        for (int c0 = 0; c0 * 32 < W; c0 += DEG_GROUP) {
-            uint32_t vv[DEG_GROUP];
+        if (deg <= LIST_MAX)
+            for (int t = deg + lane; t < ((deg + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
+        ucnt = (int)__reduce_add_sync(FULL, (unsigned)ucnt);
+        if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = deg; ws.deg[p * ws.row_stride + i] = ucnt; }
+        mine += deg;
+        mx = max(mx, deg);
+    };
+    if (W <= 256) {  // the whole row in registers; the next row's words are in flight meanwhile
+        const int w0 = 8 * lane;
+        uint32_t vn[8];
+        if (row0 + warp < row1) deg_load8(bits + (int64_t)(row0 + warp) * W, w0, W, vn);
+        for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+            uint32_t v[8];
 #pragma unroll
-            for (int k = 0; k < DEG_GROUP; ++k) {
-                const int w = (c0 + k) * 32 + lane;
-                vv[k] = (w < W) ? __ldg(ri + w) : 0u;
-            }
+            for (int k = 0; k < 8; ++k) v[k] = vn[k];
+            if (i + SEL_WARPS < row1) deg_load8(bits + (int64_t)(i + SEL_WARPS) * W, w0, W, vn);
+            int cnt = 0, ucnt = 0;
 #pragma unroll
-            for (int k = 0; k < DEG_GROUP; ++k) {
-                if ((c0 + k) * 32 >= W) break;
-                const int w = (c0 + k) * 32 + lane;
-                uint32_t v = vv[k];
-                ucnt += __popc(upper_mask(v, w, i));
-                const int cnt = __popc(v);
-                const int incl = warp_incl_scan(cnt);
-                int pos = carry + incl - cnt;
-                while (v && pos < LIST_MAX) {
-                    const int b = __ffs(v) - 1;
-                    v &= v - 1u;
-                    L[pos++] = (uint16_t)(w * 32 + b);
-                }
-                carry += __shfl_sync(FULL, incl, 31);
+            for (int k = 0; k < 8; ++k) {
+                cnt += __popc(v[k]);
+                ucnt += __popc(upper_mask(v[k], w0 + k, i));
             }
+            const int incl = warp_incl_scan(cnt);
+            const int deg = __shfl_sync(FULL, incl, 31);
+            if (deg <= LIST_MAX) deg_extract8(v, w0, incl - cnt, lists + (int64_t)i * LIST_MAX);
+            finish_row(i, deg, ucnt);
         }
-        if (carry <= LIST_MAX)
-            for (int t = carry + lane; t < ((carry + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
-        ucnt = __reduce_add_sync(FULL, ucnt);
-        if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = carry; ws.deg[p * ws.row_stride + i] = (int)ucnt; }
-        mine += carry;
-        mx = max(mx, carry);
+    } else {  // n > 8192: count first, extract in a second pass if sparse
+        for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+            const uint32_t* ri = bits + (int64_t)i * W;
+            int deg = 0, ucnt = 0;
+            for (int g = 0; g < W; g += 256) {
+                uint32_t v[8];
+                const int w0 = g + 8 * lane;
+                deg_load8(ri, w0, W, v);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    deg += __popc(v[k]);
+                    ucnt += __popc(upper_mask(v[k], w0 + k, i));
+                }
+            }
+            deg = __reduce_add_sync(FULL, (unsigned)deg);
+            if (deg <= LIST_MAX) {
+                int carry = 0;
+                for (int g = 0; g < W; g += 256) {
+                    uint32_t v[8];
+                    const int w0 = g + 8 * lane;
+                    deg_load8(ri, w0, W, v);
+                    int cnt = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) cnt += __popc(v[k]);
+                    const int incl = warp_incl_scan(cnt);
+                    deg_extract8(v, w0, carry + incl - cnt, lists + (int64_t)i * LIST_MAX);
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+            }
+            finish_row(i, deg, ucnt);
+        }
     }
     if (lane == 0 && mine) { atomicAdd(&s_sum, (unsigned long long)mine); atomicMax(&s_max, mx); }
     __syncthreads();
@@ -1769,12 +1812,14 @@ __global__ void __launch_bounds__(128) k_kabsch(WS ws) {
 constexpr int SCORE_THREADS = 128;               // each thread scores two hypotheses
 constexpr int SCORE_HT = 2 * SCORE_THREADS;      // hypotheses per block
 constexpr int SCORE_PC = 512;                    // correspondences per pipeline stage
+constexpr int SCORE_SEGS = 4;                    // correspondence segments per hypothesis block (grid balance)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // g(T) = inlier number.  A block owns 256 hypotheses of one pair (two per thread, packed as
-// f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and streams all N
-// correspondences through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
+// f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and one of
+// SCORE_SEGS contiguous segments of the N correspondences (partial counts meet in one atomicAdd per
+// hypothesis; the finer grid leaves no half-empty last wave), streamed through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
 __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
@@ -1786,7 +1831,10 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
     const int n = d.n;
     if (n == 0) return;
     const int K = ws.k1 * ws.k2;
-    const int h0 = blockIdx.x * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
+    const int seg = blockIdx.x % SCORE_SEGS;
+    const int h0 = (blockIdx.x / SCORE_SEGS) * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
+    const int pseg = (n + SCORE_SEGS - 1) / SCORE_SEGS;
+    const int pbeg = min(n, seg * pseg), np = min(n, pbeg + pseg) - pbeg;  // this block's points
     float R0[12], R1[12];
     bool v0 = false, v1 = false;
     float* hp0 = ws.hyp + (q * ws.cl_stride + h0) * 16;
@@ -1807,7 +1855,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
         R1[0] = a.x; R1[1] = a.y; R1[2] = a.z; R1[3] = a.w; R1[4] = b.x; R1[5] = b.y; R1[6] = b.z; R1[7] = b.w;
         R1[8] = c.x; R1[9] = c.y; R1[10] = c.z; R1[11] = c.w;
     }
-    if (!__syncthreads_or(v0 || v1)) return;
+    if (!__syncthreads_or((v0 || v1) && np > 0)) return;
     const uint32_t bar0 = smem_u32(&s_bar[0]), bar1 = smem_u32(&s_bar[1]);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
@@ -1815,12 +1863,12 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int nchunks = (n + SCORE_PC - 1) / SCORE_PC;
-    const float4* gs = ws.src4 + q * ws.pts_stride;
-    const float4* gd = ws.dst4 + q * ws.pts_stride;
+    const int nchunks = (np + SCORE_PC - 1) / SCORE_PC;
+    const float4* gs = ws.src4 + q * ws.pts_stride + pbeg;
+    const float4* gd = ws.dst4 + q * ws.pts_stride + pbeg;
     auto issue = [&](int c) {  // thread 0: stage chunk c into buffer c & 1
         const int st = c & 1;
-        const int kc = min(SCORE_PC, n - c * SCORE_PC);
+        const int kc = min(SCORE_PC, np - c * SCORE_PC);
         const uint32_t bytes = (uint32_t)kc * 16u;
         const uint32_t bar = st ? bar1 : bar0;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * bytes) : "memory");
@@ -1856,7 +1904,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
                     : "memory");
             }
         }
-        const int kc = min(SCORE_PC, n - c * SCORE_PC);
+        const int kc = min(SCORE_PC, np - c * SCORE_PC);
         const float4* xs = s_src[st];
         const float4* ys = s_dst[st];
 #pragma unroll 4

@@ -406,7 +406,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
-            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT), B);
+            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT * trk::SCORE_SEGS), B);
             trk::k_score<<<g, trk::SCORE_THREADS, 0, s>>>(ws);
         }));
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));

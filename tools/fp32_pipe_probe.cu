@@ -25,6 +25,10 @@ __global__ void k(float* out, int iters, float s) {
             if (MODE == 1) v[i] = ffma2(v[i], m, v[(i + 1) & 7]);
             if (MODE == 2) { if (i & 1) f[i] = fmaf(f[i], s, f[(i + 1) & 7]); else v[i] = ffma2(v[i], m, v[(i + 1) & 7]); }
             if (MODE == 3) v[i] = ffma2(v[i], m, a);
+            if (MODE == 4) {  // one operand a scalar broadcast (.F32), as in the compat/score loops
+                const u64 bs = ((u64)__float_as_uint(f[i]) << 32) | __float_as_uint(f[i]);
+                v[i] = ffma2(v[i], bs, v[(i + 1) & 7]);
+            }
         }
     }
     float acc = 0.f;
@@ -38,9 +42,10 @@ int main() {
     float* out;
     cudaMalloc(&out, sizeof(float) * sms * 8 * 1024);
     const int iters = 20000;
-    const char* names[4] = {"FFMA scalar (3-reg)", "FFMA2 (3-reg pairs)", "mix FFMA2 + FFMA", "FFMA2 (const pair)"};
-    const double lanes_per_inst[4] = {1, 2, 1.5, 2};
-    for (int mode = 0; mode < 4; ++mode) {
+    const char* names[5] = {"FFMA scalar (3-reg)", "FFMA2 (3-reg pairs)", "mix FFMA2 + FFMA", "FFMA2 (const pair)",
+                            "FFMA2 (scalar bcast)"};
+    const double lanes_per_inst[5] = {1, 2, 1.5, 2, 2};
+    for (int mode = 0; mode < 5; ++mode) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         for (int rep = 0; rep < 2; ++rep) {
@@ -49,6 +54,7 @@ int main() {
             if (mode == 1) k<1><<<sms * 8, 256>>>(out, iters, 1.0001f);
             if (mode == 2) k<2><<<sms * 8, 256>>>(out, iters, 1.0001f);
             if (mode == 3) k<3><<<sms * 8, 256>>>(out, iters, 1.0001f);
+            if (mode == 4) k<4><<<sms * 8, 256>>>(out, iters, 1.0001f);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
         }
