@@ -505,7 +505,7 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
 }
 
 template <bool BASE, int MINB = 4, int UNR = 8, int NP = 1>
-__global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
+__global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
     __shared__ float4 s_rs[64];
     __shared__ float4 s_rd[64];
     __shared__ float4 s_pxy[2][16];
@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
     if (n == 0) return;
     const int W = d.W;
     const int T = (n + 31) >> 5;
-    const int b = blockIdx.x;
+    // `split` blocks share a block-row pair (small batches: enough blocks to fill the GPU); block part sp
+    // takes every split-th item of the pair's work list
+    const int b = blockIdx.x / split, sp = blockIdx.x % split;
     if (2 * b >= T) return;
     const int warp = threadIdx.x >> 5;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
                 s_rd[t] = q;
             }
             __syncthreads();
-            for (int J = I + warp; J < T; J += 8)
+            for (int J = I + warp + 8 * sp; J < T; J += 8 * split)
                 compat_tile_base(ws, p, n, W, T, I, J, s_rs, s_rd);
         }
     } else {
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
         if constexpr (NP < 0) {
             constexpr int NC = -NP;
             const int P0 = (T - I0 + NC - 1) / NC, P1 = (I1 != I0) ? (T - I1 + NC - 1) / NC : 0;
-            for (int t = warp; t < P0 + P1; t += 8) {
+            for (int t = warp + 8 * sp; t < P0 + P1; t += 8 * split) {
                 const bool second = t >= P0;
                 const int I = second ? I1 : I0, J = I + NC * (second ? t - P0 : t), o = second ? 32 : 0, h = second;
                 compat_tiles_rp<NC, UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_pxy[h], s_pz[h], s_qxy[h],
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws) {
         }
         constexpr int NT = 2 * (NP > 0 ? NP : 1);
         const int P0 = (T - I0 + NT - 1) / NT, P1 = (I1 != I0) ? (T - I1 + NT - 1) / NT : 0;
-        for (int t = warp; t < P0 + P1; t += 8) {
+        for (int t = warp + 8 * sp; t < P0 + P1; t += 8 * split) {
             const bool second = t >= P0;
             const int I = second ? I1 : I0, J = I + NT * (second ? t - P0 : t), o = second ? 32 : 0;
             compat_tiles<(NP > 0 ? NP : 1), UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_nr + o, s_nd + o, s_col[warp]);
@@ -1186,6 +1188,24 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
         __syncthreads();
         if (cnt <= ws.heavy_cap) break;
         thr += max(1, thr / 4);
+    }
+    // widen H to every non-sparse row (degree > LIST_MAX) when that costs no extra 256-row block of the
+    // tensor-core contraction: those rows' dense-dense edges then come from the tensor cores instead of the
+    // latency-bound popcount path
+    {
+        const int thr2 = max(ws.heavy_min_deg, LIST_MAX + 1);
+        if (thr2 < thr) {
+            if (t == 0) s_cnt = 0;
+            __syncthreads();
+            int c = 0;
+            for (int i = t; i < n; i += 1024) c += deg[i] >= thr2;
+            c = __reduce_add_sync(FULL, (unsigned)c);
+            if (lane == 0 && c) atomicAdd(&s_cnt, c);
+            __syncthreads();
+            const int cnt2 = s_cnt;
+            __syncthreads();
+            if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
+        }
     }
     const bool use = ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
     if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; }
@@ -1812,17 +1832,16 @@ __global__ void __launch_bounds__(128) k_kabsch(WS ws) {
 constexpr int SCORE_THREADS = 128;               // each thread scores two hypotheses
 constexpr int SCORE_HT = 2 * SCORE_THREADS;      // hypotheses per block
 constexpr int SCORE_PC = 512;                    // correspondences per pipeline stage
-constexpr int SCORE_SEGS = 4;                    // correspondence segments per hypothesis block (grid balance)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // g(T) = inlier number.  A block owns 256 hypotheses of one pair (two per thread, packed as
 // f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and one of
-// SCORE_SEGS contiguous segments of the N correspondences (partial counts meet in one atomicAdd per
+// `segs` contiguous segments of the N correspondences (partial counts meet in one atomicAdd per
 // hypothesis; the finer grid leaves no half-empty last wave), streamed through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
-__global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
+__global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
     __shared__ __align__(16) float4 s_src[2][SCORE_PC];
     __shared__ __align__(16) float4 s_dst[2][SCORE_PC];
     __shared__ __align__(8) unsigned long long s_bar[2];
@@ -1831,9 +1850,9 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws) {
     const int n = d.n;
     if (n == 0) return;
     const int K = ws.k1 * ws.k2;
-    const int seg = blockIdx.x % SCORE_SEGS;
-    const int h0 = (blockIdx.x / SCORE_SEGS) * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
-    const int pseg = (n + SCORE_SEGS - 1) / SCORE_SEGS;
+    const int seg = blockIdx.x % segs;
+    const int h0 = (blockIdx.x / segs) * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
+    const int pseg = (n + segs - 1) / segs;
     const int pbeg = min(n, seg * pseg), np = min(n, pbeg + pseg) - pbeg;  // this block's points
     float R0[12], R1[12];
     bool v0 = false, v1 = false;

@@ -333,12 +333,15 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
         }));
         const int T = (maxn_batch + 31) / 32;
+        // small batches: several blocks share a block-row pair so the grid still covers ~2 waves
+        const int bpp = (T + 1) / 2;
+        const int split = std::max(1, std::min(8, (2 * c->num_sms + bpp * batch - 1) / (bpp * batch)));
         CK(L.run(KID_COMPAT, [&] {
-            const dim3 g((unsigned)((T + 1) / 2), B);
-            if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws);
-            else if (c->opt_compat_variant == 1) trk::k_compat<false, 4, 8, 1><<<g, 256, 0, s>>>(ws);
-            else if (c->opt_compat_variant == 2) trk::k_compat<false, 4, 16, -1><<<g, 256, 0, s>>>(ws);
-            else trk::k_compat<false, 3, 8, -2><<<g, 256, 0, s>>>(ws);
+            const dim3 g((unsigned)(bpp * split), B);
+            if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws, split);
+            else if (c->opt_compat_variant == 1) trk::k_compat<false, 4, 8, 1><<<g, 256, 0, s>>>(ws, split);
+            else if (c->opt_compat_variant == 2) trk::k_compat<false, 4, 16, -1><<<g, 256, 0, s>>>(ws, split);
+            else trk::k_compat<false, 3, 8, -2><<<g, 256, 0, s>>>(ws, split);
         }));
     }
     const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
@@ -365,7 +368,9 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     const int wpl = (Wb + 31) / 32;
     {
-        const dim3 gp((unsigned)trk::SC2_BLOCKS_PER_PAIR, B);
+        const int sc2_bpp = std::max(trk::SC2_BLOCKS_PER_PAIR,
+                                     std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
+        const dim3 gp((unsigned)sc2_bpp, B);
         CK(L.run(KID_SC2, [&] {
             if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws);
             else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws);
@@ -388,7 +393,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         }));
     }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
-    const dim3 gflat(trk::SEL_BLOCKS_PER_PAIR, B);
+    const int sel_bpp = std::max(trk::SEL_BLOCKS_PER_PAIR, std::min((4 * c->num_sms + batch - 1) / batch, 256));
+    const dim3 gflat((unsigned)sel_bpp, B);
     CK(L.run(KID_HIST_HI, [&] { trk::k_hist_hi<<<gflat, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HIST_LO, [&] { trk::k_hist_lo<<<gflat, 256, 0, s>>>(ws); }));
     CK(L.run(KID_ALPHA, [&] { trk::k_alpha<<<B, 256, 0, s>>>(ws); }));
@@ -406,8 +412,10 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
-            const dim3 g((unsigned)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT * trk::SCORE_SEGS), B);
-            trk::k_score<<<g, trk::SCORE_THREADS, 0, s>>>(ws);
+            const int hb = (int)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT);
+            const int segs = std::max(2, std::min(16, (7 * c->num_sms + hb * batch - 1) / (hb * batch)));
+            const dim3 g((unsigned)(hb * segs), B);
+            trk::k_score<<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
         }));
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
     }
