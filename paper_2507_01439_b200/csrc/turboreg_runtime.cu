@@ -91,6 +91,14 @@ struct turboreg_ctx {
     double k_ms[KID_COUNT] = {0};
     int64_t k_launches[KID_COUNT] = {0};
     int64_t launches = 0;
+    // CUDA graphs of the launch sequence, one per (batch, max n, mode); dropped whenever ws changes
+    struct GraphEntry {
+        int32_t batch, maxn, mode;
+        cudaGraphExec_t exec;
+        std::vector<int> kids;
+    };
+    std::vector<GraphEntry> graphs;
+    bool use_graphs = true;
     // SC^2 heavy/light split
     int32_t heavy_cap_alloc = 0;
     CUtensorMap tmX;
@@ -129,7 +137,13 @@ bool params_valid(const turboreg_params* p) {
     return true;
 }
 
+void drop_graphs(turboreg_ctx* c) {
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+}
+
 void free_ws(turboreg_ctx* c) {
+    drop_graphs(c);
     if (c->d_base) cudaFree(c->d_base);
     c->d_base = nullptr;
     c->ws_bytes = 0;
@@ -258,6 +272,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
 }
 
 void set_ws_params(turboreg_ctx* c) {
+    drop_graphs(c);  // captured launches hold ws by value
     c->ws.heavy_cap = c->opt_heavy_cap > 0 ? std::min(c->opt_heavy_cap, c->heavy_cap_alloc) : c->heavy_cap_alloc;
     c->ws.heavy_min_rows = c->opt_heavy_min_rows;
     c->ws.heavy_min_deg = c->opt_heavy_min_deg;
@@ -422,6 +437,47 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     return TURBOREG_OK;
 }
 
+// The launch sequence replayed from a CUDA graph (captured on first use of a (batch, max n, mode) shape):
+// one graph launch instead of ~20 kernel launches, which is most of a single pair's latency.  Per-kernel
+// timing needs the events between launches, so timed calls launch directly.
+turboreg_status run_pipeline(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode) {
+    const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
+    if (timed || !c->use_graphs) return launch_all(c, batch, maxn_batch, s, mode);
+    turboreg_ctx::GraphEntry* ge = nullptr;
+    for (auto& g : c->graphs)
+        if (g.batch == batch && g.maxn == maxn_batch && g.mode == (int32_t)mode) ge = &g;
+    if (!ge) {
+        const int64_t l0 = c->launches;
+        int64_t k0[KID_COUNT];
+        std::memcpy(k0, c->k_launches, sizeof(k0));
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            return launch_all(c, batch, maxn_batch, s, mode);  // e.g. the legacy default stream
+        }
+        const turboreg_status st = launch_all(c, batch, maxn_batch, s, mode);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(s, &g);
+        c->launches = l0;
+        turboreg_ctx::GraphEntry e{batch, maxn_batch, (int32_t)mode, nullptr, {}};
+        for (int k = 0; k < KID_COUNT; ++k)
+            for (int64_t r = k0[k]; r < c->k_launches[k]; ++r) e.kids.push_back(k);
+        std::memcpy(c->k_launches, k0, sizeof(k0));
+        if (st != TURBOREG_OK || ec != cudaSuccess || !g || cudaGraphInstantiate(&e.exec, g, 0) != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return st != TURBOREG_OK ? st : launch_all(c, batch, maxn_batch, s, mode);
+        }
+        cudaGraphDestroy(g);
+        if (c->graphs.size() >= 16) drop_graphs(c);
+        c->graphs.push_back(std::move(e));
+        ge = &c->graphs.back();
+    }
+    CK(cudaGraphLaunch(ge->exec, s));
+    c->launches += (int64_t)ge->kids.size();
+    for (int k : ge->kids) c->k_launches[k]++;
+    return TURBOREG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -516,6 +572,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "compat_variant") {
         if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_compat_variant = (int32_t)value;
+    } else if (k == "cuda_graph") {
+        if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->use_graphs = value != 0;
     } else if (k == "heavy_cap") {
         if (value < 0 || value % 256 || value > c->heavy_cap_alloc) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_cap = (int32_t)value;
@@ -612,7 +671,7 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
     }
     CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc) * batch, cudaMemcpyHostToDevice, s));
     c->last_batch = batch;
-    turboreg_status st = launch_all(c, batch, maxn_batch, s, RUN_FULL);
+    turboreg_status st = run_pipeline(c, batch, maxn_batch, s, RUN_FULL);
     if (st != TURBOREG_OK) return st;
     const bool want_stage = c->prm.flags & TURBOREG_F_STAGE_TIMING;
     if (dev_out) {
@@ -759,7 +818,7 @@ turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bit
     CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc), cudaMemcpyHostToDevice, s));
     c->last_batch = 1;
     c->last_n.assign(1, n);
-    turboreg_status st = launch_all(c, 1, n, s, RUN_FROM_ADJ);
+    turboreg_status st = run_pipeline(c, 1, n, s, RUN_FROM_ADJ);
     if (st != TURBOREG_OK) return st;
     CK(cudaStreamSynchronize(s));
     if (!c->profiling) harvest_events(c, nullptr);

@@ -336,3 +336,23 @@ def test_heavy_block_batch_mixed(tr_mod):
         if sizes[p] >= 3:
             r = {k: res[p][k] for k in res.dtype.names}
             compare_pair(tr, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+
+
+def test_graph_replay_matches_direct_launches(tr_mod):
+    # the first call of a shape is captured into a CUDA graph, later calls replay it on new inputs; results
+    # must equal a context that launches directly, for every call and across shape changes
+    cfg = synth.CONFIGS["B"]
+    g = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2500, max_batch=3)
+    d = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2500, max_batch=3)
+    d.set_option("cuda_graph", 0)
+    calls = [(2000, [40]), (2000, [41]), (2500, [42, 43]), (2000, [44]), (2500, [45, 46])]
+    for n, pairs in calls:
+        insts = [synth.workload_instance(cfg, pair=p, n=n) for p in pairs]
+        src = np.concatenate([x["src"] for x in insts])
+        dst = np.concatenate([x["dst"] for x in insts])
+        off = np.arange(len(pairs), dtype=np.int64) * n
+        nn = np.full(len(pairs), n, np.int32)
+        rg = g.register_batch(src, dst, off, nn)
+        rd = d.register_batch(src, dst, off, nn)
+        assert rg.tobytes() == rd.tobytes(), (n, pairs)
+    assert g.launch_count == d.launch_count
