@@ -154,6 +154,9 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "heavy_min_rows"   minimum |H| for the dense block to be used (default 128)
  *   "heavy_min_degree" minimum degree of a heavy row (default 32)
  *   "heavy_cap"        maximum |H| (multiple of 256, <= the allocated capacity)
+ *   "pipeline_host_inputs" 1 = a call with host inputs and >= 16 pairs copies them in 4 sub-batches, each
+ *                      copy overlapping the previous sub-batch's compatibility pass (default); 0 = one copy
+ *                      before one launch sequence
  *   "cuda_graph"       1 = replay the launch sequence from a CUDA graph captured per (batch, max n) shape
  *                      (default; calls with stage/kernel timing always launch directly); 0 = launch directly
  *   "compat_variant"   compat-graph tiling: 0 = row pairs in f32x2 lanes x 2 column tiles per warp

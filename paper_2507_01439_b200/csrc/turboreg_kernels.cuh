@@ -57,6 +57,8 @@ struct PairState {
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
 
+constexpr int PIV_CAP = 8192;  // pivot candidates sorted in shared memory per pair
+
 struct WS {
     const PairDesc* desc;
     PairState* st;
@@ -104,7 +106,44 @@ struct WS {
     int32_t heavy_min_rows, heavy_min_deg, sc2_path;
     float tau, tau_base, thr;
     int32_t k1, k2, mode;
+    int32_t pair_base;    // index of pair 0 of this view in the batch (TMA coordinates address the whole batch)
 };
+
+// The workspace restricted to pairs [p0, p0 + count): every per-pair array advanced by p0 strides.
+inline WS ws_view(const WS& w, int p0, size_t result_bytes) {
+    WS v = w;
+    v.desc = w.desc + p0;
+    v.st = w.st + p0;
+    v.src4 = w.src4 + p0 * w.pts_stride;
+    v.dst4 = w.dst4 + p0 * w.pts_stride;
+    v.bits = w.bits + p0 * w.bits_stride;
+    if (w.bits_base) v.bits_base = w.bits_base + p0 * w.bits_stride;
+    v.deg = w.deg + p0 * w.row_stride;
+    v.row_gt = w.row_gt + p0 * w.row_stride;
+    v.row_eq = w.row_eq + p0 * w.row_stride;
+    v.row_take = w.row_take + p0 * w.row_stride;
+    v.row_off = w.row_off + p0 * w.row_stride;
+    v.edges = w.edges + p0 * w.edges_stride;
+    v.rowptr = w.rowptr + p0 * w.rp_stride;
+    v.piv = w.piv + p0 * w.piv_stride;
+    v.cand = w.cand + (int64_t)p0 * PIV_CAP;
+    v.cliq = w.cliq + p0 * w.cl_stride;
+    v.hyp = w.hyp + p0 * w.cl_stride * 16;
+    v.res = static_cast<char*>(w.res) + p0 * result_bytes;
+    v.deg_full = w.deg_full + p0 * w.row_stride;
+    v.hpos = w.hpos + p0 * w.row_stride;
+    v.heavy_list = w.heavy_list + (int64_t)p0 * w.heavy_cap;
+    v.lists = w.lists + p0 * w.lists_stride;
+    v.light_list = w.light_list + p0 * w.row_stride;
+    v.dense_list = w.dense_list + p0 * w.row_stride;
+    v.heavy_mask = w.heavy_mask + p0 * (w.bits_stride / w.row_stride);
+    v.light_mask = w.light_mask + p0 * (w.bits_stride / w.row_stride);
+    v.heavy_UP = w.heavy_UP + p0 * w.heavy_UP_stride;
+    v.heavy_X = w.heavy_X + p0 * w.heavy_X_stride;
+    v.heavy_D = w.heavy_D + p0 * w.heavy_D_stride;
+    v.pair_base = w.pair_base + p0;
+    return v;
+}
 
 
 // Row i restricted to its upper part U_i = {c > i} (the O2 out-neighbourhood, Def. 2).
@@ -1372,7 +1411,6 @@ __global__ void __launch_bounds__(256) k_alpha(WS ws) {
 
 // Every edge with weight > α, or == α, is a pivot candidate: its key ((0x7fff − w) << 30 | i << 15 | j)
 // orders candidates by (w desc, i asc, j asc) (readings r4, r5).  Warp-aggregated append.
-constexpr int PIV_CAP = 8192;
 __global__ void __launch_bounds__(256) k_collect(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];

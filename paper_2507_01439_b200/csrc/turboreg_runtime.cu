@@ -59,6 +59,7 @@ const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
 constexpr int HEAVY_CAP_MAX = 2048;
+constexpr int NCHUNK = 4;  // sub-batches of a pipelined host-input call
 
 
 }  // namespace
@@ -68,6 +69,9 @@ struct turboreg_ctx {
     int device = 0;
     int32_t max_n = 0, max_batch = 0, Wmax = 0;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-input sub-batches
+    cudaEvent_t ev_start = nullptr, ev_chunk[NCHUNK] = {};
+    bool use_chunks = true;
     // device workspace
     void* d_base = nullptr;
     size_t ws_bytes = 0;
@@ -93,7 +97,7 @@ struct turboreg_ctx {
     int64_t launches = 0;
     // CUDA graphs of the launch sequence, one per (batch, max n, mode); dropped whenever ws changes
     struct GraphEntry {
-        int32_t batch, maxn, mode;
+        int32_t batch, maxn, mode, p0, phase;
         cudaGraphExec_t exec;
         std::vector<int> kids;
     };
@@ -335,15 +339,22 @@ void harvest_events(turboreg_ctx* c, float* stage_ms) {
 
 enum RunMode { RUN_FULL = 0, RUN_FROM_ADJ = 1 };
 
-turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode) {
-    trk::WS ws = c->ws;
+// phase: PH_ALL = the whole path; PH_HEAD = state reset + ingest + compat (per pipelined sub-batch);
+// PH_TAIL = everything after compat.
+enum Phase { PH_ALL = 0, PH_HEAD = 1, PH_TAIL = 2 };
+
+turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode,
+                           int32_t p0 = 0, int phase = PH_ALL) {
+    trk::WS ws = p0 ? trk::ws_view(c->ws, p0, sizeof(turboreg_result)) : c->ws;
     const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
     Launcher L{c, s, timed};
     const int Wb = words_per_row(std::max(maxn_batch, 1));
     const unsigned B = (unsigned)batch;
-    CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
-    CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 16, s));
-    if (mode == RUN_FULL) {
+    if (phase != PH_TAIL) {
+        CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
+        CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 16, s));
+    }
+    if (mode == RUN_FULL && phase != PH_TAIL) {
         CK(L.run(KID_INGEST, [&] {
             trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
         }));
@@ -359,6 +370,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else trk::k_compat<false, 3, 8, -2><<<g, 256, 0, s>>>(ws, split);
         }));
     }
+    if (phase == PH_HEAD) return TURBOREG_OK;
     const dim3 grow((maxn_batch + trk::SC2_ROWS_PER_BLOCK - 1) / trk::SC2_ROWS_PER_BLOCK, B);
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
@@ -440,32 +452,34 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
 // The launch sequence replayed from a CUDA graph (captured on first use of a (batch, max n, mode) shape):
 // one graph launch instead of ~20 kernel launches, which is most of a single pair's latency.  Per-kernel
 // timing needs the events between launches, so timed calls launch directly.
-turboreg_status run_pipeline(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode) {
+turboreg_status run_pipeline(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode,
+                             int32_t p0 = 0, int phase = PH_ALL) {
     const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
-    if (timed || !c->use_graphs) return launch_all(c, batch, maxn_batch, s, mode);
+    if (timed || !c->use_graphs) return launch_all(c, batch, maxn_batch, s, mode, p0, phase);
     turboreg_ctx::GraphEntry* ge = nullptr;
     for (auto& g : c->graphs)
-        if (g.batch == batch && g.maxn == maxn_batch && g.mode == (int32_t)mode) ge = &g;
+        if (g.batch == batch && g.maxn == maxn_batch && g.mode == (int32_t)mode && g.p0 == p0 && g.phase == phase)
+            ge = &g;
     if (!ge) {
         const int64_t l0 = c->launches;
         int64_t k0[KID_COUNT];
         std::memcpy(k0, c->k_launches, sizeof(k0));
         if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
             cudaGetLastError();
-            return launch_all(c, batch, maxn_batch, s, mode);  // e.g. the legacy default stream
+            return launch_all(c, batch, maxn_batch, s, mode, p0, phase);  // e.g. the legacy default stream
         }
-        const turboreg_status st = launch_all(c, batch, maxn_batch, s, mode);
+        const turboreg_status st = launch_all(c, batch, maxn_batch, s, mode, p0, phase);
         cudaGraph_t g = nullptr;
         const cudaError_t ec = cudaStreamEndCapture(s, &g);
         c->launches = l0;
-        turboreg_ctx::GraphEntry e{batch, maxn_batch, (int32_t)mode, nullptr, {}};
+        turboreg_ctx::GraphEntry e{batch, maxn_batch, (int32_t)mode, p0, phase, nullptr, {}};
         for (int k = 0; k < KID_COUNT; ++k)
             for (int64_t r = k0[k]; r < c->k_launches[k]; ++r) e.kids.push_back(k);
         std::memcpy(c->k_launches, k0, sizeof(k0));
         if (st != TURBOREG_OK || ec != cudaSuccess || !g || cudaGraphInstantiate(&e.exec, g, 0) != cudaSuccess) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
-            return st != TURBOREG_OK ? st : launch_all(c, batch, maxn_batch, s, mode);
+            return st != TURBOREG_OK ? st : launch_all(c, batch, maxn_batch, s, mode, p0, phase);
         }
         cudaGraphDestroy(g);
         if (c->graphs.size() >= 16) drop_graphs(c);
@@ -517,9 +531,13 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     turboreg_status st = TURBOREG_OK;
     // A blocking stream: it orders itself with the legacy default stream, so inputs produced there (e.g. by
     // torch's default stream) are complete before our kernels read them.
-    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreate(&c->own_stream) != cudaSuccess) {
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreate(&c->own_stream) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess) {
         st = TURBOREG_ERR_CUDA;
     }
+    for (auto& e : c->ev_chunk)
+        if (st == TURBOREG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) st = TURBOREG_ERR_CUDA;
     if (st == TURBOREG_OK) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (st == TURBOREG_OK) st = alloc_ws(c);
     if (st == TURBOREG_OK) {
@@ -572,6 +590,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "compat_variant") {
         if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_compat_variant = (int32_t)value;
+    } else if (k == "pipeline_host_inputs") {
+        if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->use_chunks = value != 0;
     } else if (k == "cuda_graph") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->use_graphs = value != 0;
@@ -610,6 +631,10 @@ void turboreg_destroy(turboreg_ctx* c) {
     if (c->h_desc) cudaFreeHost(c->h_desc);
     if (c->h_results) cudaFreeHost(c->h_results);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    for (auto e : c->ev_chunk)
+        if (e) cudaEventDestroy(e);
     delete c;
 }
 
@@ -624,38 +649,46 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
     const bool dev_in = is_device_ptr(src) && is_device_ptr(dst);
     const bool dev_out = is_device_ptr(out);
     if (is_device_ptr(src) != is_device_ptr(dst)) return TURBOREG_ERR_INVALID_ARGUMENT;
-    // host inputs: copy each pair's rows into the device staging area (pairs are packed contiguously)
+    // Host inputs of a large batch are pipelined: the batch is cut into NCHUNK sub-batches whose H2D copies
+    // run on the copy stream while the previous sub-batch's ingest + compat run (on a view of the
+    // workspace); the rest of the path then runs once on the whole batch.  Device inputs and small batches
+    // run as one launch sequence.
+    const int nchunk = (!dev_in && batch >= 16 && c->use_chunks) ? NCHUNK : 1;
+    int32_t bnd[NCHUNK + 1];
+    for (int k = 0; k <= nchunk; ++k) bnd[k] = (int32_t)((int64_t)batch * k / nchunk);
+    // host inputs: each pair's rows go to the device staging area (pairs packed contiguously)
     const float* dsrc = src;
     const float* ddst = dst;
     std::vector<int64_t> dev_off(offsets, offsets + batch);
+    struct Copy { int64_t dst_off, src_off, len; int chunk; };
+    std::vector<Copy> copies;
     if (!dev_in) {
         int64_t cursor = 0;
-        float* stage_src = c->d_inputs;
-        float* stage_dst = c->d_inputs + 3 * (int64_t)c->max_n * c->max_batch;
-        // coalesce runs of contiguous pairs into single copies
         int32_t p = 0;
-        while (p < batch) {
-            int32_t q = p;
-            int64_t len = (n[p] >= 3 && n[p] <= c->max_n) ? n[p] : 0;
-            while (q + 1 < batch && offsets[q + 1] == offsets[q] + n[q] && n[q + 1] >= 3 && n[q + 1] <= c->max_n && len > 0) {
-                ++q;
-                len += n[q];
+        for (int k = 0; k < nchunk; ++k) {
+            p = bnd[k];
+            while (p < bnd[k + 1]) {  // coalesce runs of contiguous pairs into single copies
+                int32_t q = p;
+                int64_t len = (n[p] >= 3 && n[p] <= c->max_n) ? n[p] : 0;
+                while (q + 1 < bnd[k + 1] && offsets[q + 1] == offsets[q] + n[q] && n[q + 1] >= 3 &&
+                       n[q + 1] <= c->max_n && len > 0) {
+                    ++q;
+                    len += n[q];
+                }
+                if (len > 0) {
+                    copies.push_back({cursor, offsets[p], len, k});
+                    int64_t cc = cursor;
+                    for (int32_t r = p; r <= q; ++r) { dev_off[r] = cc; cc += n[r]; }
+                    cursor += len;
+                }
+                p = q + 1;
             }
-            if (len > 0) {
-                CK(cudaMemcpyAsync(stage_src + 3 * cursor, src + 3 * offsets[p], sizeof(float) * 3 * len,
-                                   cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(stage_dst + 3 * cursor, dst + 3 * offsets[p], sizeof(float) * 3 * len,
-                                   cudaMemcpyHostToDevice, s));
-                int64_t cc = cursor;
-                for (int32_t r = p; r <= q; ++r) { dev_off[r] = cc; cc += n[r]; }
-                cursor += len;
-            }
-            p = q + 1;
         }
-        dsrc = stage_src;
-        ddst = stage_dst;
+        dsrc = c->d_inputs;
+        ddst = c->d_inputs + 3 * (int64_t)c->max_n * c->max_batch;
     }
     int32_t maxn_batch = 3;
+    int32_t maxn_chunk[NCHUNK] = {3, 3, 3, 3};
     c->last_n.assign(n, n + batch);
     for (int32_t p = 0; p < batch; ++p) {
         trk::PairDesc& d = c->h_desc[p];
@@ -668,11 +701,40 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
         d.n = d.host_status ? 0 : n[p];
         d.W = d.n ? words_per_row(d.n) : 0;
         if (d.n > maxn_batch) maxn_batch = d.n;
+        for (int k = 0; k < nchunk; ++k)
+            if (p >= bnd[k] && p < bnd[k + 1] && d.n > maxn_chunk[k]) maxn_chunk[k] = d.n;
     }
     CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc) * batch, cudaMemcpyHostToDevice, s));
     c->last_batch = batch;
-    turboreg_status st = run_pipeline(c, batch, maxn_batch, s, RUN_FULL);
-    if (st != TURBOREG_OK) return st;
+    cudaStream_t cs = nchunk > 1 ? c->copy_stream : s;
+    if (nchunk > 1) {  // the staging area is free once everything queued before on s is done
+        CK(cudaEventRecord(c->ev_start, s));
+        CK(cudaStreamWaitEvent(cs, c->ev_start, 0));
+    }
+    for (int k = 0; k < nchunk; ++k) {
+        for (const Copy& cp : copies) {
+            if (cp.chunk != k) continue;
+            CK(cudaMemcpyAsync(const_cast<float*>(dsrc) + 3 * cp.dst_off, src + 3 * cp.src_off,
+                               sizeof(float) * 3 * cp.len, cudaMemcpyHostToDevice, cs));
+            CK(cudaMemcpyAsync(const_cast<float*>(ddst) + 3 * cp.dst_off, dst + 3 * cp.src_off,
+                               sizeof(float) * 3 * cp.len, cudaMemcpyHostToDevice, cs));
+        }
+        if (nchunk > 1) CK(cudaEventRecord(c->ev_chunk[k], cs));
+    }
+    if (nchunk == 1) {
+        turboreg_status st = run_pipeline(c, batch, maxn_batch, s, RUN_FULL);
+        if (st != TURBOREG_OK) return st;
+    } else {  // compat of sub-batch k overlaps the copy of sub-batch k+1; the rest runs on the whole batch
+        for (int k = 0; k < nchunk; ++k) {
+            CK(cudaStreamWaitEvent(s, c->ev_chunk[k], 0));
+            const int32_t cnt = bnd[k + 1] - bnd[k];
+            if (cnt == 0) continue;
+            turboreg_status st = run_pipeline(c, cnt, maxn_chunk[k], s, RUN_FULL, bnd[k], PH_HEAD);
+            if (st != TURBOREG_OK) return st;
+        }
+        turboreg_status st = run_pipeline(c, batch, maxn_batch, s, RUN_FULL, 0, PH_TAIL);
+        if (st != TURBOREG_OK) return st;
+    }
     const bool want_stage = c->prm.flags & TURBOREG_F_STAGE_TIMING;
     if (dev_out) {
         CK(cudaMemcpyAsync(out, c->d_results, sizeof(turboreg_result) * batch, cudaMemcpyDeviceToDevice, s));

@@ -171,9 +171,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     const uint32_t a_dst = tiles + s * MMA_STAGE_BYTES;
                     const uint32_t b_dst = a_dst + MMA_A_BYTES;
                     mbar_expect_tx(full0 + 8 * s, MMA_STAGE_BYTES);
-                    tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, p);
-                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN, p);
-                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN + 128, p);
+                    tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, ws.pair_base + p);
+                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN, ws.pair_base + p);
+                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN + 128, ws.pair_base + p);
                 }
             }
         }

@@ -356,3 +356,27 @@ def test_graph_replay_matches_direct_launches(tr_mod):
         rd = d.register_batch(src, dst, off, nn)
         assert rg.tobytes() == rd.tobytes(), (n, pairs)
     assert g.launch_count == d.launch_count
+
+
+def test_pipelined_host_batch_matches_single_launch(tr_mod):
+    # >= 16 pairs from host memory run as 4 sub-batches (workspace views, overlapped H2D); results must be
+    # identical to one launch sequence, including empty / too-small pairs at sub-batch edges
+    cfg = synth.CONFIGS["D"]
+    sizes = [1200, 0, 900, 1500, 2, 1100, 1300, 700, 1500, 1000, 1200, 800, 1400, 600, 1500, 1250, 0, 1000, 950]
+    srcs, dsts = [], []
+    for p, n in enumerate(sizes):
+        inst = synth.workload_instance(cfg, pair=60 + p, n=max(n, 1))
+        srcs.append(inst["src"][:n])
+        dsts.append(inst["dst"][:n])
+    n = np.array(sizes, np.int32)
+    off = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64)
+    src, dst = np.concatenate(srcs), np.concatenate(dsts)
+    a = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=1500, max_batch=len(sizes))
+    b = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=1500, max_batch=len(sizes))
+    b.set_option("pipeline_host_inputs", 0)
+    ra = a.register_batch(src, dst, off, n)
+    rb = b.register_batch(src, dst, off, n)
+    assert ra.tobytes() == rb.tobytes()
+    for p in (0, 5, 14):
+        r = {k: ra[p][k] for k in ra.dtype.names}
+        compare_pair(a, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
