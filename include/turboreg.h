@@ -37,6 +37,7 @@ typedef enum {
     TURBOREG_OK = 0,
     TURBOREG_ERR_INVALID_ARGUMENT = 1, /* NULL pointer; tau <= 0; k1 < 1; k2 < 1; inlier_threshold <= 0;
                                           tau_base not 0 and < tau; unknown graph_mode or flags;
+                                          graph_mode 1 with k1*k2 > 16384;
                                           batch < 1 or > max_batch; max_n outside [3, 32768]        */
     TURBOREG_ERR_TOO_FEW_POINTS = 2,   /* N < 3: no 3-clique exists          — per pair */
     TURBOREG_ERR_TOO_MANY_POINTS = 3,  /* N > max_n fixed at create                         — per pair */
@@ -59,7 +60,9 @@ typedef struct {
     int32_t k2;             /* K2 TurboCliques per pivot (Eq. 7); paper: 2                       */
     float inlier_threshold; /* residual bound of g(·), metres, > 0 (paper silent; reading r12)          */
     int32_t graph_mode;     /* 0 = O2Graph (Def. 2, the paper's method); 1 = undirected SC^2 graph
-                               (Table 5 row 10) with duplicate cliques removed (reading r9)       */
+                               (Table 5 row 10): cliques from neighbours on both sides of a pivot,
+                               listed in canonical order (S desc, i, j, z asc) with duplicates removed
+                               (reading r9); requires k1*k2 <= 16384                                    */
     uint32_t flags;         /* TURBOREG_F_*                                                               */
 } turboreg_params;
 
@@ -118,7 +121,8 @@ const char* turboreg_status_string(turboreg_status s);
  *   TURBOREG_I_SC2       int32  [n][n]  Ĝ expanded to a dense symmetric matrix
  *   TURBOREG_I_PIVOTS    int32  [P][3]  (i, j, w) in (w desc, i asc, j asc) order — (i, j) lexicographic
  *                        order when more than 8192 edges reach the cut weight α_K1
- *   TURBOREG_I_CLIQUES   int32  [K1*K2][4] (i, j, z, S) per slot p*K2 + r; empty slots are (-1,-1,-1,0)
+ *   TURBOREG_I_CLIQUES   int32  [K1*K2][4] (i, j, z, S), i < j < z: O2 mode per slot p*K2 + r; SC^2 mode
+ *                        in canonical order, de-duplicated, compacted; empty slots are (-1,-1,-1,0)
  *   TURBOREG_I_HYPS      float  [K1*K2][16]: R[9], t[3], count (int32 bits), flag (int32 bits:
  *                        0 valid, 1 degenerate, 2 empty slot), S (int32 bits), 0
  *   TURBOREG_I_STATE     int64  [16] per-pair scalars: n, W, edges, positive edges, alpha, c_gt, need,

@@ -107,6 +107,7 @@ struct WS {
     float tau, tau_base, thr;
     int32_t k1, k2, mode;
     int32_t pair_base;    // index of pair 0 of this view in the batch (TMA coordinates address the whole batch)
+    uint16_t* uprefix;    // SC^2 mode only: [n][W] exclusive prefix popcount of U_i per word (stride bits_stride)
 };
 
 // The workspace restricted to pairs [p0, p0 + count): every per-pair array advanced by p0 strides.
@@ -142,6 +143,7 @@ inline WS ws_view(const WS& w, int p0, size_t result_bytes) {
     v.heavy_X = w.heavy_X + p0 * w.heavy_X_stride;
     v.heavy_D = w.heavy_D + p0 * w.heavy_D_stride;
     v.pair_base = w.pair_base + p0;
+    if (w.uprefix) v.uprefix = w.uprefix + p0 * w.bits_stride;
     return v;
 }
 
@@ -1151,15 +1153,28 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = vn[k];
             if (i + SEL_WARPS < row1) deg_load8(bits + (int64_t)(i + SEL_WARPS) * W, w0, W, vn);
-            int cnt = 0, ucnt = 0;
+            int cnt = 0, ucnt = 0, uc[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 cnt += __popc(v[k]);
-                ucnt += __popc(upper_mask(v[k], w0 + k, i));
+                uc[k] = __popc(upper_mask(v[k], w0 + k, i));
+                ucnt += uc[k];
             }
             const int incl = warp_incl_scan(cnt);
             const int deg = __shfl_sync(FULL, incl, 31);
             if (deg <= LIST_MAX) deg_extract8(v, w0, incl - cnt, lists + (int64_t)i * LIST_MAX);
+            if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
+                int run = warp_incl_scan(ucnt) - ucnt;
+                uint32_t pk[4];
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) {
+                    pk[k >> 1] = (uint32_t)run | ((uint32_t)(run + uc[k]) << 16);
+                    run += uc[k] + uc[k + 1];
+                }
+                uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
+                if (w0 < W) *reinterpret_cast<uint2*>(up) = make_uint2(pk[0], pk[1]);
+                if (w0 + 4 < W) *reinterpret_cast<uint2*>(up + 4) = make_uint2(pk[2], pk[3]);
+            }
             finish_row(i, deg, ucnt);
         }
     } else {  // n > 8192: count first, extract in a second pass if sparse
@@ -1177,6 +1192,26 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
                 }
             }
             deg = __reduce_add_sync(FULL, (unsigned)deg);
+            if (ws.uprefix) {
+                int carry = 0;
+                for (int g = 0; g < W; g += 256) {
+                    uint32_t v[8];
+                    const int w0 = g + 8 * lane;
+                    deg_load8(ri, w0, W, v);
+                    int uc[8], tot = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) { uc[k] = __popc(upper_mask(v[k], w0 + k, i)); tot += uc[k]; }
+                    const int incl = warp_incl_scan(tot);
+                    int run = carry + incl - tot;
+                    uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (w0 + k < W) up[k] = (uint16_t)run;
+                        run += uc[k];
+                    }
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+            }
             if (deg <= LIST_MAX) {
                 int carry = 0;
                 for (int g = 0; g < W; g += 256) {
@@ -1659,15 +1694,61 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
     }
 }
 
+// SC^2 (undirected) mode, reading r9: N(i,j) = {z ∉ {i,j} : C_iz ∧ C_jz} on both sides of the pivot
+// (Table 5 row 10).  Ĝ_iz for z > i is row i's rank-indexed entry; for z < i the edge lives in row
+// z at rank uprefix[z][i>>5] + popc(U_z word below i).
+__device__ __forceinline__ uint32_t sc2_lower_weight(const WS& ws, int q, int W, int z, int x) {
+    const int wx = x >> 5;
+    const uint32_t u = upper_mask(__ldg(ws.bits + q * ws.bits_stride + (int64_t)z * W + wx), wx, z);
+    const int rk = (int)__ldg(ws.uprefix + q * ws.bits_stride + (int64_t)z * W + wx) + __popc(u & ((1u << (x & 31)) - 1u));
+    return __ldg(ws.edges + q * ws.edges_stride + ws.rowptr[q * ws.rp_stride + z] + rk) & 0xffffu;
+}
+template <typename F>
+__device__ __forceinline__ void pgs_scan_candidates_sc2(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj,
+                                                        int W, int i, int j, const uint32_t* ei, const uint32_t* ej,
+                                                        int wij, F&& f) {
+    const int lane = threadIdx.x & 31;
+    int carry_i = 0, carry_j = 0;
+    const int nchunks = (W + 31) >> 5;
+    for (int c = 0; c < nchunks; ++c) {
+        const int w = c * 32 + lane;
+        const uint32_t vi = (w < W) ? ri[w] : 0u, vj = (w < W) ? rj[w] : 0u;
+        const uint32_t ui = (w < W) ? upper_mask(vi, w, i) : 0u;
+        const uint32_t uj = (w < W) ? upper_mask(vj, w, j) : 0u;
+        const int pi = __popc(ui), pj = __popc(uj);
+        const int si = warp_incl_scan(pi), sj = warp_incl_scan(pj);
+        const int exi = carry_i + si - pi, exj = carry_j + sj - pj;
+        carry_i += __shfl_sync(FULL, si, 31);
+        carry_j += __shfl_sync(FULL, sj, 31);
+        uint32_t m = vi & vj;  // C_ii = C_jj = 0 and C_ij = 1: i and j are never in both rows
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t below = (1u << b) - 1u;
+            const int z = w * 32 + b;
+            const uint32_t wiz = (z > i) ? (__ldg(ei + exi + __popc(ui & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, i);
+            const uint32_t wjz = (z > j) ? (__ldg(ej + exj + __popc(uj & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, j);
+            const int S = wij + (int)wiz + (int)wjz;
+            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+        }
+    }
+}
+
+// A clique as (i, j, z) ascending (O2 mode: z > j > i already; SC^2 mode: z anywhere) and S.
+__device__ __forceinline__ int4 sorted_clique(int i, int j, int z, int S) {
+    const int a = min(i, min(j, z)), c = max(i, max(j, z));
+    return make_int4(a, i + j + z - a - c, c, S);
+}
+
 // Per-lane sorted top-KL lists (KL >= K2) merged by K2 warp argmax rounds.
 template <int KL>
-__device__ __forceinline__ int pgs_topk_list(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
-                                             const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
+__device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj, int W, int i,
+                                             int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
     const int lane = threadIdx.x & 31;
     unsigned long long top[KL];
 #pragma unroll
     for (int r = 0; r < KL; ++r) top[r] = 0ull;
-    pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
+    auto insert = [&](unsigned long long key) {
         if (key > top[KL - 1]) {  // sorted insertion, descending
             unsigned long long k = key;
 #pragma unroll
@@ -1675,7 +1756,9 @@ __device__ __forceinline__ int pgs_topk_list(const uint32_t* ri, const uint32_t*
                 if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
             }
         }
-    });
+    };
+    if (ws.mode == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, insert);
+    else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, insert);
     int emitted = 0;
     for (int r = 0; r < K2; ++r) {
         const unsigned long long head = top[0];
@@ -1688,7 +1771,7 @@ __device__ __forceinline__ int pgs_topk_list(const uint32_t* ri, const uint32_t*
         }
         if (lane == 0) {
             const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
-            out[r] = make_int4(i, j, z, (int)(best >> 32));
+            out[r] = sorted_clique(i, j, z, (int)(best >> 32));
         }
         ++emitted;
     }
@@ -1721,23 +1804,25 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
     int emitted = 0;
     if (K2 <= 2) {
-        emitted = pgs_topk_list<2>(ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<2>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else if (K2 <= 4) {
-        emitted = pgs_topk_list<4>(ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<4>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else if (K2 <= PGS_KL) {
-        emitted = pgs_topk_list<PGS_KL>(ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<PGS_KL>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else {
         unsigned long long thr = ~0ull;
         for (int r = 0; r < K2; ++r) {
             unsigned long long mine = 0ull;
-            pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, [&](unsigned long long key) {
+            auto take = [&](unsigned long long key) {
                 if (key < thr && key > mine) mine = key;
-            });
+            };
+            if (ws.mode == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
+            else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, take);
             const unsigned long long best = warp_max_u64(mine);
             if (best == 0ull) break;
             if (lane == 0) {
                 const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
-                out[r] = make_int4(i, j, z, (int)(best >> 32));
+                out[r] = sorted_clique(i, j, z, (int)(best >> 32));
             }
             thr = best;
             ++emitted;
@@ -1822,6 +1907,67 @@ __device__ bool kabsch3(const float4& x0f, const float4& x1f, const float4& x2f,
     t[1] = cy.y - (R[3] * cx.x + R[4] * cx.y + R[5] * cx.z);
     t[2] = cy.z - (R[6] * cx.x + R[7] * cx.y + R[8] * cx.z);
     return true;
+}
+
+// SC^2 mode only (reading r9): the K1·K2 clique slots of a pair in canonical order (S desc, (i,j,z) asc)
+// with duplicate triples (found from several pivots) dropped, compacted to the front; the rest invalid.
+// One block per pair, bitonic sort of 64-bit keys ((2^18-1-S) << 45 | i << 30 | j << 15 | z) in shared
+// memory (K1·K2 <= CANON_CAP).
+constexpr int CANON_CAP = 16384;
+__global__ void __launch_bounds__(1024) k_canon(WS ws) {
+    extern __shared__ unsigned long long s_key[];
+    __shared__ int s_warp[32];
+    const int q = blockIdx.x;
+    if (ws.desc[q].n == 0) return;
+    const int K = ws.k1 * ws.k2;
+    int4* cl = ws.cliq + q * ws.cl_stride;
+    int m2 = 1;
+    while (m2 < K) m2 <<= 1;
+    for (int k = threadIdx.x; k < m2; k += blockDim.x) {
+        unsigned long long key = ~0ull;
+        if (k < K) {
+            const int4 c = cl[k];
+            if (c.x >= 0)
+                key = ((unsigned long long)(0x3ffff - c.w) << 45) | ((unsigned long long)c.x << 30) |
+                      ((unsigned long long)c.y << 15) | (unsigned long long)c.z;
+        }
+        s_key[k] = key;
+    }
+    __syncthreads();
+    for (int size = 2; size <= m2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int k = threadIdx.x; k < m2 / 2; k += blockDim.x) {
+                const int lo = 2 * k - (k & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = s_key[lo], b = s_key[hi];
+                if ((a > b) == up) { s_key[lo] = b; s_key[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+    // keep the first of each run of equal triples (equal triples have equal S: S is the triangle's weight)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int base = 0;
+    for (int k0 = 0; k0 < K; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        const unsigned long long key = (k < K) ? s_key[k] : ~0ull;
+        const bool keep = key != ~0ull && (k == 0 || s_key[k - 1] != key);
+        const unsigned b = __ballot_sync(FULL, keep);
+        if (lane == 0) s_warp[warp] = __popc(b);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { before += (w < warp) ? s_warp[w] : 0; total += s_warp[w]; }
+        __syncthreads();
+        if (keep) {
+            const int slot = base + before + __popc(b & ((1u << lane) - 1u));
+            cl[slot] = make_int4((int)((key >> 30) & 0x7fff), (int)((key >> 15) & 0x7fff), (int)(key & 0x7fff),
+                                 0x3ffff - (int)(key >> 45));
+        }
+        base += total;
+    }
+    __syncthreads();
+    for (int k = base + threadIdx.x; k < K; k += blockDim.x) cl[k] = make_int4(-1, -1, -1, 0);
 }
 
 __global__ void __launch_bounds__(128) k_kabsch(WS ws) {

@@ -44,6 +44,7 @@ enum KernelId {
     KID_SEL_SCAN,
     KID_SEL_EMIT,
     KID_PGS,
+    KID_CANON,
     KID_KABSCH,
     KID_SCORE,
     KID_FINALIZE,
@@ -52,9 +53,9 @@ enum KernelId {
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
                                        "k_expand",   "k_sc2_mma",      "k_emit_hh",     "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
-                                       "k_kabsch",   "k_score",        "k_finalize"};
+                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -136,7 +137,8 @@ bool params_valid(const turboreg_params* p) {
     if (p->k1 < 1 || p->k2 < 1) return false;
     if ((int64_t)p->k1 * p->k2 > (int64_t)1 << 30) return false;
     if (!(p->inlier_threshold > 0.f) || !std::isfinite(p->inlier_threshold)) return false;
-    if (p->graph_mode != 0) return false;  // undirected SC^2 mode: not in this build yet
+    if (p->graph_mode != 0 && p->graph_mode != 1) return false;
+    if (p->graph_mode == 1 && (int64_t)p->k1 * p->k2 > trk::CANON_CAP) return false;  // canonical sort in smem
     if (p->flags & ~(TURBOREG_F_STAGE_TIMING | TURBOREG_F_KERNEL_TIMING)) return false;
     return true;
 }
@@ -169,7 +171,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -204,6 +206,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(int32_t) * (size_t)((N + 1) * B), &p_rp},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
+    if (c->prm.graph_mode == 1) items.push_back({sizeof(uint16_t) * N * W * B, &p_upre});
     size_t total = 0;
     for (auto& it : items) total += round_up((int64_t)it.bytes, 256);
     void* basep = nullptr;
@@ -246,6 +249,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
     w.light_mask = static_cast<uint32_t*>(p_lm);
     w.heavy_UP = static_cast<uint2*>(p_up);
+    w.uprefix = static_cast<uint16_t*>(p_upre);
     w.heavy_UP_stride = cap * W;
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
@@ -435,6 +439,11 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_PGS, [&] {
         trk::k_pgs<<<dim3((c->prm.k1 + trk::PGS_WARPS - 1) / trk::PGS_WARPS, B), trk::PGS_WARPS * 32, 0, s>>>(ws);
     }));
+    if (c->prm.graph_mode == 1) {  // canonical order + de-duplication of the SC^2-mode clique list (r9)
+        int m2 = 1;
+        while (m2 < c->prm.k1 * c->prm.k2) m2 <<= 1;
+        CK(L.run(KID_CANON, [&] { trk::k_canon<<<B, 1024, sizeof(unsigned long long) * m2, s>>>(ws); }));
+    }
     if (mode == RUN_FULL) {
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
@@ -553,6 +562,8 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     set_ws_params(c);
     if (cudaFuncSetAttribute(trk::k_sc2_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::MMA_SMEM_BYTES) !=
             cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(unsigned long long) * trk::CANON_CAP)) != cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<16>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
@@ -609,6 +620,7 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
 turboreg_status turboreg_set_params(turboreg_ctx* c, const turboreg_params* p) {
     if (!c || !params_valid(p)) return TURBOREG_ERR_INVALID_ARGUMENT;
     const bool realloc = (int64_t)p->k1 * p->k2 != (int64_t)c->prm.k1 * c->prm.k2 || p->k1 != c->prm.k1 ||
+                         p->graph_mode != c->prm.graph_mode ||
                          ((p->tau_base > 0.f) != (c->prm.tau_base > 0.f));
     c->prm = *p;
     set_ws_params(c);

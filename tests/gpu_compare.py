@@ -40,9 +40,9 @@ def gpu_trace(tr, pair=0):
     }
 
 
-def compare_pair(tr, pair, src, dst, tau, k1, k2, thr, result=None, check_graph=True):
+def compare_pair(tr, pair, src, dst, tau, k1, k2, thr, result=None, check_graph=True, graph_mode=0):
     """Assert every match criterion for `pair` of the last call on context `tr`.  Returns stats."""
-    ref = oracle.estimate(src, dst, tau, k1, k2, thr, trace=True)
+    ref = oracle.estimate(src, dst, tau, k1, k2, thr, graph_mode=graph_mode, trace=True)
     g = gpu_trace(tr, pair)
     n = src.shape[0]
     stats = {"n": n, "edges": ref["num_edges"], "near_edges": ref["near_edges"], "cliques": ref["num_cliques"]}
