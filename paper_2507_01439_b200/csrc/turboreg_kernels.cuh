@@ -643,7 +643,9 @@ constexpr int SEL_ROWS_PER_BLOCK = 64;
 constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
 constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
 template <int WPL>
-constexpr int sc2_warp_words() { return 96 * WPL + 32 * WPL; }  // U_i, rank prefix, row i, queue
+constexpr int sc2_warp_words() {  // U_i, rank prefix, row i, queue (+ row i as a byte map for n <= 8192)
+    return 96 * WPL + 32 * WPL + (WPL <= 8 ? 32 * WPL * 32 / 4 : 0);
+}
 template <int WPL>
 constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
 
@@ -712,21 +714,46 @@ __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, in
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
-// Edge between dense row i (bitmap sr, U_i words su, rank prefix sp in shared memory) and sparse row j.
+// As list_bitmap_count_rank, against row i as a byte map (one byte per column, 0/1) in shared memory:
+// one byte load per list entry instead of word load + shift + mask.
+__device__ __forceinline__ uint32_t list_bytemap_count_rank(const uint16_t* L, int len, const uint8_t* sb, int i, int j,
+                                                            int* rank) {
+    const int nch = (len + 7) >> 3;
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+    int r = 0;
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                cnt += (uint32_t)sb[k0] + (uint32_t)sb[k1];
+                r += (k0 > j && k0 < i) + (k1 > j && k1 < i);  // pads are 0 <= j: never counted
+            }
+        }
+    }
+    *rank = r;
+    return cnt - (uint32_t)(nch * 8 - len) * (uint32_t)sb[0];
+}
+
+// Edge between dense row i (bitmap sr — or byte map sb when non-null —, U_i words su, rank prefix sp in
+// shared memory) and sparse row j, on either side of i: one code path for both sides (no divergence).
 __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
                                                 const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
-                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr, int i,
-                                                int j) {
+                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr,
+                                                const uint8_t* sb, int i, int j) {
     const uint16_t* L = lists + (int64_t)j * LIST_MAX;
-    if (j > i) {
-        const uint32_t c = list_bitmap_count(L, deg_full[j], sr);
-        const int wj = j >> 5;
-        erow[sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u))] = ((uint32_t)j << 16) | c;
-    } else {
-        int rank;
-        const uint32_t c = list_bitmap_count_rank(L, deg_full[j], sr, i, j, &rank);
-        edges[rowptr[j] + rank] = ((uint32_t)i << 16) | c;
-    }
+    int rank;
+    const uint32_t c = sb ? list_bytemap_count_rank(L, deg_full[j], sb, i, j, &rank)
+                          : list_bitmap_count_rank(L, deg_full[j], sr, i, j, &rank);
+    const int wj = j >> 5;
+    uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u)) : edges + rowptr[j] + rank;
+    *dst = ((uint32_t)((j > i) ? j : i) << 16) | c;
 }
 
 template <int WPL>
@@ -742,6 +769,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
     uint32_t* sq = su + 96 * WPL;
+    uint8_t* sbm = (WPL <= 8) ? reinterpret_cast<uint8_t*>(su + 128 * WPL) : nullptr;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -782,6 +810,17 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
                 const int cnt = __popc(u);
                 const int incl = warp_incl_scan(cnt);
                 sr[w] = reg[k];
+                if (sbm) {  // bits of word w -> bytes 32w .. 32w+31 (two 16-byte stores)
+                    uint32_t b[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t nib = (reg[k] >> (4 * q)) & 0xfu;
+                        b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+                    }
+                    uint4* d = reinterpret_cast<uint4*>(sbm + 32 * w);
+                    d[0] = make_uint4(b[0], b[1], b[2], b[3]);
+                    d[1] = make_uint4(b[4], b[5], b[6], b[7]);
+                }
                 su[w] = u;
                 sp[w] = carry + incl - cnt;
                 carry += __shfl_sync(FULL, incl, 31);
@@ -811,7 +850,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
                 nq += __popc(sb);
                 if (nq > QCAP - 32) {
                     __syncwarp();
-                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
+                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
                     __syncwarp();
                     nq = 0;
                 }
@@ -854,7 +893,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
             }
         }
         __syncwarp();
-        for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
+        for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
         __syncwarp();
     }
 }
@@ -1741,7 +1780,7 @@ __device__ __forceinline__ int4 sorted_clique(int i, int j, int z, int S) {
 }
 
 // Per-lane sorted top-KL lists (KL >= K2) merged by K2 warp argmax rounds.
-template <int KL>
+template <int KL, int MODE>
 __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj, int W, int i,
                                              int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
     const int lane = threadIdx.x & 31;
@@ -1757,7 +1796,7 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
             }
         }
     };
-    if (ws.mode == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, insert);
+    if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, insert);
     else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, insert);
     int emitted = 0;
     for (int r = 0; r < K2; ++r) {
@@ -1778,6 +1817,7 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
     return emitted;
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
@@ -1804,11 +1844,11 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
     int emitted = 0;
     if (K2 <= 2) {
-        emitted = pgs_topk_list<2>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<2, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else if (K2 <= 4) {
-        emitted = pgs_topk_list<4>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<4, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else if (K2 <= PGS_KL) {
-        emitted = pgs_topk_list<PGS_KL>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<PGS_KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else {
         unsigned long long thr = ~0ull;
         for (int r = 0; r < K2; ++r) {
@@ -1816,7 +1856,7 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
             auto take = [&](unsigned long long key) {
                 if (key < thr && key > mine) mine = key;
             };
-            if (ws.mode == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
+            if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
             else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, take);
             const unsigned long long best = warp_max_u64(mine);
             if (best == 0ull) break;

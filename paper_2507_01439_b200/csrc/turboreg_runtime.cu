@@ -437,7 +437,9 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_SEL_SCAN, [&] { trk::k_select_scan<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_EMIT, [&] { trk::k_select_emit<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_PGS, [&] {
-        trk::k_pgs<<<dim3((c->prm.k1 + trk::PGS_WARPS - 1) / trk::PGS_WARPS, B), trk::PGS_WARPS * 32, 0, s>>>(ws);
+        const dim3 g((c->prm.k1 + trk::PGS_WARPS - 1) / trk::PGS_WARPS, B);
+        if (c->prm.graph_mode == 1) trk::k_pgs<1><<<g, trk::PGS_WARPS * 32, 0, s>>>(ws);
+        else trk::k_pgs<0><<<g, trk::PGS_WARPS * 32, 0, s>>>(ws);
     }));
     if (c->prm.graph_mode == 1) {  // canonical order + de-duplication of the SC^2-mode clique list (r9)
         int m2 = 1;
@@ -564,6 +566,16 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(unsigned long long) * trk::CANON_CAP)) != cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<1>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<2>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<4>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<5>()) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(trk::k_sc2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<8>()) !=
+            cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<16>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
