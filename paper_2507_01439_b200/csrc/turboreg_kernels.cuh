@@ -969,6 +969,13 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
 // staged in shared memory), enumerates all their upper edges, and pushes them into two queues — j sparse
 // (|L_j ∩ N(i)| against row i's bitmap) and j dense (|L_i ∩ N(j)| against row j's words) — each flushed
 // 32 edges at a time, one edge per lane.
+// 16-byte asynchronous global -> shared copy (LDGSTS), completed by cp.async.wait_all.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+
 template <int WPL>
 constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
 template <int WPL>
@@ -1016,22 +1023,28 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const uint16_t* lists = ws.lists + p * ws.lists_stride;
     const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
     const int32_t* light = ws.light_list + p * ws.row_stride;
-    // stage the group's bitmaps and lists; per-row meta (i, d, lo)
+    // stage the group's bitmaps and lists with asynchronous 16-byte copies (all rows in flight at once);
+    // per-row meta (i, d, lo)
     int my_i = 0, my_d = 0;
-    for (int r = 0; r < nr; ++r) {
-        const int i = light[g0 + r];
-        const uint32_t* ri = bits + (int64_t)i * W;
-#pragma unroll
-        for (int k = 0; k < WPL; ++k) {
-            const int w = lane + 32 * k;
-            bm[r * 32 * WPL + w] = (w < W) ? ri[w] : 0u;
-        }
-        const int di = deg_full[i];
-        if (lane < LIST_MAX / 8)
-            reinterpret_cast<uint4*>(ls + r * LIST_MAX)[lane] =
-                (lane * 8 < di) ? __ldg(reinterpret_cast<const uint4*>(lists + (int64_t)i * LIST_MAX) + lane) : make_uint4(0, 0, 0, 0);
-        if (lane == r) { my_i = i; my_d = di; }
+    if (lane < nr) {
+        my_i = light[g0 + lane];
+        my_d = deg_full[my_i];
+        meta[4 * lane] = my_i;
+        meta[4 * lane + 1] = my_d;
     }
+    __syncwarp();
+    const int W4 = W >> 2;  // 16-byte chunks of a bit row (W is a multiple of 4)
+    for (int idx = lane; idx < nr * W4; idx += 32) {
+        const int r = idx / W4, c = idx - r * W4;
+        cp_async16(bm + r * 32 * WPL + 4 * c, bits + (int64_t)meta[4 * r] * W + 4 * c);
+    }
+    for (int idx = lane; idx < nr * (LIST_MAX / 8); idx += 32) {
+        const int r = idx / (LIST_MAX / 8), c = idx - r * (LIST_MAX / 8);
+        uint16_t* dst = ls + r * LIST_MAX + 8 * c;
+        if (c * 8 < meta[4 * r + 1]) cp_async16(dst, lists + (int64_t)meta[4 * r] * LIST_MAX + 8 * c);
+        else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     int my_lo = 0;
     for (int r = 0; r < nr; ++r) {
