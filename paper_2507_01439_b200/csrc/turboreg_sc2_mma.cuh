@@ -4,14 +4,14 @@
 // C·C over H is a dense binary contraction, so it runs on the 5th-gen tensor cores:
 //   X = C[H, :] as uint8 0/1 (K-major, [h][K]),  D = X · X^T  (exact: int32 accumulate, K <= 32768)
 // with tcgen05.mma kind::i8 (M=128, N=256, K=32 per instruction), operands staged by TMA
-// (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline.
+// (cp.async.bulk.tensor, 128B swizzle) through a 3-stage mbarrier pipeline.
 // Persistent: one CTA per SM walks the (pair, tile) list of the whole batch; the accumulator is double
 // buffered in TMEM (2 × 256 columns) so the epilogue of tile t overlaps the MMAs of tile t+1.
 // The epilogue (4 warps, tcgen05.ld 32x32b, thread = output row a) does not store D: it keeps the entries
 // that are O2 edges — b > a and C[H_a][H_b] = 1, tested on row H_a's upper words — and writes each
 // straight to its slot in the compact edge list, rowptr(H_a) + rank of H_b in U_{H_a} (prefix counts
 // per word from k_expand).  Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread
-// MMA issuer, warps 2..5 = epilogue.  Which rows are heavy only changes speed, never the result.
+// MMA issuer, warps 2..17 = epilogue (4 per TMEM lane quarter).  Which rows are heavy only changes speed.
 // =====================================================================================================
 #pragma once
 #include <cuda.h>
@@ -22,11 +22,12 @@ namespace trk {
 constexpr int MMA_BM = 128;
 constexpr int MMA_BN = 256;
 constexpr int MMA_BK = 128;  // bytes = int8 elements per stage per row
-constexpr int MMA_STAGES = 4;
+constexpr int MMA_STAGES = 3;
 constexpr int MMA_A_BYTES = MMA_BM * MMA_BK;  // 16 KB
 constexpr int MMA_B_BYTES = MMA_BN * MMA_BK;  // 32 KB
 constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
-constexpr int MMA_EPI_WARPS = 8;  // 2 per TMEM lane quarter, each draining half of the 256 columns
+constexpr int MMA_EPI_WARPS = 16;  // 4 per TMEM lane quarter; sub-warp k drains 32-column chunks k, k+4
+constexpr int MMA_EPI_SUB = MMA_EPI_WARPS / 4;
 constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larger batches loop over it)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                                2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 32 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     uint8_t* gen_tptr = smem_raw + (tptr - base);
     int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
     uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [8][32][34] (Ĝ < 65536)
-    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 32 * 34);   // [8][32] edge-list bases
+    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 32 * 34);   // [warps][32] edge-list bases
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -204,10 +205,12 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 umma_commit(tfull0 + 8 * acc);  // accumulator complete
             }
         }
-    } else {  // epilogue: warp w owns TMEM lane quarter w % 4 and column half (w - 2) / 4
+    } else {  // epilogue: warp w owns TMEM lane quarter w % 4 and the chunks c ≡ (w - 2) / 4 mod MMA_EPI_SUB
         const int q = warp & 3;
-        const int ew = warp - 2;           // 0..7
-        const int half = ew >> 2;
+        const int ew = warp - 2;           // 0 .. MMA_EPI_WARPS-1
+        const int sub = ew >> 2;
+        constexpr int NCH = MMA_BN / 32;
+        const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
         const int et = threadIdx.x - 64;  // 0..255
         TileCursor cur;
         int lt = 0;
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-            for (int c = half * (MMA_BN / 64); c < (half + 1) * (MMA_BN / 64); ++c) {
+            for (int c = sub; c < NCH; c += MMA_EPI_SUB) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * MMA_BN + c * 32);
                 asm volatile(
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                       "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (c == (half + 1) * (MMA_BN / 64) - 1) {  // my half drained: hand it back to the MMA issuer
+                if (c == last_c) {  // my chunks drained: hand the accumulator back to the MMA issuer
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
@@ -261,17 +264,20 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 const uint32_t bit = 1u << (jb & 31);
                 const int wb = jb >> 5;
                 const int a0 = rb * MMA_BM + q * 32;
-                uint2 u[32];
 #pragma unroll
-                for (int r = 0; r < 32; ++r) {  // all 32 rows' words in flight at once
-                    const bool ok = s_eb[ew * 32 + r] >= 0 && jb >= 0 && b > a0 + r;
-                    u[r] = ok ? __ldg(up0 + (int64_t)(a0 + r) * W + wb) : make_uint2(0u, 0u);
+                for (int rh = 0; rh < 32; rh += 16) {
+                    uint2 u[16];
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {  // 16 rows' words in flight at once
+                        const bool ok = s_eb[ew * 32 + rh + r] >= 0 && jb >= 0 && b > a0 + rh + r;
+                        u[r] = ok ? __ldg(up0 + (int64_t)(a0 + rh + r) * W + wb) : make_uint2(0u, 0u);
+                    }
+#pragma unroll
+                    for (int r = 0; r < 16; ++r)
+                        if (u[r].x & bit)
+                            edges[s_eb[ew * 32 + rh + r] + (int)u[r].y + __popc(u[r].x & (bit - 1u))] =
+                                ((uint32_t)jb << 16) | vt[(rh + r) * 34 + lane];
                 }
-#pragma unroll
-                for (int r = 0; r < 32; ++r)
-                    if (u[r].x & bit)
-                        edges[s_eb[ew * 32 + r] + (int)u[r].y + __popc(u[r].x & (bit - 1u))] =
-                            ((uint32_t)jb << 16) | vt[r * 34 + lane];
                 __syncwarp();
             }
             named_bar(1, 32 * MMA_EPI_WARPS);  // everyone done with hl[acc] before it is refilled two tiles later
