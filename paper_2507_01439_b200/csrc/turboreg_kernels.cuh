@@ -53,6 +53,7 @@ struct PairState {
     int32_t ncand;               // pivot candidates (weight >= α) collected
     int32_t cand_overflow;       // ncand > PIV_CAP: the ordered count/scan/emit path selects instead
     int32_t pad[1];
+    uint32_t bbox[12];     // order keys of max src xyz, -min src xyz, max dst xyz, -min dst xyz (k_ingest)
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
@@ -184,6 +185,28 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 // ------------------------------------------------------------------------------------------ a1 ingest
+// Monotone map float -> uint32 (larger float, larger key; keys of finite floats are > 0).
+__device__ __forceinline__ uint32_t float_order_key(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_key(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+// κ = τ² + 2^-21 S_max (1 + 2^-20), rounded up, with S_max = diam²(src) + diam²(dst) from the bounding boxes
+// (an upper bound of |Δs|² + |Δd|² for every pair): the S-dependent term of the compat filter's margin Tq
+// bounded once per pair.
+__device__ __forceinline__ float compat_kappa(const PairState* st, float t2) {
+    double smax = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double es = (double)float_from_order_key(st->bbox[c]) + (double)float_from_order_key(st->bbox[3 + c]);
+        const double ed = (double)float_from_order_key(st->bbox[6 + c]) + (double)float_from_order_key(st->bbox[9 + c]);
+        smax += es * es + ed * ed;
+    }
+    return __double2float_ru((double)t2 + ldexp(smax * (1.0 + 0x1p-20), -21));
+}
+
 // Repack the caller's N×3 float32 rows into float4 (x, y, z, 0) and flag non-finite input.
 __global__ void __launch_bounds__(256) k_ingest(WS ws) {
     const int p = blockIdx.y;
@@ -196,6 +219,19 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
         bad = !(isfinite(sx) && isfinite(sy) && isfinite(sz) && isfinite(tx) && isfinite(ty) && isfinite(tz));
         ws.src4[p * ws.pts_stride + k] = make_float4(sx, sy, sz, 0.f);
         ws.dst4[p * ws.pts_stride + k] = make_float4(tx, ty, tz, 0.f);
+    }
+    // bounding boxes (order-preserving float keys, atomicMax; 0 = empty): the compat filter's S bound
+    float v[12];
+    if (k < d.n && !bad) {
+        const float4 a = ws.src4[p * ws.pts_stride + k], b = ws.dst4[p * ws.pts_stride + k];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = -a.x; v[4] = -a.y; v[5] = -a.z;
+        v[6] = b.x; v[7] = b.y; v[8] = b.z; v[9] = -b.x; v[10] = -b.y; v[11] = -b.z;
+    }
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+        const uint32_t key = (k < d.n && !bad) ? float_order_key(v[c]) : 0u;
+        const uint32_t m = __reduce_max_sync(FULL, key);
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(&ws.st[p].bbox[c], m);
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.st[p].nonfinite, 1);
 }
@@ -213,11 +249,13 @@ __global__ void __launch_bounds__(256) k_ingest(WS ws) {
 // S = A + B:
 //   S < τ²  ⇒ edge;   S > τ²  ⇒ ( edge ⇔ q := (A − B)² − τ²(2S − τ²) <= 0 )     (q = (S−τ²)² − 4AB)
 // In float32 (ε = 2^-24, FMAs) the error of q is below 8ε|A−B|S + 15ετ²S and the filter decides only when
-// |q| > 2^-19 (|A−B| + τ² + 2^-21 S) S and S is outside τ²(1 ± 2^-16).  These margins also exceed the
-// oracle's own float32 rounding band around τ (|Δ − τ| <= 2^-22 (a + b)), so wherever the filter decides it
-// provably agrees with the exact tree.  The rest — pairs with |Δ − τ| ≲ 2^-20 (a + b),
-// a few per million — are re-evaluated with the exact tree after the tile loop (lanes that met one redo
-// their 32 tests; the warp re-ballots), so the common path carries no branch.
+// S > τ²(1 + 2^-16) and |q| > Tq = 2^-19 (|A−B| + κ) S, κ = τ² + 2^-21 S_max (1 + 2^-20) >= τ² + 2^-21 S,
+// S_max = diam²(src) + diam²(dst) from the pair's bounding boxes.  These margins also exceed the oracle's
+// own float32 rounding band around τ (|Δ − τ| <= 2^-22 (a + b)), so wherever the filter decides it
+// provably agrees with the exact tree.  The rest — pairs with |Δ − τ| ≲ 2^-20 (a + b), a
+// few per million, and pairs whose points nearly coincide in both clouds (S <= τ²(1 + 2^-16)) — are
+// re-evaluated with the exact tree after the tile loop (lanes that met one redo their tests), so the common
+// path carries no branch.
 __device__ __forceinline__ float f32_dist(float ax, float ay, float az, float bx, float by, float bz) {
     float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
     return __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)));
@@ -328,7 +366,7 @@ __device__ __forceinline__ void compat_tile_base(const WS& ws, int p, int n, int
 template <int NP, int UNR>
 __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, int T, int I, int J,
                                              const float4* s_rs, const float4* s_rd, const float4* s_nr,
-                                             const float4* s_nd, f2_t* s_col) {
+                                             const float4* s_nd, f2_t* s_col, float kap) {
     constexpr int NT = 2 * NP;  // tiles (I, J) .. (I, J+NT-1); lane column k: (J+k)*32 + lane
     const int lane = threadIdx.x & 31;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
@@ -369,12 +407,13 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
     const float t2 = __fmul_rn(tau, tau);
     const float t4 = __fmul_rn(t2, t2);
     const f2_t t2x2 = f2_pack(t2, t2), m2t2x2 = f2_pack(-2.0f * t2, -2.0f * t2), t4x2 = f2_pack(t4, t4);
-    const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
+    const f2_t nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
     const f2_t mone = f2_pack(-1.0f, -1.0f);
-    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
-    const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
-    // per test, in bit 31:  a: S < s_lo (sure edge);  cc: S > s_hi (q decides);  b: |q| < Tq (q unsure);
-    // q: q < 0.  decided x = a | (~b & cc);  edge e = x & (a | q);  sacc keeps bit 31 while all decided.
+    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f);
+    const f2_t s_hi2 = f2_pack(s_hi, s_hi);
+    const f2_t kap2 = f2_pack(kap, kap);
+    // per test, in bit 31:  cc: S > s_hi (q decides);  b: |q| < Tq (q unsure);  q: q < 0.
+    // decided x = ~b & cc;  edge e = x & q;  sacc keeps bit 31 while all decided.
     uint32_t colw[NT], sacc = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < NT; ++k) colw[k] = 0u;
@@ -394,13 +433,13 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
             const f2_t D = f2_fma(B, mone, A);
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
+            const f2_t nTq = f2_mul(f2_add(absD, kap2), f2_mul(S, nc19));
             const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
-            const f2_t a = f2_add(S, ns_lo2), cc = f2_fma(S, mone, s_hi2);
-            const uint32_t a0 = f2_lo(a), a1 = f2_hi(a), k0 = f2_lo(cc), k1 = f2_hi(cc);
-            const uint32_t x0 = a0 | (~f2_lo(b) & k0), x1 = a1 | (~f2_hi(b) & k1);
-            colw[2 * m] = __funnelshift_l(x0 & (a0 | f2_lo(q)), colw[2 * m], 1);
-            colw[2 * m + 1] = __funnelshift_l(x1 & (a1 | f2_hi(q)), colw[2 * m + 1], 1);
+            const f2_t cc = f2_fma(S, mone, s_hi2);
+            const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
+            const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
+            colw[2 * m] = __funnelshift_l(x0 & f2_lo(q), colw[2 * m], 1);
+            colw[2 * m + 1] = __funnelshift_l(x1 & f2_hi(q), colw[2 * m + 1], 1);
             sacc &= x0 & x1;
         }
     }
@@ -451,7 +490,8 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
 template <int NC, int UNR>
 __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int W, int T, int I, int J,
                                                 const float4* s_rs, const float4* s_rd, const float4* s_pxy,
-                                                const float2* s_pz, const float4* s_qxy, const float2* s_qz) {
+                                                const float2* s_pz, const float4* s_qxy, const float2* s_qz,
+                                                float kap) {
     const int lane = threadIdx.x & 31;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
     const float4* d4 = ws.dst4 + p * ws.pts_stride;
@@ -471,10 +511,11 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
     const float t2 = __fmul_rn(tau, tau);
     const float t4 = __fmul_rn(t2, t2);
     const f2_t t2x2 = f2_pack(t2, t2), m2t2x2 = f2_pack(-2.0f * t2, -2.0f * t2), t4x2 = f2_pack(t4, t4);
-    const f2_t c21 = f2_pack(0x1p-21f, 0x1p-21f), nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
+    const f2_t nc19 = f2_pack(-0x1p-19f, -0x1p-19f);
     const f2_t mone = f2_pack(-1.0f, -1.0f);
-    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f), s_lo = __fmul_rn(t2, 1.0f - 0x1p-16f);
-    const f2_t s_hi2 = f2_pack(s_hi, s_hi), ns_lo2 = f2_pack(-s_lo, -s_lo);
+    const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f);
+    const f2_t s_hi2 = f2_pack(s_hi, s_hi);
+    const f2_t kap2 = f2_pack(kap, kap);
     uint32_t colw[NC], sacc = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < NC; ++k) colw[k] = 0u;
@@ -498,13 +539,13 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
             const f2_t D = f2_fma(B, mone, A);
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t nTq = f2_mul(f2_fma(S, c21, f2_add(absD, t2x2)), f2_mul(S, nc19));
+            const f2_t nTq = f2_mul(f2_add(absD, kap2), f2_mul(S, nc19));
             const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
-            const f2_t a = f2_add(S, ns_lo2), cc = f2_fma(S, mone, s_hi2);
-            const uint32_t a0 = f2_lo(a), a1 = f2_hi(a), k0 = f2_lo(cc), k1 = f2_hi(cc);
-            const uint32_t x0 = a0 | (~f2_lo(b) & k0), x1 = a1 | (~f2_hi(b) & k1);
-            colw[k] = __funnelshift_l(x0 & (a0 | f2_lo(q)), colw[k], 1);
-            colw[k] = __funnelshift_l(x1 & (a1 | f2_hi(q)), colw[k], 1);
+            const f2_t cc = f2_fma(S, mone, s_hi2);
+            const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
+            const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
+            colw[k] = __funnelshift_l(x0 & f2_lo(q), colw[k], 1);
+            colw[k] = __funnelshift_l(x1 & f2_hi(q), colw[k], 1);
             sacc &= x0 & x1;
         }
     }
@@ -589,6 +630,8 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
         // block-rows I0 = b and I1 = T-1-b (T+1 tiles together, so every block has the same work) are
         // staged at once and their tile pairs dealt to the 8 warps as one list: no barrier between them
         const int I0 = b, I1 = T - 1 - b;
+        __shared__ float s_kap;
+        if (threadIdx.x == 0) s_kap = compat_kappa(ws.st + p, __fmul_rn(ws.tau, ws.tau));
         if (threadIdx.x < 64) {
             const int t = threadIdx.x, I = t < 32 ? I0 : I1, r0 = I * 32 + (t & 31);
             const float4 a = r0 < n ? s4[r0] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -606,6 +649,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
             reinterpret_cast<float*>(s_qz[h])[u] = -q.z;
         }
         __syncthreads();
+        const float kap = s_kap;
         if constexpr (NP < 0) {
             constexpr int NC = -NP;
             const int P0 = (T - I0 + NC - 1) / NC, P1 = (I1 != I0) ? (T - I1 + NC - 1) / NC : 0;
@@ -613,7 +657,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
                 const bool second = t >= P0;
                 const int I = second ? I1 : I0, J = I + NC * (second ? t - P0 : t), o = second ? 32 : 0, h = second;
                 compat_tiles_rp<NC, UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_pxy[h], s_pz[h], s_qxy[h],
-                                         s_qz[h]);
+                                         s_qz[h], kap);
             }
             return;
         }
@@ -622,7 +666,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
         for (int t = warp + 8 * sp; t < P0 + P1; t += 8 * split) {
             const bool second = t >= P0;
             const int I = second ? I1 : I0, J = I + NT * (second ? t - P0 : t), o = second ? 32 : 0;
-            compat_tiles<(NP > 0 ? NP : 1), UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_nr + o, s_nd + o, s_col[warp]);
+            compat_tiles<(NP > 0 ? NP : 1), UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_nr + o, s_nd + o, s_col[warp], kap);
         }
     }
 }
