@@ -38,6 +38,7 @@ class Params(ctypes.Structure):
         ("k2", ctypes.c_int32),
         ("inlier_threshold", ctypes.c_float),
         ("graph_mode", ctypes.c_int32),
+        ("rank_metric", ctypes.c_int32),
     ]
 
 
@@ -58,6 +59,8 @@ class Result(ctypes.Structure):
         ("neighbor_checks", ctypes.c_int64),
         ("best_count_f64", ctypes.c_int32),
         ("near_corr", ctypes.c_int32),
+        ("mae", ctypes.c_double),
+        ("mse", ctypes.c_double),
     ]
 
 
@@ -88,7 +91,8 @@ def lib():
         _lib.oracle_count_inliers.restype = i32
         _lib.oracle_brute_triangles.argtypes = [P, i32, P, i64]
         _lib.oracle_brute_triangles.restype = i64
-        _lib.oracle_estimate.argtypes = [P, P, i32, ctypes.POINTER(Params), ctypes.POINTER(Result), P, P, P, P, P]
+        _lib.oracle_estimate.argtypes = [P, P, i32, ctypes.POINTER(Params), ctypes.POINTER(Result), P, P, P, P, P, P]
+        _lib.oracle_hypothesis_errors.argtypes = [P, P, i32, P, P, P, P]
         _lib.oracle_estimate.restype = i32
     return _lib
 
@@ -189,20 +193,23 @@ def brute_triangles(C):
     return out[:m].copy()
 
 
-def estimate(src, dst, tau, k1, k2, inlier_threshold, graph_mode=0, trace=False):
-    """Full oracle pipeline (steps 1-9).  Returns dict with the result and, if trace, the intermediates."""
+def estimate(src, dst, tau, k1, k2, inlier_threshold, graph_mode=0, trace=False, rank_metric=0):
+    """Full oracle pipeline (steps 1-9).  Returns dict with the result and, if trace, the intermediates.
+    rank_metric: 0 = inlier number (Eq. 9), 1 = MAE, 2 = MSE (App. F.1, reading r20)."""
     src, dst = _f32(src), _f32(dst)
     n = src.shape[0]
-    prm = Params(float(tau), int(k1), int(k2), float(inlier_threshold), int(graph_mode))
+    prm = Params(float(tau), int(k1), int(k2), float(inlier_threshold), int(graph_mode), int(rank_metric))
     res = Result()
-    C = G = piv = cl = hyp = None
+    C = G = piv = cl = hyp = err = None
     if trace:
         C = np.zeros((n, n), np.uint8)
         G = np.zeros((n, n), np.int32)
         piv = np.zeros((max(k1, 1), 3), np.int32)
         cl = np.zeros((max(k1 * k2, 1), 4), np.int32)
         hyp = np.zeros((max(k1 * k2, 1), 16), np.float32)
-    lib().oracle_estimate(_p(src), _p(dst), n, ctypes.byref(prm), ctypes.byref(res), _p(C), _p(G), _p(piv), _p(cl), _p(hyp))
+        err = np.zeros((max(k1 * k2, 1), 2), np.float64)
+    lib().oracle_estimate(_p(src), _p(dst), n, ctypes.byref(prm), ctypes.byref(res), _p(C), _p(G), _p(piv), _p(cl), _p(hyp),
+                          _p(err))
     out = {
         "status": res.status,
         "R": np.array(res.R, np.float32).reshape(3, 3),
@@ -219,6 +226,8 @@ def estimate(src, dst, tau, k1, k2, inlier_threshold, graph_mode=0, trace=False)
         "neighbor_checks": res.neighbor_checks,
         "best_count_f64": res.best_count_f64,
         "near_corr": res.near_corr,
+        "mae": res.mae,
+        "mse": res.mse,
     }
     if trace:
         nc = res.num_cliques
@@ -232,5 +241,16 @@ def estimate(src, dst, tau, k1, k2, inlier_threshold, graph_mode=0, trace=False)
             hyp_t=h[:, 9:12].copy(),
             hyp_count=h[:, 12].copy().view(np.int32),
             hyp_degenerate=h[:, 13].copy().view(np.int32),
+            hyp_mae=err[:nc, 0].copy(),
+            hyp_mse=err[:nc, 1].copy(),
         )
     return out
+
+
+def hypothesis_errors(src, dst, R, t):
+    """(MAE, MSE) of a float32 hypothesis over all correspondences (reading r20)."""
+    src, dst = _f32(src), _f32(dst)
+    mae, mse = ctypes.c_double(), ctypes.c_double()
+    lib().oracle_hypothesis_errors(_p(src), _p(dst), src.shape[0], _p(_f32(np.asarray(R).reshape(9))),
+                                   _p(_f32(np.asarray(t).reshape(3))), ctypes.byref(mae), ctypes.byref(mse))
+    return mae.value, mse.value

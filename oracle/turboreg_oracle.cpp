@@ -21,6 +21,7 @@
 //   6 canonical clique order (+ dedup in SC^2 mode)                    oracle_canonical
 //   7 Kabsch per clique, one-sided Jacobi SVD in double        oracle_kabsch
 //   8 inlier number g(T) in fixed-order float32            oracle_count_inliers
+//   8' MAE / MSE of a hypothesis (App. F.1, reading r20)     oracle_hypothesis_errors
 //   9 argmax T* (Eq. 9)                                     oracle_estimate
 // plus a brute-force 3-clique enumerator used only as a test pin (App. B/C).
 //
@@ -41,6 +42,7 @@ struct oracle_params {
     int32_t k2;              // K2, TurboCliques per pivot (Eq. 7)
     float inlier_threshold;  // residual bound of g(·) (reading r12)
     int32_t graph_mode;      // 0 = O2Graph (Def. 2), 1 = undirected SC^2 graph (Table 5 row 10)
+    int32_t rank_metric;     // 0 = inlier number (Eq. 9), 1 = MAE, 2 = MSE (App. F.1, reading r20)
 };
 
 struct oracle_result {
@@ -59,6 +61,7 @@ struct oracle_result {
     int64_t neighbor_checks;    // Alg. 1 L8 evaluations = Σ_pivots (N-2)
     int32_t best_count_f64;     // shadow: inliers of the winner's float64 (R,t) in float64
     int32_t near_corr;          // winner: correspondences within the near band of the inlier threshold
+    double mae, mse;            // winner's mean absolute / squared residual (reading r20)
 };
 
 // ------------------------------------------------------------------------------------------ step 1
@@ -346,6 +349,28 @@ int32_t oracle_count_inliers(const float* src, const float* dst, int32_t n, cons
 }
 
 // float64 shadow count and near-band count (diagnostics only; reading r13).
+// App. F.1 ranks the K1K2 hypotheses by inlier number, mean absolute error (MAE) and mean
+// squared error (MSE) without writing the errors out; SPEC ranks MAE/MSE ascending.  Reading
+// r20: over all N correspondences, with the residual of reading r13 (float32 FMA tree, s = |r|^2 in
+// float32): MAE = (1/N) Σ_k sqrtf(s_k), MSE = (1/N) Σ_k s_k, the sums in float64 in index order.
+void oracle_hypothesis_errors(const float* src, const float* dst, int32_t n, const float* R, const float* t,
+                              double* mae, double* mse) {
+    double sa = 0.0, ss = 0.0;
+    for (int32_t k = 0; k < n; ++k) {
+        float x = src[3 * k], y = src[3 * k + 1], z = src[3 * k + 2];
+        float e[3];
+        for (int r = 0; r < 3; ++r) {
+            float p = std::fma(R[3 * r + 2], z, std::fma(R[3 * r + 1], y, std::fma(R[3 * r + 0], x, t[r])));
+            e[r] = p - dst[3 * k + r];
+        }
+        float s2 = std::fma(e[2], e[2], std::fma(e[1], e[1], e[0] * e[0]));
+        sa += (double)std::sqrt(s2);
+        ss += (double)s2;
+    }
+    *mae = n > 0 ? sa / n : 0.0;
+    *mse = n > 0 ? ss / n : 0.0;
+}
+
 static void shadow_count(const float* src, const float* dst, int32_t n, const double* R, const double* t, float thr,
                          int32_t* cnt64, int32_t* near) {
     int32_t c = 0, nb = 0;
@@ -386,7 +411,8 @@ int64_t oracle_brute_triangles(const uint8_t* C, int32_t n, int32_t* out, int64_
 // (canonical order), hyp_out [k1*k2*16] floats: R[9], t[3], count (as float bits of int32 via memcpy),
 // degenerate flag, S, pad — in canonical clique order.
 int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const oracle_params* prm, oracle_result* res,
-                        uint8_t* C_out, int32_t* G_out, int32_t* piv_out, int32_t* cliques_out, float* hyp_out) {
+                        uint8_t* C_out, int32_t* G_out, int32_t* piv_out, int32_t* cliques_out, float* hyp_out,
+                        double* err_out) {
     std::memset(res, 0, sizeof(*res));
     if (n < 3) { res->status = 2; return 2; }
     std::vector<uint8_t> C((size_t)n * n);
@@ -413,6 +439,7 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
     if (cliques_out) std::memcpy(cliques_out, cl.data(), (size_t)4 * nc * sizeof(int32_t));
 
     int32_t best = -1, best_cnt = -1, best_s = -1;
+    double best_err = 0.0;
     int32_t nvalid = 0;
     std::vector<double> bestR64(9), bestt64(3);
     for (int32_t c = 0; c < nc; ++c) {
@@ -428,6 +455,7 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
         if (!degen && oracle_kabsch(P, Q, 3, R64, t64) != 0) degen = true;
         if (degen) {
             if (h) { int32_t one = 1; std::memcpy(&h[13], &one, 4); }
+            if (err_out) err_out[2 * c] = err_out[2 * c + 1] = std::nan("");
             continue;
         }
         ++nvalid;
@@ -435,6 +463,9 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
         for (int k = 0; k < 9; ++k) R32[k] = (float)R64[k];
         for (int k = 0; k < 3; ++k) t32[k] = (float)t64[k];
         int32_t cnt = oracle_count_inliers(src, dst, n, R32, t32, prm->inlier_threshold);
+        double mae = 0.0, mse = 0.0;
+        if (prm->rank_metric != 0 || err_out) oracle_hypothesis_errors(src, dst, n, R32, t32, &mae, &mse);
+        if (err_out) { err_out[2 * c] = mae; err_out[2 * c + 1] = mse; }
         if (h) {
             std::memcpy(h, R32, sizeof(R32));
             std::memcpy(h + 9, t32, sizeof(t32));
@@ -443,8 +474,14 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
         }
         // Eq. 9 argmax with reading r14: (count desc, S desc, (i,j,z) asc).  The list is already in
         // (S desc, ijz asc) order, so the first strictly larger count wins.
-        if (cnt > best_cnt || (cnt == best_cnt && s > best_s)) {
-            best = c; best_cnt = cnt; best_s = s;
+        // reading r20: with rank_metric MAE / MSE the first strictly smaller error wins (ties keep the list's
+        // (S desc, ijz asc) order)
+        const double err = prm->rank_metric == 1 ? mae : mse;
+        const bool better = prm->rank_metric == 0 ? (cnt > best_cnt || (cnt == best_cnt && s > best_s))
+                                                  : (best < 0 || err < best_err);
+        if (better) {
+            best = c; best_cnt = cnt; best_s = s; best_err = err;
+            res->mae = mae; res->mse = mse;
             std::memcpy(res->R, R32, sizeof(R32));
             std::memcpy(res->t, t32, sizeof(t32));
             std::memcpy(bestR64.data(), R64, sizeof(R64));
