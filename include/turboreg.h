@@ -51,6 +51,11 @@ typedef enum {
 /* turboreg_params.flags */
 #define TURBOREG_F_STAGE_TIMING 0x1u  /* fill turboreg_result.stage_ms (CUDA events; adds ~12 events)  */
 #define TURBOREG_F_KERNEL_TIMING 0x2u /* accumulate per-kernel CUDA-event times, see turboreg_profile_* */
+#define TURBOREG_F_HYP_ERRORS 0x4u    /* also accumulate MAE / MSE of every hypothesis over all N
+                                         correspondences (App. F.1, reading r20; TURBOREG_I_ERRORS)      */
+#define TURBOREG_F_RANK_MAE 0x8u      /* select T* by minimum MAE instead of maximum inlier number
+                                         (ties: S desc, then (i,j,z) asc); implies HYP_ERRORS           */
+#define TURBOREG_F_RANK_MSE 0x10u     /* likewise by minimum MSE; not together with RANK_MAE             */
 
 typedef struct {
     float tau;              /* τ of Eq. 1, metres, > 0: the stringent TurboClique threshold (Def. 1); drives
@@ -125,6 +130,8 @@ const char* turboreg_status_string(turboreg_status s);
  *                        in canonical order, de-duplicated, compacted; empty slots are (-1,-1,-1,0)
  *   TURBOREG_I_HYPS      float  [K1*K2][16]: R[9], t[3], count (int32 bits), flag (int32 bits:
  *                        0 valid, 1 degenerate, 2 empty slot), S (int32 bits), 0
+ *   TURBOREG_I_ERRORS    double [K1*K2][2] (MAE, MSE) per slot, NaN for empty / degenerate slots (needs
+ *                        TURBOREG_F_HYP_ERRORS or a RANK flag, else TURBOREG_ERR_INVALID_ARGUMENT)
  *   TURBOREG_I_STATE     int64  [16] per-pair scalars: n, W, edges, positive edges, alpha, c_gt, need,
  *                        num_pivots, nonfinite, ...                                                   */
 #define TURBOREG_I_BITS 1
@@ -134,6 +141,7 @@ const char* turboreg_status_string(turboreg_status s);
 #define TURBOREG_I_CLIQUES 5
 #define TURBOREG_I_HYPS 6
 #define TURBOREG_I_STATE 7
+#define TURBOREG_I_ERRORS 8
 turboreg_status turboreg_get_intermediates(turboreg_ctx* ctx, int32_t pair, int32_t what, void* dst, size_t bytes,
                                            size_t* needed);
 

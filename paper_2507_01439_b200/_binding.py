@@ -34,8 +34,11 @@ class Status(enum.IntEnum):
 
 F_STAGE_TIMING = 0x1
 F_KERNEL_TIMING = 0x2
+F_HYP_ERRORS = 0x4
+F_RANK_MAE = 0x8
+F_RANK_MSE = 0x10
 
-I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE = 1, 2, 3, 4, 5, 6, 7
+I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 class Params(ctypes.Structure):
@@ -149,9 +152,11 @@ class TurboReg:
     """
 
     def __init__(self, tau, k1=1000, k2=2, inlier_threshold=0.1, *, tau_base=0.0, graph_mode=0,
-                 max_n=5000, max_batch=1, device=0, stage_timing=False, kernel_timing=False):
+                 max_n=5000, max_batch=1, device=0, stage_timing=False, kernel_timing=False, hyp_errors=False,
+                 rank_metric="in"):
         self._lib = library()
         flags = (F_STAGE_TIMING if stage_timing else 0) | (F_KERNEL_TIMING if kernel_timing else 0)
+        flags |= (F_HYP_ERRORS if hyp_errors else 0) | {"in": 0, "mae": F_RANK_MAE, "mse": F_RANK_MSE}[rank_metric]
         self.params = Params(float(tau), float(tau_base), int(k1), int(k2), float(inlier_threshold),
                              int(graph_mode), flags)
         h = ctypes.c_void_p()
@@ -249,6 +254,8 @@ class TurboReg:
             return buf.view(np.int32).reshape(-1, 4)
         if what == I_HYPS:
             return buf.view(np.float32).reshape(-1, 16)
+        if what == I_ERRORS:
+            return buf.view(np.float64).reshape(-1, 2)
         if what == I_STATE:
             s = buf.view(np.int64)
             keys = ["n", "W", "edges", "epos", "alpha", "c_gt", "need", "npiv", "nonfinite", "b1", "above",

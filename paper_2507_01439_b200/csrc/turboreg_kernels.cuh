@@ -109,6 +109,8 @@ struct WS {
     int32_t k1, k2, mode;
     int32_t pair_base;    // index of pair 0 of this view in the batch (TMA coordinates address the whole batch)
     uint16_t* uprefix;    // SC^2 mode only: [n][W] exclusive prefix popcount of U_i per word (stride bits_stride)
+    double2* herr;        // [K1*K2] per hypothesis (Σ sqrtf(s), Σ s) over the pair's correspondences (r20)
+    int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
 };
 
 // The workspace restricted to pairs [p0, p0 + count): every per-pair array advanced by p0 strides.
@@ -145,6 +147,7 @@ inline WS ws_view(const WS& w, int p0, size_t result_bytes) {
     v.heavy_D = w.heavy_D + p0 * w.heavy_D_stride;
     v.pair_base = w.pair_base + p0;
     if (w.uprefix) v.uprefix = w.uprefix + p0 * w.bits_stride;
+    v.herr = w.herr + p0 * w.cl_stride;
     return v;
 }
 
@@ -2122,6 +2125,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // hypothesis; the finer grid leaves no half-empty last wave), streamed through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
+template <bool ERR>
 __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
     __shared__ __align__(16) float4 s_src[2][SCORE_PC];
     __shared__ __align__(16) float4 s_dst[2][SCORE_PC];
@@ -2190,6 +2194,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
     for (int k = 0; k < 3; ++k) tp[k] = f2_pack(R0[9 + k], R1[9 + k]);
     const f2_t mone = f2_pack(-1.0f, -1.0f);
     int cnt0 = 0, cnt1 = 0;
+    double ea0 = 0.0, ea1 = 0.0, es0 = 0.0, es1 = 0.0;  // ERR: Σ sqrtf(s), Σ s per hypothesis (r20)
     for (int c = 0; c < nchunks; ++c) {
         const int st = c & 1;
         if (threadIdx.x == 0 && c + 1 < nchunks) issue(c + 1);  // buffer st^1 was released by the barrier below
@@ -2222,11 +2227,23 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
             // s >= 0, so integer order of the bit patterns is float order
             cnt0 += f2_lo(sq) <= thr2b;
             cnt1 += f2_hi(sq) <= thr2b;
+            if constexpr (ERR) {
+                const float s0 = __uint_as_float(f2_lo(sq)), s1 = __uint_as_float(f2_hi(sq));
+                ea0 += (double)__fsqrt_rn(s0);
+                ea1 += (double)__fsqrt_rn(s1);
+                es0 += (double)s0;
+                es1 += (double)s1;
+            }
         }
         __syncthreads();  // every thread is done with buffer st before it is refilled
     }
     if (v0 && cnt0) atomicAdd(reinterpret_cast<int*>(hp0 + 12), cnt0);
     if (v1 && cnt1) atomicAdd(reinterpret_cast<int*>(hp1 + 12), cnt1);
+    if constexpr (ERR) {
+        double2* he = ws.herr + q * ws.cl_stride;
+        if (v0) { atomicAdd(&he[h0].x, ea0); atomicAdd(&he[h0].y, es0); }
+        if (v1) { atomicAdd(&he[h1].x, ea1); atomicAdd(&he[h1].y, es1); }
+    }
 }
 
 // ------------------------------------------------------------------------------------------ a8 argmax
@@ -2255,6 +2272,17 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     const int K = ws.k1 * ws.k2;
     const float* hyp = ws.hyp + q * ws.cl_stride * 16;
     const int4* cl = ws.cliq + q * ws.cl_stride;
+    // key of a valid hypothesis, maximised: inlier mode (count << 17 | S); error modes (reading r20) the
+    // complement of the error's bit pattern (non-negative doubles order like their bits) — S and ijz break
+    // ties below, as in the oracle's scan of the canonical list
+    const int rank = ws.err_mode >> 1;
+    const double2* he = ws.herr + q * ws.cl_stride;
+    auto key_of = [&](int s, const float* h) -> unsigned long long {
+        if (rank == 0)
+            return ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+        const double e = rank == 1 ? he[s].x : he[s].y;
+        return ~(unsigned long long)__double_as_longlong(e);
+    };
     unsigned long long best1 = 0ull;
     int ncl = 0, nev = 0;
     if (d.n > 0) {
@@ -2264,8 +2292,7 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
             if (flag != 2) ++ncl;
             if (flag == 0) {
                 ++nev;
-                const unsigned long long key =
-                    ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+                const unsigned long long key = key_of(s, h);
                 best1 = key > best1 ? key : best1;
             }
         }
@@ -2286,14 +2313,34 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     ncl = s_cnt[0][0];
     nev = s_cnt[1][0];
     __syncthreads();
+    int bestS = -1;  // error modes: the largest S among the minimum-error hypotheses
+    if (rank != 0) {
+        int ms = -1;
+        if (d.n > 0 && nev > 0)
+            for (int s = t; s < K; s += blockDim.x) {
+                const float* h = hyp + (int64_t)s * 16;
+                if (__float_as_int(h[13]) == 0 && key_of(s, h) == best1) ms = max(ms, __float_as_int(h[14]));
+            }
+        ms = (int)__reduce_max_sync(FULL, (unsigned)(ms + 1)) - 1;
+        if (lane == 0) s_cnt[0][warp] = ms;
+        __syncthreads();
+        if (t == 0) {
+            int m = -1;
+            for (int w = 0; w < 8; ++w) m = max(m, s_cnt[0][w]);
+            s_cnt[0][0] = m;
+        }
+        __syncthreads();
+        bestS = s_cnt[0][0];
+        __syncthreads();
+    }
     unsigned long long bestt = ~0ull;
     if (d.n > 0 && nev > 0) {
         for (int s = t; s < K; s += blockDim.x) {
             const float* h = hyp + (int64_t)s * 16;
             if (__float_as_int(h[13]) != 0) continue;
-            const unsigned long long key =
-                ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+            const unsigned long long key = key_of(s, h);
             if (key != best1) continue;
+            if (rank != 0 && __float_as_int(h[14]) != bestS) continue;
             const int4 c = cl[s];
             const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
             if (tk < bestt) bestt = tk;
@@ -2314,6 +2361,7 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     if (bestt != ~0ull) {  // the slot holding the winning triple (duplicates carry identical values)
         for (int s = t; s < K; s += blockDim.x) {
             if (__float_as_int(hyp[(int64_t)s * 16 + 13]) != 0) continue;
+            if (key_of(s, hyp + (int64_t)s * 16) != best1) continue;
             const int4 c = cl[s];
             const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
             if (tk == bestt) atomicMin(&s_slot, s);

@@ -139,7 +139,10 @@ bool params_valid(const turboreg_params* p) {
     if (!(p->inlier_threshold > 0.f) || !std::isfinite(p->inlier_threshold)) return false;
     if (p->graph_mode != 0 && p->graph_mode != 1) return false;
     if (p->graph_mode == 1 && (int64_t)p->k1 * p->k2 > trk::CANON_CAP) return false;  // canonical sort in smem
-    if (p->flags & ~(TURBOREG_F_STAGE_TIMING | TURBOREG_F_KERNEL_TIMING)) return false;
+    if (p->flags & ~(TURBOREG_F_STAGE_TIMING | TURBOREG_F_KERNEL_TIMING | TURBOREG_F_HYP_ERRORS | TURBOREG_F_RANK_MAE |
+                     TURBOREG_F_RANK_MSE))
+        return false;
+    if ((p->flags & TURBOREG_F_RANK_MAE) && (p->flags & TURBOREG_F_RANK_MSE)) return false;
     return true;
 }
 
@@ -171,7 +174,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
     const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -197,6 +200,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(int32_t) * (size_t)(cap * B), &p_hl},
         {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
         {sizeof(uint32_t) * (size_t)(W * B), &p_lm},
+        {sizeof(double2) * (size_t)(KC * B), &p_herr},
         {sizeof(uint2) * (size_t)(cap * W * B), &p_up},
         {sizeof(int) * 16, &p_ctr},
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
@@ -250,6 +254,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.light_mask = static_cast<uint32_t*>(p_lm);
     w.heavy_UP = static_cast<uint2*>(p_up);
     w.uprefix = static_cast<uint16_t*>(p_upre);
+    w.herr = static_cast<double2*>(p_herr);
     w.heavy_UP_stride = cap * W;
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
@@ -291,6 +296,10 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.k1 = c->prm.k1;
     c->ws.k2 = c->prm.k2;
     c->ws.mode = c->prm.graph_mode;
+    {
+        const int rank = (c->prm.flags & TURBOREG_F_RANK_MAE) ? 1 : (c->prm.flags & TURBOREG_F_RANK_MSE) ? 2 : 0;
+        c->ws.err_mode = ((rank || (c->prm.flags & TURBOREG_F_HYP_ERRORS)) ? 1 : 0) | (rank << 1);
+    }
 }
 
 bool is_device_ptr(const void* p) {
@@ -448,12 +457,14 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     if (mode == RUN_FULL) {
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
+        if (ws.err_mode & 1) CK(cudaMemsetAsync(ws.herr, 0, sizeof(double2) * KC * batch, s));
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
             const int hb = (int)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT);
             const int segs = std::max(2, std::min(16, (7 * c->num_sms + hb * batch - 1) / (hb * batch)));
             const dim3 g((unsigned)(hb * segs), B);
-            trk::k_score<<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+            if (ws.err_mode & 1) trk::k_score<true><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+            else trk::k_score<false><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
         }));
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
     }
@@ -862,6 +873,26 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             if (!dst) return TURBOREG_OK;
             if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
             CK(cudaMemcpy(dst, w.hyp + pair * w.cl_stride * 16, need, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
+        case TURBOREG_I_ERRORS: {  // (MAE, MSE) per slot; NaN for empty / degenerate slots (reading r20)
+            need = sizeof(double) * 2 * (size_t)w.cl_stride;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            if (!(w.err_mode & 1)) return TURBOREG_ERR_INVALID_ARGUMENT;
+            std::vector<double2> e((size_t)w.cl_stride);
+            std::vector<float> h((size_t)w.cl_stride * 16);
+            CK(cudaMemcpy(e.data(), w.herr + pair * w.cl_stride, sizeof(double2) * e.size(), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h.data(), w.hyp + pair * w.cl_stride * 16, sizeof(float) * h.size(), cudaMemcpyDeviceToHost));
+            const double nn = (double)c->last_n[pair];
+            double* out = static_cast<double*>(dst);
+            for (size_t s = 0; s < e.size(); ++s) {
+                int32_t flag;
+                std::memcpy(&flag, &h[16 * s + 13], 4);
+                out[2 * s] = flag == 0 ? e[s].x / nn : std::nan("");
+                out[2 * s + 1] = flag == 0 ? e[s].y / nn : std::nan("");
+            }
             return TURBOREG_OK;
         }
         case TURBOREG_I_STATE: {

@@ -19,7 +19,7 @@ import synth  # noqa: E402
 from paper_2507_01439_b200 import RESULT_DTYPE, TurboReg  # noqa: E402
 
 
-def run(cfg, pairs, opts, reps=3, n=None, graph_mode=0):
+def run(cfg, pairs, opts, reps=3, n=None, graph_mode=0, rank_metric="in", hyp_errors=False):
     n = n or cfg.n
     src = np.concatenate([synth.workload_instance(cfg, pair=p, n=n)["src"] for p in range(pairs)])
     dst = np.concatenate([synth.workload_instance(cfg, pair=p, n=n)["dst"] for p in range(pairs)])
@@ -30,7 +30,7 @@ def run(cfg, pairs, opts, reps=3, n=None, graph_mode=0):
     sd, dd = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
     out = torch.zeros(pairs * RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
     tr = TurboReg(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n, max_batch=pairs, kernel_timing=True,
-                  graph_mode=graph_mode)
+                  graph_mode=graph_mode, rank_metric=rank_metric, hyp_errors=hyp_errors)
     for k, v in opts.items():
         tr.set_option(k, v)
     for _ in range(2):
@@ -56,6 +56,8 @@ def main():
     ap.add_argument("--opt", action="append", default=[])
     ap.add_argument("--variants", default="")
     ap.add_argument("--graph-mode", type=int, default=0)
+    ap.add_argument("--rank-metric", default="in", choices=["in", "mae", "mse"])
+    ap.add_argument("--hyp-errors", action="store_true")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.cfg]
     variants = [dict(kv.split("=") for kv in args.opt)]
@@ -64,7 +66,9 @@ def main():
     for v in variants:
         opts = {k: int(x) for k, x in v.items()}
         print(json.dumps({"cfg": args.cfg, "opts": opts, "graph_mode": args.graph_mode,
-                          "us_per_pair": run(cfg, args.pairs, opts, n=args.n, graph_mode=args.graph_mode)}))
+                          "rank_metric": args.rank_metric, "hyp_errors": args.hyp_errors,
+                          "us_per_pair": run(cfg, args.pairs, opts, n=args.n, graph_mode=args.graph_mode,
+                                             rank_metric=args.rank_metric, hyp_errors=args.hyp_errors)}))
 
 
 if __name__ == "__main__":
