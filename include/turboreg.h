@@ -169,6 +169,7 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "pipeline_host_inputs" 1 = a call with host inputs and >= 16 pairs copies them in 4 sub-batches, each
  *                      copy overlapping the previous sub-batch's compatibility pass (default); 0 = one copy
  *                      before one launch sequence
+ *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1
  *   "cuda_graph"       1 = replay the launch sequence from a CUDA graph captured per (batch, max n) shape
  *                      (default; calls with stage/kernel timing always launch directly); 0 = launch directly
  *   "compat_variant"   compat-graph tiling: 0 = row pairs in f32x2 lanes x 2 column tiles per warp

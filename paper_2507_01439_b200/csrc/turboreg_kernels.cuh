@@ -2114,19 +2114,21 @@ __global__ void __launch_bounds__(128) k_kabsch(WS ws) {
 // completing on an mbarrier; every thread then streams the chunk (broadcast LDS.128) through its own
 // (R, t) in the oracle's fixed fp32 FMA tree (reading r13) and adds its count atomically.
 constexpr int SCORE_THREADS = 128;               // each thread scores two hypotheses
-constexpr int SCORE_HT = 2 * SCORE_THREADS;      // hypotheses per block
+constexpr int SCORE_HT = 2 * SCORE_THREADS;      // hypotheses per block (one packed pair per thread)
 constexpr int SCORE_PC = 512;                    // correspondences per pipeline stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// g(T) = inlier number.  A block owns 256 hypotheses of one pair (two per thread, packed as
-// f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and one of
+// g(T) = inlier number.  A block owns 256·NP hypotheses of one pair (2·NP per thread, packed
+// in pairs as f32x2 lanes: one fma.rn.f32x2 evaluates the same correspondence under two transforms) and one of
 // `segs` contiguous segments of the N correspondences (partial counts meet in one atomicAdd per
 // hypothesis; the finer grid leaves no half-empty last wave), streamed through a 2-stage shared-memory ring filled by bulk async copies (cp.async.bulk, the TMA
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
-template <bool ERR>
-__global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
+template <bool ERR, int NP>
+__global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS ws, int segs) {
+    // NP packed hypothesis pairs per thread: hypotheses h = base + threadIdx.x + SCORE_THREADS * u, u < 2 NP
+    constexpr int NH = 2 * NP;
     __shared__ __align__(16) float4 s_src[2][SCORE_PC];
     __shared__ __align__(16) float4 s_dst[2][SCORE_PC];
     __shared__ __align__(8) unsigned long long s_bar[2];
@@ -2136,30 +2138,28 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
     if (n == 0) return;
     const int K = ws.k1 * ws.k2;
     const int seg = blockIdx.x % segs;
-    const int h0 = (blockIdx.x / segs) * SCORE_HT + threadIdx.x, h1 = h0 + SCORE_THREADS;
+    const int hbase = (blockIdx.x / segs) * (SCORE_THREADS * NH) + threadIdx.x;
     const int pseg = (n + segs - 1) / segs;
     const int pbeg = min(n, seg * pseg), np = min(n, pbeg + pseg) - pbeg;  // this block's points
-    float R0[12], R1[12];
-    bool v0 = false, v1 = false;
-    float* hp0 = ws.hyp + (q * ws.cl_stride + h0) * 16;
-    float* hp1 = ws.hyp + (q * ws.cl_stride + h1) * 16;
+    float Rh[NH][12];
+    bool vh[NH];
+    bool any = false;
 #pragma unroll
-    for (int k = 0; k < 12; ++k) { R0[k] = 0.f; R1[k] = 0.f; }
-    if (h0 < K) {
-        const float4* h4 = reinterpret_cast<const float4*>(hp0);
-        const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
-        v0 = __float_as_int(e.y) == 0;
-        R0[0] = a.x; R0[1] = a.y; R0[2] = a.z; R0[3] = a.w; R0[4] = b.x; R0[5] = b.y; R0[6] = b.z; R0[7] = b.w;
-        R0[8] = c.x; R0[9] = c.y; R0[10] = c.z; R0[11] = c.w;
+    for (int u = 0; u < NH; ++u) {
+        const int h = hbase + SCORE_THREADS * u;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) Rh[u][k] = 0.f;
+        vh[u] = false;
+        if (h < K) {
+            const float4* h4 = reinterpret_cast<const float4*>(ws.hyp + (q * ws.cl_stride + h) * 16);
+            const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
+            vh[u] = __float_as_int(e.y) == 0;
+            Rh[u][0] = a.x; Rh[u][1] = a.y; Rh[u][2] = a.z; Rh[u][3] = a.w; Rh[u][4] = b.x; Rh[u][5] = b.y;
+            Rh[u][6] = b.z; Rh[u][7] = b.w; Rh[u][8] = c.x; Rh[u][9] = c.y; Rh[u][10] = c.z; Rh[u][11] = c.w;
+        }
+        any |= vh[u];
     }
-    if (h1 < K) {
-        const float4* h4 = reinterpret_cast<const float4*>(hp1);
-        const float4 a = h4[0], b = h4[1], c = h4[2], e = h4[3];
-        v1 = __float_as_int(e.y) == 0;
-        R1[0] = a.x; R1[1] = a.y; R1[2] = a.z; R1[3] = a.w; R1[4] = b.x; R1[5] = b.y; R1[6] = b.z; R1[7] = b.w;
-        R1[8] = c.x; R1[9] = c.y; R1[10] = c.z; R1[11] = c.w;
-    }
-    if (!__syncthreads_or((v0 || v1) && np > 0)) return;
+    if (!__syncthreads_or(any && np > 0)) return;
     const uint32_t bar0 = smem_u32(&s_bar[0]), bar1 = smem_u32(&s_bar[1]);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
@@ -2187,14 +2187,19 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
     };
     if (threadIdx.x == 0) issue(0);
     const uint32_t thr2b = __float_as_uint(__fmul_rn(ws.thr, ws.thr));
-    f2_t Rp[9], tp[3];
+    f2_t Rp[NP][9], tp[NP][3];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Rp[k] = f2_pack(R0[k], R1[k]);
+    for (int m = 0; m < NP; ++m) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) tp[k] = f2_pack(R0[9 + k], R1[9 + k]);
+        for (int k = 0; k < 9; ++k) Rp[m][k] = f2_pack(Rh[2 * m][k], Rh[2 * m + 1][k]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tp[m][k] = f2_pack(Rh[2 * m][9 + k], Rh[2 * m + 1][9 + k]);
+    }
     const f2_t mone = f2_pack(-1.0f, -1.0f);
-    int cnt0 = 0, cnt1 = 0;
-    double ea0 = 0.0, ea1 = 0.0, es0 = 0.0, es1 = 0.0;  // ERR: Σ sqrtf(s), Σ s per hypothesis (r20)
+    int cnt[NH];
+    double ea[NH], es[NH];  // ERR: Σ sqrtf(s), Σ s per hypothesis (r20)
+#pragma unroll
+    for (int u = 0; u < NH; ++u) { cnt[u] = 0; ea[u] = es[u] = 0.0; }
     for (int c = 0; c < nchunks; ++c) {
         const int st = c & 1;
         if (threadIdx.x == 0 && c + 1 < nchunks) issue(c + 1);  // buffer st^1 was released by the barrier below
@@ -2217,32 +2222,39 @@ __global__ void __launch_bounds__(SCORE_THREADS, 8) k_score(WS ws, int segs) {
             const float4 x = xs[k];
             const float4 y = ys[k];
             const f2_t X = f2_pack(x.x, x.x), Y = f2_pack(x.y, x.y), Z = f2_pack(x.z, x.z);
-            const f2_t p0 = f2_fma(Rp[2], Z, f2_fma(Rp[1], Y, f2_fma(Rp[0], X, tp[0])));
-            const f2_t p1 = f2_fma(Rp[5], Z, f2_fma(Rp[4], Y, f2_fma(Rp[3], X, tp[1])));
-            const f2_t p2 = f2_fma(Rp[8], Z, f2_fma(Rp[7], Y, f2_fma(Rp[6], X, tp[2])));
-            const f2_t e0 = f2_fma(f2_pack(y.x, y.x), mone, p0);  // p − y: exact negation, one rounding
-            const f2_t e1 = f2_fma(f2_pack(y.y, y.y), mone, p1);
-            const f2_t e2 = f2_fma(f2_pack(y.z, y.z), mone, p2);
-            const f2_t sq = f2_fma(e2, e2, f2_fma(e1, e1, f2_mul(e0, e0)));
-            // s >= 0, so integer order of the bit patterns is float order
-            cnt0 += f2_lo(sq) <= thr2b;
-            cnt1 += f2_hi(sq) <= thr2b;
-            if constexpr (ERR) {
-                const float s0 = __uint_as_float(f2_lo(sq)), s1 = __uint_as_float(f2_hi(sq));
-                ea0 += (double)__fsqrt_rn(s0);
-                ea1 += (double)__fsqrt_rn(s1);
-                es0 += (double)s0;
-                es1 += (double)s1;
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+                const f2_t p0 = f2_fma(Rp[m][2], Z, f2_fma(Rp[m][1], Y, f2_fma(Rp[m][0], X, tp[m][0])));
+                const f2_t p1 = f2_fma(Rp[m][5], Z, f2_fma(Rp[m][4], Y, f2_fma(Rp[m][3], X, tp[m][1])));
+                const f2_t p2 = f2_fma(Rp[m][8], Z, f2_fma(Rp[m][7], Y, f2_fma(Rp[m][6], X, tp[m][2])));
+                const f2_t e0 = f2_fma(f2_pack(y.x, y.x), mone, p0);  // p − y: exact negation, one rounding
+                const f2_t e1 = f2_fma(f2_pack(y.y, y.y), mone, p1);
+                const f2_t e2 = f2_fma(f2_pack(y.z, y.z), mone, p2);
+                const f2_t sq = f2_fma(e2, e2, f2_fma(e1, e1, f2_mul(e0, e0)));
+                // s >= 0, so integer order of the bit patterns is float order
+                cnt[2 * m] += f2_lo(sq) <= thr2b;
+                cnt[2 * m + 1] += f2_hi(sq) <= thr2b;
+                if constexpr (ERR) {
+                    const float s0 = __uint_as_float(f2_lo(sq)), s1 = __uint_as_float(f2_hi(sq));
+                    ea[2 * m] += (double)__fsqrt_rn(s0);
+                    ea[2 * m + 1] += (double)__fsqrt_rn(s1);
+                    es[2 * m] += (double)s0;
+                    es[2 * m + 1] += (double)s1;
+                }
             }
         }
         __syncthreads();  // every thread is done with buffer st before it is refilled
     }
-    if (v0 && cnt0) atomicAdd(reinterpret_cast<int*>(hp0 + 12), cnt0);
-    if (v1 && cnt1) atomicAdd(reinterpret_cast<int*>(hp1 + 12), cnt1);
-    if constexpr (ERR) {
-        double2* he = ws.herr + q * ws.cl_stride;
-        if (v0) { atomicAdd(&he[h0].x, ea0); atomicAdd(&he[h0].y, es0); }
-        if (v1) { atomicAdd(&he[h1].x, ea1); atomicAdd(&he[h1].y, es1); }
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int h = hbase + SCORE_THREADS * u;
+        if (!vh[u]) continue;
+        if (cnt[u]) atomicAdd(reinterpret_cast<int*>(ws.hyp + (q * ws.cl_stride + h) * 16 + 12), cnt[u]);
+        if constexpr (ERR) {
+            double2* he = ws.herr + q * ws.cl_stride;
+            atomicAdd(&he[h].x, ea[u]);
+            atomicAdd(&he[h].y, es[u]);
+        }
     }
 }
 

@@ -110,6 +110,7 @@ struct turboreg_ctx {
     bool tmX_ok = false;
     int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
     int num_sms = 148;
+    int32_t opt_score_pairs = 2;
 };
 
 namespace {
@@ -460,11 +461,17 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         if (ws.err_mode & 1) CK(cudaMemsetAsync(ws.herr, 0, sizeof(double2) * KC * batch, s));
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
-            const int hb = (int)((KC + trk::SCORE_HT - 1) / trk::SCORE_HT);
+            const int npk = c->opt_score_pairs;  // packed hypothesis pairs per thread
+            const int hb = (int)((KC + trk::SCORE_HT * npk - 1) / (trk::SCORE_HT * npk));
             const int segs = std::max(2, std::min(16, (7 * c->num_sms + hb * batch - 1) / (hb * batch)));
             const dim3 g((unsigned)(hb * segs), B);
-            if (ws.err_mode & 1) trk::k_score<true><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
-            else trk::k_score<false><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+            if (ws.err_mode & 1) {
+                if (npk == 2) trk::k_score<true, 2><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+                else trk::k_score<true, 1><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+            } else {
+                if (npk == 2) trk::k_score<false, 2><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+                else trk::k_score<false, 1><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
+            }
         }));
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
     }
@@ -627,6 +634,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "pipeline_host_inputs") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->use_chunks = value != 0;
+    } else if (k == "score_pairs") {
+        if (value < 1 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_score_pairs = (int32_t)value;
     } else if (k == "cuda_graph") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->use_graphs = value != 0;

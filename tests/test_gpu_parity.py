@@ -380,3 +380,13 @@ def test_pipelined_host_batch_matches_single_launch(tr_mod):
     for p in (0, 5, 14):
         r = {k: ra[p][k] for k in ra.dtype.names}
         compare_pair(a, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+
+
+@pytest.mark.parametrize("pairs_per_thread", [1, 2])
+def test_score_packings_agree_with_oracle(tr_mod, pairs_per_thread):
+    cfg = synth.CONFIGS["B"]
+    inst = synth.workload_instance(cfg, pair=17, n=1700)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=1700)
+    tr.set_option("score_pairs", pairs_per_thread)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
