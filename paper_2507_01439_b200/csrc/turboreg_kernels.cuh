@@ -689,9 +689,12 @@ constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 64;
 constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
 constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
+// Row i as a byte map (one byte per column) trades the per-row expansion (~40 instructions per word) for
+// cheaper list lookups; with a few dozen sparse neighbours per dense row it does not pay, so it is off.
+constexpr bool SC2_BYTEMAP = false;
 template <int WPL>
-constexpr int sc2_warp_words() {  // U_i, rank prefix, row i, queue (+ row i as a byte map for n <= 8192)
-    return 96 * WPL + 32 * WPL + (WPL <= 8 ? 32 * WPL * 32 / 4 : 0);
+constexpr int sc2_warp_words() {  // U_i, rank prefix, row i, queue (+ row i as a byte map if enabled)
+    return 96 * WPL + 32 * WPL + ((SC2_BYTEMAP && WPL <= 8) ? 32 * WPL * 32 / 4 : 0);
 }
 template <int WPL>
 constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
@@ -745,6 +748,7 @@ __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, in
         v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
     uint32_t cnt = 0;
     int r = 0;
+    const unsigned span = (unsigned)(i - j - 1);
 #pragma unroll
     for (int c = 0; c < LIST_MAX / 8; ++c) {
         if (c < nch) {
@@ -753,7 +757,8 @@ __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, in
             for (int e = 0; e < 4; ++e) {
                 const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
                 cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
-                r += (k0 > j && k0 < i) + (k1 > j && k1 < i);  // pads are 0 <= j: never counted
+                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
+                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
             }
         }
     }
@@ -772,6 +777,7 @@ __device__ __forceinline__ uint32_t list_bytemap_count_rank(const uint16_t* L, i
         v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
     uint32_t cnt = 0;
     int r = 0;
+    const unsigned span = (unsigned)(i - j - 1);
 #pragma unroll
     for (int c = 0; c < LIST_MAX / 8; ++c) {
         if (c < nch) {
@@ -780,7 +786,8 @@ __device__ __forceinline__ uint32_t list_bytemap_count_rank(const uint16_t* L, i
             for (int e = 0; e < 4; ++e) {
                 const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
                 cnt += (uint32_t)sb[k0] + (uint32_t)sb[k1];
-                r += (k0 > j && k0 < i) + (k1 > j && k1 < i);  // pads are 0 <= j: never counted
+                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
+                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
             }
         }
     }
@@ -816,7 +823,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
     uint32_t* sq = su + 96 * WPL;
-    uint8_t* sbm = (WPL <= 8) ? reinterpret_cast<uint8_t*>(su + 128 * WPL) : nullptr;
+    uint8_t* sbm = (SC2_BYTEMAP && WPL <= 8) ? reinterpret_cast<uint8_t*>(su + 128 * WPL) : nullptr;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
