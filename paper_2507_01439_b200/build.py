@@ -11,7 +11,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libturboreg.so")
 SOURCES = [os.path.join(CSRC, "turboreg_runtime.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "turboreg_kernels.cuh"), os.path.join(CSRC, "turboreg_sc2_mma.cuh"), os.path.join(ROOT, "include", "turboreg.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")] + [
+    os.path.join(ROOT, "include", "turboreg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,186 @@
+// a5 Pivot-Guided Search (Alg. 1 L5-13, Eqs. 5-7) and the SC^2-mode canonical list.
+// Part of turboreg_kernels.cuh.
+#pragma once
+#include "turboreg_select.cuh"
+
+namespace trk {
+
+// ------------------------------------------------------------------------------------------ a5 PGS
+// Alg. 1 L5-13, Eqs. 5-7.  One warp per pivot (i, j): the O2 common neighbours are
+// M = U_i ∧ U_j (z > j > i; for a pivot C_ij = 1, so Ĝ_iz > 0 ⇔ C_iz, reading r10), scanned word-parallel;
+// Ĝ_iz and Ĝ_jz are gathered from the rank-indexed edge lists (rank = prefix popcount of U_i / U_j below
+// z, from a warp scan).  S = Ĝ_ij + Ĝ_iz + Ĝ_jz; the top-K2 by (S desc, z asc) are kept (readings r7, r8):
+// per-lane register lists (K2 <= KL) merged by K2 warp argmax rounds, or K2 threshold rounds otherwise.
+constexpr int PGS_WARPS = 8;
+constexpr int PGS_KL = 8;
+
+template <typename F>
+__device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
+                                                    const uint32_t* ei, const uint32_t* ej, int wij, F&& f) {
+    const int lane = threadIdx.x & 31;
+    int carry_i = 0, carry_j = 0;
+    const int nchunks = (W + 31) >> 5;
+    for (int c = (i + 1) >> 10; c < nchunks; ++c) {  // chunks holding no bit > i contribute nothing
+        const int w = c * 32 + lane;
+        const uint32_t ui = (w < W) ? upper_mask(ri[w], w, i) : 0u;
+        const uint32_t uj = (w < W) ? upper_mask(rj[w], w, j) : 0u;
+        const int pi = __popc(ui), pj = __popc(uj);
+        const int si = warp_incl_scan(pi), sj = warp_incl_scan(pj);
+        const int exi = carry_i + si - pi, exj = carry_j + sj - pj;
+        carry_i += __shfl_sync(FULL, si, 31);
+        carry_j += __shfl_sync(FULL, sj, 31);
+        uint32_t m = ui & uj;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t below = (1u << b) - 1u;
+            const int rk_i = exi + __popc(ui & below);
+            const int rk_j = exj + __popc(uj & below);
+            const int wiz = (int)(__ldg(ei + rk_i) & 0xffffu);
+            const int wjz = (int)(__ldg(ej + rk_j) & 0xffffu);
+            const int z = w * 32 + b;
+            const int S = wij + wiz + wjz;
+            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+        }
+    }
+}
+
+// SC^2 (undirected) mode, reading r9: N(i,j) = {z ∉ {i,j} : C_iz ∧ C_jz} on both sides of the pivot
+// (Table 5 row 10).  Ĝ_iz for z > i is row i's rank-indexed entry; for z < i the edge lives in row
+// z at rank uprefix[z][i>>5] + popc(U_z word below i).
+__device__ __forceinline__ uint32_t sc2_lower_weight(const WS& ws, int q, int W, int z, int x) {
+    const int wx = x >> 5;
+    const uint32_t u = upper_mask(__ldg(ws.bits + q * ws.bits_stride + (int64_t)z * W + wx), wx, z);
+    const int rk = (int)__ldg(ws.uprefix + q * ws.bits_stride + (int64_t)z * W + wx) + __popc(u & ((1u << (x & 31)) - 1u));
+    return __ldg(ws.edges + q * ws.edges_stride + ws.rowptr[q * ws.rp_stride + z] + rk) & 0xffffu;
+}
+template <typename F>
+__device__ __forceinline__ void pgs_scan_candidates_sc2(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj,
+                                                        int W, int i, int j, const uint32_t* ei, const uint32_t* ej,
+                                                        int wij, F&& f) {
+    const int lane = threadIdx.x & 31;
+    int carry_i = 0, carry_j = 0;
+    const int nchunks = (W + 31) >> 5;
+    for (int c = 0; c < nchunks; ++c) {
+        const int w = c * 32 + lane;
+        const uint32_t vi = (w < W) ? ri[w] : 0u, vj = (w < W) ? rj[w] : 0u;
+        const uint32_t ui = (w < W) ? upper_mask(vi, w, i) : 0u;
+        const uint32_t uj = (w < W) ? upper_mask(vj, w, j) : 0u;
+        const int pi = __popc(ui), pj = __popc(uj);
+        const int si = warp_incl_scan(pi), sj = warp_incl_scan(pj);
+        const int exi = carry_i + si - pi, exj = carry_j + sj - pj;
+        carry_i += __shfl_sync(FULL, si, 31);
+        carry_j += __shfl_sync(FULL, sj, 31);
+        uint32_t m = vi & vj;  // C_ii = C_jj = 0 and C_ij = 1: i and j are never in both rows
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t below = (1u << b) - 1u;
+            const int z = w * 32 + b;
+            const uint32_t wiz = (z > i) ? (__ldg(ei + exi + __popc(ui & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, i);
+            const uint32_t wjz = (z > j) ? (__ldg(ej + exj + __popc(uj & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, j);
+            const int S = wij + (int)wiz + (int)wjz;
+            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+        }
+    }
+}
+
+// A clique as (i, j, z) ascending (O2 mode: z > j > i already; SC^2 mode: z anywhere) and S.
+__device__ __forceinline__ int4 sorted_clique(int i, int j, int z, int S) {
+    const int a = min(i, min(j, z)), c = max(i, max(j, z));
+    return make_int4(a, i + j + z - a - c, c, S);
+}
+
+// Per-lane sorted top-KL lists (KL >= K2) merged by K2 warp argmax rounds.
+template <int KL, int MODE>
+__device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj, int W, int i,
+                                             int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long top[KL];
+#pragma unroll
+    for (int r = 0; r < KL; ++r) top[r] = 0ull;
+    auto insert = [&](unsigned long long key) {
+        if (key > top[KL - 1]) {  // sorted insertion, descending
+            unsigned long long k = key;
+#pragma unroll
+            for (int r = 0; r < KL; ++r) {
+                if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
+            }
+        }
+    };
+    if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, insert);
+    else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, insert);
+    int emitted = 0;
+    for (int r = 0; r < K2; ++r) {
+        const unsigned long long head = top[0];
+        const unsigned long long best = warp_max_u64(head);
+        if (best == 0ull) break;
+        if (head == best) {  // keys are unique (distinct z), exactly one lane pops
+#pragma unroll
+            for (int s2 = 0; s2 < KL - 1; ++s2) top[s2] = top[s2 + 1];
+            top[KL - 1] = 0ull;
+        }
+        if (lane == 0) {
+            const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
+            out[r] = sorted_clique(i, j, z, (int)(best >> 32));
+        }
+        ++emitted;
+    }
+    return emitted;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
+    const int q = blockIdx.y;
+    const PairDesc d = ws.desc[q];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pv = blockIdx.x * PGS_WARPS + warp;
+    const int K1 = ws.k1, K2 = ws.k2;
+    if (pv >= K1) return;
+    int4* out = ws.cliq + q * ws.cl_stride + (int64_t)pv * K2;
+    const int P = ws.st[q].npiv;
+    if (pv >= P) {
+        for (int r = lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
+        return;
+    }
+    const int4 pvt = ws.piv[q * ws.piv_stride + pv];
+    const int i = pvt.x, j = pvt.y, wij = pvt.z;
+    const uint32_t* bits = ws.bits + q * ws.bits_stride;
+    const uint32_t* ri = bits + (int64_t)i * W;
+    const uint32_t* rj = bits + (int64_t)j * W;
+    const uint32_t* edges = ws.edges + q * ws.edges_stride;
+    const uint32_t* ei = edges + ws.rowptr[q * ws.rp_stride + i];
+    const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
+    int emitted = 0;
+    if (K2 <= 2) {
+        emitted = pgs_topk_list<2, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+    } else if (K2 <= 4) {
+        emitted = pgs_topk_list<4, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+    } else if (K2 <= PGS_KL) {
+        emitted = pgs_topk_list<PGS_KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+    } else {
+        unsigned long long thr = ~0ull;
+        for (int r = 0; r < K2; ++r) {
+            unsigned long long mine = 0ull;
+            auto take = [&](unsigned long long key) {
+                if (key < thr && key > mine) mine = key;
+            };
+            if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
+            else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, take);
+            const unsigned long long best = warp_max_u64(mine);
+            if (best == 0ull) break;
+            if (lane == 0) {
+                const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
+                out[r] = sorted_clique(i, j, z, (int)(best >> 32));
+            }
+            thr = best;
+            ++emitted;
+        }
+    }
+    for (int r = emitted + lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
+}
+
+}  // namespace trk

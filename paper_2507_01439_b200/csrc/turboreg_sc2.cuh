@@ -1,0 +1,792 @@
+// a3 SC^2 weights and the O2 edge lists (Eq. 2, Def. 2): degrees, heavy/sparse split, assembly.
+// Part of turboreg_kernels.cuh.
+#pragma once
+#include "turboreg_compat.cuh"
+
+namespace trk {
+
+// ------------------------------------------------------------------------------------------ a3 SC^2
+// Eq. 2 for every O2 edge (i < j), assembled in row i's rank order.  One warp per row i;
+// U_i's words are enumerated lane-parallel (lane = word, rank = warp prefix of popcounts), one edge per
+// lane per round:
+//   * both endpoints heavy → Ĝ_ij was computed on the tensor cores: gather D[hpos i][hpos j];
+//   * otherwise (the sparse remainder) → popcount(row_i AND row_j): row_i in registers (lane-strided),
+//     G light edges at a time so G·WPL row_j loads are in flight, REDUX per edge.
+// The result (j << 16 | Ĝ_ij) goes to edges[rowptr(i) + rank]; positive weights feed a 256-bin histogram
+// of Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
+constexpr int SC2_WARPS = 8;
+constexpr int SC2_ROWS_PER_BLOCK = 64;
+constexpr int SEL_WARPS = 8;
+constexpr int SEL_ROWS_PER_BLOCK = 64;
+constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
+constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
+// Row i as a byte map (one byte per column) trades the per-row expansion (~40 instructions per word) for
+// cheaper list lookups; with a few dozen sparse neighbours per dense row it does not pay, so it is off.
+constexpr bool SC2_BYTEMAP = false;
+template <int WPL>
+constexpr int sc2_warp_words() {  // U_i, rank prefix, row i, queue (+ row i as a byte map if enabled)
+    return 96 * WPL + 32 * WPL + ((SC2_BYTEMAP && WPL <= 8) ? 32 * WPL * 32 / 4 : 0);
+}
+template <int WPL>
+constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
+
+// Dense rows (not sparse: heavy, or degree > LIST_MAX), one warp per row i, SC2_BLOCKS_PER_PAIR blocks of
+// warps striding over the pair's dense rows.  Row i's edges come from three sources:
+//   (1) i, j both heavy: written by the tensor-core epilogue (k_sc2_mma) or k_emit_hh, not here;
+//   (2) j sparse (degree <= LIST_MAX, sorted neighbour list L_j), on EITHER side of i:
+//       Ĝ_ij = |L_j ∩ N(i)|, one edge per lane, list entries tested against row i's bitmap in shared
+//       memory.  For j > i the result goes to row i's slot; for j < i to row j's slot, whose rank
+//       (entries of L_j below i, minus those up to j) falls out of the same pass over L_j;
+//   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
+// Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
+constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
+constexpr int SC2_BLOCKS_PER_PAIR = 32;  // 256 warps stride over a pair's dense rows
+constexpr int SC2_CLAIM = 4;
+
+// |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned, zero padded) against row
+// i's bitmap in shared memory.  Entries past len are zeros, so a chunk is processed whole and the pad's
+// bit 0 tests are subtracted once (row i's own bit 0 is read once).
+__device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len, const uint32_t* sr) {
+    const int nch = (len + 7) >> 3;
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t k0 = wv[e] & 0xffffu, k1 = wv[e] >> 16;
+                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+            }
+        }
+    }
+    return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
+}
+
+
+// As list_bitmap_count, for an edge (j, i) with j < i stored in row j: also returns the rank of i among
+// the entries of L_j above j (= #{x in L_j : j < x < i}).
+__device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, int len, const uint32_t* sr, int i,
+                                                           int j, int* rank) {
+    const int nch = (len + 7) >> 3;
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+    int r = 0;
+    const unsigned span = (unsigned)(i - j - 1);
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
+                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
+            }
+        }
+    }
+    *rank = r;
+    return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
+}
+
+// As list_bitmap_count_rank, against row i as a byte map (one byte per column, 0/1) in shared memory:
+// one byte load per list entry instead of word load + shift + mask.
+__device__ __forceinline__ uint32_t list_bytemap_count_rank(const uint16_t* L, int len, const uint8_t* sb, int i, int j,
+                                                            int* rank) {
+    const int nch = (len + 7) >> 3;
+    uint4 v[LIST_MAX / 8];
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c)
+        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
+    uint32_t cnt = 0;
+    int r = 0;
+    const unsigned span = (unsigned)(i - j - 1);
+#pragma unroll
+    for (int c = 0; c < LIST_MAX / 8; ++c) {
+        if (c < nch) {
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                cnt += (uint32_t)sb[k0] + (uint32_t)sb[k1];
+                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
+                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
+            }
+        }
+    }
+    *rank = r;
+    return cnt - (uint32_t)(nch * 8 - len) * (uint32_t)sb[0];
+}
+
+// Edge between dense row i (bitmap sr — or byte map sb when non-null —, U_i words su, rank prefix sp in
+// shared memory) and sparse row j, on either side of i: one code path for both sides (no divergence).
+__device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
+                                                const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
+                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr,
+                                                const uint8_t* sb, int i, int j) {
+    const uint16_t* L = lists + (int64_t)j * LIST_MAX;
+    int rank;
+    const uint32_t c = sb ? list_bytemap_count_rank(L, deg_full[j], sb, i, j, &rank)
+                          : list_bitmap_count_rank(L, deg_full[j], sr, i, j, &rank);
+    const int wj = j >> 5;
+    uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u)) : edges + rowptr[j] + rank;
+    *dst = ((uint32_t)((j > i) ? j : i) << 16) | c;
+}
+
+template <int WPL>
+__global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
+    constexpr int G = 4;
+    constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
+    extern __shared__ uint32_t s_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // block: heavy mask, sparse mask; per warp: U_i, rank prefix, row i, queue
+    uint32_t* hm = s_dyn;
+    uint32_t* lm = s_dyn + 32 * WPL;
+    uint32_t* su = s_dyn + 64 * WPL + warp * sc2_warp_words<WPL>();
+    int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
+    uint32_t* sr = su + 64 * WPL;
+    uint32_t* sq = su + 96 * WPL;
+    uint8_t* sbm = (SC2_BYTEMAP && WPL <= 8) ? reinterpret_cast<uint8_t*>(su + 128 * WPL) : nullptr;
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int nd = ws.st[p].n_dense;
+    const int W = d.W;
+    const int nchunks = (W + 31) >> 5;
+    const int mstride = ws.bits_stride / ws.row_stride;
+    for (int w = threadIdx.x; w < 32 * WPL; w += blockDim.x) {
+        hm[w] = (w < W) ? ws.heavy_mask[p * mstride + w] : 0u;
+        lm[w] = (w < W) ? ws.light_mask[p * mstride + w] : 0u;
+    }
+    __syncthreads();
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    const int32_t* rowptr = ws.rowptr + p * ws.rp_stride;
+    uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int nw = gridDim.x * SC2_WARPS;
+    for (int kq = blockIdx.x * SC2_WARPS + warp; kq < nd; kq += nw) {
+        const int i = ws.dense_list[p * ws.row_stride + kq];
+        const uint32_t* ri = bits + (int64_t)i * W;
+        const int hi = hpos[i];
+        uint32_t* erow = edges + rowptr[i];
+        uint32_t reg[WPL];
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+            const int w = lane + 32 * k;
+            reg[k] = (w < W) ? ri[w] : 0u;
+        }
+        {
+            int carry = 0;
+#pragma unroll
+            for (int k = 0; k < WPL; ++k) {
+                const int w = lane + 32 * k;
+                const uint32_t u = (w < W) ? upper_mask(reg[k], w, i) : 0u;
+                const int cnt = __popc(u);
+                const int incl = warp_incl_scan(cnt);
+                sr[w] = reg[k];
+                if (sbm) {  // bits of word w -> bytes 32w .. 32w+31 (two 16-byte stores)
+                    uint32_t b[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t nib = (reg[k] >> (4 * q)) & 0xfu;
+                        b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+                    }
+                    uint4* d = reinterpret_cast<uint4*>(sbm + 32 * w);
+                    d[0] = make_uint4(b[0], b[1], b[2], b[3]);
+                    d[1] = make_uint4(b[4], b[5], b[6], b[7]);
+                }
+                su[w] = u;
+                sp[w] = carry + incl - cnt;
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+        }
+        __syncwarp();
+        // (2) sparse neighbours on both sides (queued, one edge per lane) and (3) dense-dense upper
+        // neighbours that are not both heavy (warp-cooperative popcount)
+        int nq = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int w = c * 32 + lane;
+            const uint32_t lmw = (w < W) ? lm[w] : 0u;
+            uint32_t ul = ((w < W) ? sr[w] : 0u) & lmw;
+            uint32_t ud = ((w < W) ? su[w] : 0u) & ~lmw;
+            if (hi >= 0 && w < W) ud &= ~hm[w];
+            while (__any_sync(FULL, (ul | ud) != 0u)) {
+                int jl = -1, jd = -1;
+                if (ul) {
+                    jl = w * 32 + __ffs(ul) - 1;
+                    ul &= ul - 1u;
+                } else if (ud) {
+                    jd = w * 32 + __ffs(ud) - 1;
+                    ud &= ud - 1u;
+                }
+                const unsigned sb = __ballot_sync(FULL, jl >= 0);
+                if (jl >= 0) sq[nq + __popc(sb & ((1u << lane) - 1u))] = (uint32_t)jl;
+                nq += __popc(sb);
+                if (nq > QCAP - 32) {
+                    __syncwarp();
+                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
+                    __syncwarp();
+                    nq = 0;
+                }
+                unsigned lb = __ballot_sync(FULL, jd >= 0);
+                while (lb) {
+                    int jj[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        int src = -1;
+                        if (lb) {
+                            src = __ffs(lb) - 1;
+                            lb &= lb - 1u;
+                        }
+                        jj[g] = __shfl_sync(FULL, jd, src < 0 ? 0 : src);
+                        if (src < 0) jj[g] = -1;
+                    }
+                    uint32_t part[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        part[g] = 0u;
+                        if (jj[g] >= 0) {
+                            const uint32_t* rj = bits + (int64_t)jj[g] * W;
+#pragma unroll
+                            for (int k = 0; k < WPL; ++k) {
+                                const int wk = lane + 32 * k;
+                                if (wk < W) part[g] += __popc(reg[k] & __ldg(rj + wk));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        if (jj[g] < 0) break;
+                        const uint32_t tot = __reduce_add_sync(FULL, part[g]);
+                        if (lane == g) {
+                            const int j = jj[g], wj = j >> 5;
+                            erow[sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u))] = ((uint32_t)j << 16) | tot;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
+        __syncwarp();
+    }
+}
+
+// Row classes for the SC^2 assembly: sparse rows (a list, not heavy) go to k_sc2_light, the rest to k_sc2.
+__global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    const int p = blockIdx.x;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int32_t* deg = ws.deg_full + p * ws.row_stride;
+    const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int32_t* L = ws.light_list + p * ws.row_stride;
+    int32_t* Dn = ws.dense_list + p * ws.row_stride;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (i < n && hpos[i] < 0 && deg[i] <= LIST_MAX) ? 1 : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) {
+            if (f) L[pos] = i;
+            else Dn[i - pos] = i;
+        }
+        const unsigned fb = __ballot_sync(FULL, f);
+        if (lane == 0 && ((r0 + warp * 32) >> 5) < d.W)
+            ws.light_mask[p * (ws.bits_stride / ws.row_stride) + ((r0 + warp * 32) >> 5)] = fb;
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+    if (t == 0) { ws.st[p].n_light = s_carry; ws.st[p].n_dense = n - s_carry; }
+    // compact CSR row pointers of the O2 edge lists: exclusive scan of the upper degrees
+    __syncthreads();
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    const int32_t* udeg = ws.deg + p * ws.row_stride;
+    int32_t* rp = ws.rowptr + p * ws.rp_stride;
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (i < n) ? udeg[i] : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) rp[i] = pos;
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+    if (t == 0) { rp[n] = s_carry; ws.st[p].edges = s_carry; }
+}
+
+// SC^2 edges of the sparse rows, packed for full lanes: a warp takes LG sparse rows (bitmaps and lists
+// staged in shared memory), enumerates all their upper edges, and pushes them into two queues — j sparse
+// (|L_j ∩ N(i)| against row i's bitmap) and j dense (|L_i ∩ N(j)| against row j's words) — each flushed
+// 32 edges at a time, one edge per lane.
+// 16-byte asynchronous global -> shared copy (LDGSTS), completed by cp.async.wait_all.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+
+template <int WPL>
+constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
+template <int WPL>
+constexpr int light_warp_words() {
+    return light_rows<WPL>() * 32 * WPL + light_rows<WPL>() * (LIST_MAX / 2) + 64 + 64 + 4 * light_rows<WPL>();
+}
+template <int WPL>
+constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL>() * 4; }
+
+template <int WPL>
+__device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t* bm, const int32_t* meta,
+                                            const uint32_t* q, int cnt) {
+    const int lane = threadIdx.x & 31;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    if (lane < cnt) {
+        const uint32_t e = q[lane];
+        const int j = (int)(e & 0xffffu), t = (int)((e >> 16) & 63), r = (int)(e >> 22);
+        const int i = meta[4 * r], lo = meta[4 * r + 2];
+        const uint32_t c = list_bitmap_count(lists + (int64_t)j * LIST_MAX, deg_full[j], bm + r * 32 * WPL);
+        ws.edges[p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i] + (t - lo)] = ((uint32_t)j << 16) | c;
+    }
+}
+
+template <int WPL>
+__global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
+    constexpr int LG = light_rows<WPL>();
+    extern __shared__ uint32_t s_dyn[];
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    const int W = d.W;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nl = ws.st[p].n_light;
+    const int g0 = (blockIdx.x * 8 + warp) * LG;
+    if (g0 >= nl) return;
+    const int nr = min(LG, nl - g0);
+    uint32_t* bm = s_dyn + warp * light_warp_words<WPL>();
+    uint16_t* ls = reinterpret_cast<uint16_t*>(bm + LG * 32 * WPL);
+    uint32_t* qL = bm + LG * 32 * WPL + LG * (LIST_MAX / 2);
+    uint32_t* qD = qL + 64;
+    int32_t* meta = reinterpret_cast<int32_t*>(qD + 64);
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const uint16_t* lists = ws.lists + p * ws.lists_stride;
+    const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
+    const int32_t* light = ws.light_list + p * ws.row_stride;
+    // stage the group's bitmaps and lists with asynchronous 16-byte copies (all rows in flight at once);
+    // per-row meta (i, d, lo)
+    int my_i = 0, my_d = 0;
+    if (lane < nr) {
+        my_i = light[g0 + lane];
+        my_d = deg_full[my_i];
+        meta[4 * lane] = my_i;
+        meta[4 * lane + 1] = my_d;
+    }
+    __syncwarp();
+    const int W4 = W >> 2;  // 16-byte chunks of a bit row (W is a multiple of 4)
+    for (int idx = lane; idx < nr * W4; idx += 32) {
+        const int r = idx / W4, c = idx - r * W4;
+        cp_async16(bm + r * 32 * WPL + 4 * c, bits + (int64_t)meta[4 * r] * W + 4 * c);
+    }
+    for (int idx = lane; idx < nr * (LIST_MAX / 8); idx += 32) {
+        const int r = idx / (LIST_MAX / 8), c = idx - r * (LIST_MAX / 8);
+        uint16_t* dst = ls + r * LIST_MAX + 8 * c;
+        if (c * 8 < meta[4 * r + 1]) cp_async16(dst, lists + (int64_t)meta[4 * r] * LIST_MAX + 8 * c);
+        else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    int my_lo = 0;
+    for (int r = 0; r < nr; ++r) {
+        const int i = __shfl_sync(FULL, my_i, r), di = __shfl_sync(FULL, my_d, r);
+        int c = 0;
+        for (int t = lane; t < di; t += 32) c += (int)ls[r * LIST_MAX + t] <= i;
+        c = __reduce_add_sync(FULL, (unsigned)c);
+        if (lane == r) my_lo = c;
+    }
+    if (lane < nr) {
+        meta[4 * lane] = my_i; meta[4 * lane + 1] = my_d; meta[4 * lane + 2] = my_lo;
+    }
+    // edge prefix over rows: pref(r) = Σ_{r' < r} (d − lo)
+    const int my_up = (lane < nr) ? my_d - my_lo : 0;
+    const int incl = warp_incl_scan(my_up);
+    const int my_pref = incl - my_up;
+    const int M = __shfl_sync(FULL, incl, 31);
+    if (lane < nr) meta[4 * lane + 3] = my_pref;
+    __syncwarp();
+    const int mstride = ws.bits_stride / ws.row_stride;
+    const uint32_t* lmask = ws.light_mask + p * mstride;
+    int nL = 0;
+    for (int e0 = 0; e0 < M; e0 += 32) {
+        const int e = e0 + lane;
+        bool isL = false;
+        uint32_t packed = 0;
+        if (e < M) {
+            int r = 0;
+            for (int rr = 1; rr < nr; ++rr)
+                if (meta[4 * rr + 3] <= e) r = rr;
+            const int lo = meta[4 * r + 2];
+            const int pr = meta[4 * r + 3];
+            const int t = lo + (e - pr);
+            const int j = ls[r * LIST_MAX + t];
+            packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 22);
+            isL = (__ldg(lmask + (j >> 5)) >> (j & 31)) & 1u;  // sparse j; dense j is k_sc2's edge
+        }
+        const unsigned bL = __ballot_sync(FULL, isL);
+        if (isL) qL[nL + __popc(bL & ((1u << lane) - 1u))] = packed;
+        nL += __popc(bL);
+        __syncwarp();
+        if (nL >= 32) {
+            light_flush<WPL>(ws, p, bm, meta, qL, 32);
+            __syncwarp();
+            if (lane < nL - 32) qL[lane] = qL[32 + lane];
+            nL -= 32;
+            __syncwarp();
+        }
+    }
+    light_flush<WPL>(ws, p, bm, meta, qL, nL);
+}
+
+// The pivot passes stream the pair's compact O2 edge array (E words) with a grid stride: coalesced,
+// no per-row bookkeeping.
+constexpr int SEL_BLOCKS_PER_PAIR = 32;
+
+// Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4).
+// The three edge passes below stream the pair's compact O2 edge array (edges_stride is a multiple of 4
+// words) as uint4: EDGE_VEC edges per thread per round, all loads issued before any is consumed.
+constexpr int EDGE_VEC = 8;
+__device__ __forceinline__ void load_edges8(const uint32_t* edges, int e, int E, uint32_t (&v)[EDGE_VEC]) {
+    if (e + EDGE_VEC <= E) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(edges + e));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(edges + e) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) v[k] = (e + k < E) ? __ldg(edges + e + k) : 0u;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
+    __shared__ int s_hist[256];
+    const int p = blockIdx.y;
+    if (ws.desc[p].n == 0) return;
+    PairState* st = ws.st + p;
+    const int E = st->edges;
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
+    __syncthreads();
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; e < E; e += gridDim.x * blockDim.x * EDGE_VEC) {
+        uint32_t v[EDGE_VEC];
+        load_edges8(edges, e, E, v);
+        // consecutive weights come from one row and cluster in one bin: add runs, not single edges
+        int run_bin = -1, run = 0;
+#pragma unroll
+        for (int k = 0; k < EDGE_VEC; ++k) {
+            const uint32_t w = v[k] & 0xffffu;
+            const int bin = w ? (int)(w >> 7) : -1;
+            if (bin != run_bin) {
+                if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
+                run_bin = bin;
+                run = 0;
+            }
+            ++run;
+        }
+        if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (s_hist[b]) atomicAdd(&st->hist_hi[b], s_hist[b]);
+}
+
+// ------------------------------------------------------------------------------------------ a3 heavy split
+// Full degrees (popcount of each bit row), their sum and maximum, and the sorted uint16 neighbour list of
+// every row with degree <= LIST_MAX (zero-padded to a 16-byte chunk); one warp per row.
+// Degrees and the sorted lists of sparse rows.  Lane l owns 8 consecutive words [g + 8l, g + 8l + 8) of a
+// 256-word group (two 16-byte loads), so lane order is column order and one warp scan of the per-lane
+// counts places every lane's entries; only rows with degree <= LIST_MAX extract their set bits.
+__device__ __forceinline__ void deg_load8(const uint32_t* ri, int w0, int W, uint32_t (&v)[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint4 q = (w0 + 4 * h < W) ? __ldg(reinterpret_cast<const uint4*>(ri + w0 + 4 * h)) : make_uint4(0, 0, 0, 0);
+        v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
+    }
+}
+__device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int pos, uint16_t* L) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint32_t x = v[k];
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1u;
+            L[pos++] = (uint16_t)((w0 + k) * 32 + b);
+        }
+    }
+}
+__global__ void __launch_bounds__(256) k_degree(WS ws) {
+    __shared__ unsigned long long s_sum;
+    __shared__ int s_max;
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    if (threadIdx.x == 0) { s_sum = 0ull; s_max = 0; }
+    __syncthreads();
+    const int W = d.W, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    unsigned mine = 0;
+    int mx = 0;
+    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    uint16_t* lists = ws.lists + p * ws.lists_stride;
+    auto finish_row = [&](int i, int deg, int ucnt) {
+        uint16_t* L = lists + (int64_t)i * LIST_MAX;
+        if (deg <= LIST_MAX)
+            for (int t = deg + lane; t < ((deg + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
+        ucnt = (int)__reduce_add_sync(FULL, (unsigned)ucnt);
+        if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = deg; ws.deg[p * ws.row_stride + i] = ucnt; }
+        mine += deg;
+        mx = max(mx, deg);
+    };
+    if (W <= 256) {  // the whole row in registers; the next row's words are in flight meanwhile
+        const int w0 = 8 * lane;
+        uint32_t vn[8];
+        if (row0 + warp < row1) deg_load8(bits + (int64_t)(row0 + warp) * W, w0, W, vn);
+        for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = vn[k];
+            if (i + SEL_WARPS < row1) deg_load8(bits + (int64_t)(i + SEL_WARPS) * W, w0, W, vn);
+            int cnt = 0, ucnt = 0, uc[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                cnt += __popc(v[k]);
+                uc[k] = __popc(upper_mask(v[k], w0 + k, i));
+                ucnt += uc[k];
+            }
+            const int incl = warp_incl_scan(cnt);
+            const int deg = __shfl_sync(FULL, incl, 31);
+            if (deg <= LIST_MAX) deg_extract8(v, w0, incl - cnt, lists + (int64_t)i * LIST_MAX);
+            if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
+                int run = warp_incl_scan(ucnt) - ucnt;
+                uint32_t pk[4];
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) {
+                    pk[k >> 1] = (uint32_t)run | ((uint32_t)(run + uc[k]) << 16);
+                    run += uc[k] + uc[k + 1];
+                }
+                uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
+                if (w0 < W) *reinterpret_cast<uint2*>(up) = make_uint2(pk[0], pk[1]);
+                if (w0 + 4 < W) *reinterpret_cast<uint2*>(up + 4) = make_uint2(pk[2], pk[3]);
+            }
+            finish_row(i, deg, ucnt);
+        }
+    } else {  // n > 8192: count first, extract in a second pass if sparse
+        for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+            const uint32_t* ri = bits + (int64_t)i * W;
+            int deg = 0, ucnt = 0;
+            for (int g = 0; g < W; g += 256) {
+                uint32_t v[8];
+                const int w0 = g + 8 * lane;
+                deg_load8(ri, w0, W, v);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    deg += __popc(v[k]);
+                    ucnt += __popc(upper_mask(v[k], w0 + k, i));
+                }
+            }
+            deg = __reduce_add_sync(FULL, (unsigned)deg);
+            if (ws.uprefix) {
+                int carry = 0;
+                for (int g = 0; g < W; g += 256) {
+                    uint32_t v[8];
+                    const int w0 = g + 8 * lane;
+                    deg_load8(ri, w0, W, v);
+                    int uc[8], tot = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) { uc[k] = __popc(upper_mask(v[k], w0 + k, i)); tot += uc[k]; }
+                    const int incl = warp_incl_scan(tot);
+                    int run = carry + incl - tot;
+                    uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (w0 + k < W) up[k] = (uint16_t)run;
+                        run += uc[k];
+                    }
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+            }
+            if (deg <= LIST_MAX) {
+                int carry = 0;
+                for (int g = 0; g < W; g += 256) {
+                    uint32_t v[8];
+                    const int w0 = g + 8 * lane;
+                    deg_load8(ri, w0, W, v);
+                    int cnt = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) cnt += __popc(v[k]);
+                    const int incl = warp_incl_scan(cnt);
+                    deg_extract8(v, w0, carry + incl - cnt, lists + (int64_t)i * LIST_MAX);
+                    carry += __shfl_sync(FULL, incl, 31);
+                }
+            }
+            finish_row(i, deg, ucnt);
+        }
+    }
+    if (lane == 0 && mine) { atomicAdd(&s_sum, (unsigned long long)mine); atomicMax(&s_max, mx); }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_sum) { atomicAdd(&ws.st[p].deg_sum, s_sum); atomicMax(&ws.st[p].deg_max, s_max); }
+}
+
+// One block per pair: H = rows with degree >= θ, θ = max(heavy_min_deg, ⌈max degree / 3⌉), raised until
+// |H| <= heavy_cap; |H| < heavy_min_rows ⇒ no tensor-core block.  Ordered compaction (H in index order, so
+// i < j ⇔ hpos(i) < hpos(j)).
+__global__ void __launch_bounds__(1024) k_heavy(WS ws) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry, s_cnt;
+    const int p = blockIdx.x;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n;
+    if (n == 0) return;
+    PairState* st = ws.st + p;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int32_t* deg = ws.deg_full + p * ws.row_stride;
+    int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int thr = max(ws.heavy_min_deg, (st->deg_max + 2) / 3);
+    int cnt = 0;
+    for (int it = 0; it < 64; ++it) {
+        if (t == 0) s_cnt = 0;
+        __syncthreads();
+        int c = 0;
+        for (int i = t; i < n; i += 1024) c += deg[i] >= thr;
+        c = __reduce_add_sync(FULL, (unsigned)c);
+        if (lane == 0 && c) atomicAdd(&s_cnt, c);
+        __syncthreads();
+        cnt = s_cnt;
+        __syncthreads();
+        if (cnt <= ws.heavy_cap) break;
+        thr += max(1, thr / 4);
+    }
+    // widen H to every non-sparse row (degree > LIST_MAX) when that costs no extra 256-row block of the
+    // tensor-core contraction: those rows' dense-dense edges then come from the tensor cores instead of the
+    // latency-bound popcount path
+    {
+        const int thr2 = max(ws.heavy_min_deg, LIST_MAX + 1);
+        if (thr2 < thr) {
+            if (t == 0) s_cnt = 0;
+            __syncthreads();
+            int c = 0;
+            for (int i = t; i < n; i += 1024) c += deg[i] >= thr2;
+            c = __reduce_add_sync(FULL, (unsigned)c);
+            if (lane == 0 && c) atomicAdd(&s_cnt, c);
+            __syncthreads();
+            const int cnt2 = s_cnt;
+            __syncthreads();
+            if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
+        }
+    }
+    const bool use = ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
+    if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; }
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024) {
+        const int i = r0 + t;
+        const int f = (use && i < n && deg[i] >= thr) ? 1 : 0;
+        int x = warp_incl_scan(f);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int y = s_w[lane];
+            int yi = warp_incl_scan(y);
+            s_w[lane] = yi - y;
+        }
+        __syncthreads();
+        const int pos = s_carry + s_w[warp] + x - f;
+        if (i < n) hpos[i] = f ? pos : -1;
+        if (f) ws.heavy_list[p * ws.heavy_cap + pos] = i;
+        const unsigned fb = __ballot_sync(FULL, f);
+        if (lane == 0) {
+            const int wi = (r0 + warp * 32) >> 5;
+            if (wi < d.W) ws.heavy_mask[p * (ws.bits_stride / ws.row_stride) + wi] = fb;
+        }
+        __syncthreads();
+        if (t == 1023) s_carry = pos + f;
+        __syncthreads();
+    }
+}
+
+// X[a][k] = C[H_a][k] as uint8 0/1 over all columns (rows a in [|H|, round_up(|H|, 256)) are zero), and
+// for a < |H| the upper words of row H_a with their exclusive prefix popcounts (UP), from which the
+// tensor-core epilogue reads the O2 test and the edge-list rank of every (H_a, H_b).  One warp per X row.
+__global__ void __launch_bounds__(256) k_expand(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    if (d.n == 0) return;
+    const int h = ws.st[p].heavy_h;
+    if (h == 0) return;
+    const int hp = (h + 255) / 256 * 256;
+    const int a = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (a >= hp) return;
+    const int W = d.W;
+    const int ia = (a < h) ? ws.heavy_list[p * ws.heavy_cap + a] : -1;
+    const uint32_t* row = (a < h) ? ws.bits + p * ws.bits_stride + (int64_t)ia * W : nullptr;
+    uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
+    uint2* up = ws.heavy_UP + p * ws.heavy_UP_stride + (int64_t)a * W;
+    int carry = 0;
+    for (int w0 = 0; w0 < W; w0 += 32) {  // 32 bytes per bit word (two 16-byte stores)
+        const int w = w0 + lane;
+        const uint32_t v = (row && w < W) ? row[w] : 0u;
+        if (w < W) {
+            uint32_t b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t nib = (v >> (4 * q)) & 0xfu;
+                b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
+            dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
+            dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
+        }
+        if (row) {
+            const uint32_t u = (w < W) ? upper_mask(v, w, ia) : 0u;
+            const int cnt = __popc(u);
+            const int incl = warp_incl_scan(cnt);
+            if (w < W) up[w] = make_uint2(u, (uint32_t)(carry + incl - cnt));
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+    }
+}
+
+}  // namespace trk
