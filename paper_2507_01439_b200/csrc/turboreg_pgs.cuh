@@ -129,8 +129,10 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
     return emitted;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
+// KL: per-lane top list length (2, 4, PGS_KL; 0 = K2 threshold rounds), fixed per launch so each
+// instantiation only holds the registers its own branch needs (occupancy: the kernel is latency-bound).
+template <int MODE, int KL>
+__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws) {
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
     const int n = d.n;
@@ -155,12 +157,8 @@ __global__ void __launch_bounds__(PGS_WARPS * 32) k_pgs(WS ws) {
     const uint32_t* ei = edges + ws.rowptr[q * ws.rp_stride + i];
     const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
     int emitted = 0;
-    if (K2 <= 2) {
-        emitted = pgs_topk_list<2, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
-    } else if (K2 <= 4) {
-        emitted = pgs_topk_list<4, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
-    } else if (K2 <= PGS_KL) {
-        emitted = pgs_topk_list<PGS_KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+    if constexpr (KL > 0) {
+        emitted = pgs_topk_list<KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
     } else {
         unsigned long long thr = ~0ull;
         for (int r = 0; r < K2; ++r) {

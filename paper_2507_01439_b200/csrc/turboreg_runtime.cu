@@ -448,8 +448,18 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_SEL_EMIT, [&] { trk::k_select_emit<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_PGS, [&] {
         const dim3 g((c->prm.k1 + trk::PGS_WARPS - 1) / trk::PGS_WARPS, B);
-        if (c->prm.graph_mode == 1) trk::k_pgs<1><<<g, trk::PGS_WARPS * 32, 0, s>>>(ws);
-        else trk::k_pgs<0><<<g, trk::PGS_WARPS * 32, 0, s>>>(ws);
+        const int k2 = c->prm.k2, bt = trk::PGS_WARPS * 32;
+        if (c->prm.graph_mode == 1) {
+            if (k2 <= 2) trk::k_pgs<1, 2><<<g, bt, 0, s>>>(ws);
+            else if (k2 <= 4) trk::k_pgs<1, 4><<<g, bt, 0, s>>>(ws);
+            else if (k2 <= trk::PGS_KL) trk::k_pgs<1, trk::PGS_KL><<<g, bt, 0, s>>>(ws);
+            else trk::k_pgs<1, 0><<<g, bt, 0, s>>>(ws);
+        } else {
+            if (k2 <= 2) trk::k_pgs<0, 2><<<g, bt, 0, s>>>(ws);
+            else if (k2 <= 4) trk::k_pgs<0, 4><<<g, bt, 0, s>>>(ws);
+            else if (k2 <= trk::PGS_KL) trk::k_pgs<0, trk::PGS_KL><<<g, bt, 0, s>>>(ws);
+            else trk::k_pgs<0, 0><<<g, bt, 0, s>>>(ws);
+        }
     }));
     if (c->prm.graph_mode == 1) {  // canonical order + de-duplication of the SC^2-mode clique list (r9)
         int m2 = 1;
