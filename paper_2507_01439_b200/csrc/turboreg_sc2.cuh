@@ -142,7 +142,7 @@ __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* li
 }
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32, 3) k_sc2(WS ws) {
+__global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws) {
     constexpr int G = 4;
     constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
