@@ -572,11 +572,10 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
     int mx = 0;
     const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
-    auto finish_row = [&](int i, int deg, int ucnt) {
+    auto finish_row = [&](int i, int deg, int ucnt) {  // ucnt: the row's total |U_i|
         uint16_t* L = lists + (int64_t)i * LIST_MAX;
         if (deg <= LIST_MAX)
             for (int t = deg + lane; t < ((deg + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
-        ucnt = (int)__reduce_add_sync(FULL, (unsigned)ucnt);
         if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = deg; ws.deg[p * ws.row_stride + i] = ucnt; }
         mine += deg;
         mx = max(mx, deg);
@@ -590,18 +589,26 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = vn[k];
             if (i + SEL_WARPS < row1) deg_load8(bits + (int64_t)(i + SEL_WARPS) * W, w0, W, vn);
-            int cnt = 0, ucnt = 0, uc[8];
+            int cnt = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                cnt += __popc(v[k]);
-                uc[k] = __popc(upper_mask(v[k], w0 + k, i));
-                ucnt += uc[k];
-            }
+            for (int k = 0; k < 8; ++k) cnt += __popc(v[k]);
             const int incl = warp_incl_scan(cnt);
             const int deg = __shfl_sync(FULL, incl, 31);
+            // |U_i| = deg - #neighbours below i: the lane holding word i>>5 counts them from its prefix
+            int below = incl - cnt;
+            {
+                const int k0 = (i >> 5) & 7;
+                const uint32_t mb = (1u << (i & 31)) - 1u;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) below += (k < k0) ? __popc(v[k]) : (k == k0 ? __popc(v[k] & mb) : 0);
+            }
+            const int ucnt = deg - __shfl_sync(FULL, below, (i >> 8) & 31);
             if (deg <= LIST_MAX) deg_extract8(v, w0, incl - cnt, lists + (int64_t)i * LIST_MAX);
             if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
-                int run = warp_incl_scan(ucnt) - ucnt;
+                int uc[8], ul = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) { uc[k] = __popc(upper_mask(v[k], w0 + k, i)); ul += uc[k]; }
+                int run = warp_incl_scan(ul) - ul;
                 uint32_t pk[4];
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) {
@@ -663,7 +670,7 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
                     carry += __shfl_sync(FULL, incl, 31);
                 }
             }
-            finish_row(i, deg, ucnt);
+            finish_row(i, deg, (int)__reduce_add_sync(FULL, (unsigned)ucnt));
         }
     }
     if (lane == 0 && mine) { atomicAdd(&s_sum, (unsigned long long)mine); atomicMax(&s_max, mx); }
