@@ -421,7 +421,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws);
             else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws);
         }));
-        const int lgr = wpl >= 16 ? 2 : 8;  // trk::light_rows<WPL>()
+        // rows per warp group of the instantiation chosen below: light_rows<WPL>() of the rounded-up WPL
+        const int lgr = wpl > 8 ? trk::light_rows<16>() : trk::light_rows<8>();
         const dim3 gl((unsigned)((maxn_batch + 8 * lgr - 1) / (8 * lgr)), B);
         CK(L.run(KID_SC2_LIGHT, [&] {
             if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), s>>>(ws);

@@ -692,20 +692,28 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int32_t* deg = ws.deg_full + p * ws.row_stride;
     int32_t* hpos = ws.hpos + p * ws.row_stride;
-    int thr = max(ws.heavy_min_deg, (st->deg_max + 2) / 3);
-    int cnt = 0;
-    for (int it = 0; it < 64; ++it) {
+    auto count_ge = [&](int th) {  // #rows with degree >= th (block-wide)
         if (t == 0) s_cnt = 0;
         __syncthreads();
         int c = 0;
-        for (int i = t; i < n; i += 1024) c += deg[i] >= thr;
+        for (int i = t; i < n; i += 1024) c += deg[i] >= th;
         c = __reduce_add_sync(FULL, (unsigned)c);
         if (lane == 0 && c) atomicAdd(&s_cnt, c);
         __syncthreads();
-        cnt = s_cnt;
+        const int r = s_cnt;
         __syncthreads();
-        if (cnt <= ws.heavy_cap) break;
-        thr += max(1, thr / 4);
+        return r;
+    };
+    int thr = max(ws.heavy_min_deg, (st->deg_max + 2) / 3);
+    int cnt = count_ge(thr);
+    if (cnt > ws.heavy_cap) {  // smallest threshold whose row count fits the block: binary search
+        int lo = thr, hi = st->deg_max + 1;  // count(lo) > cap >= count(hi) = 0
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (count_ge(mid) > ws.heavy_cap) lo = mid; else hi = mid;
+        }
+        thr = hi;
+        cnt = count_ge(thr);
     }
     // widen H to every non-sparse row (degree > LIST_MAX) when that costs no extra 256-row block of the
     // tensor-core contraction: those rows' dense-dense edges then come from the tensor cores instead of the

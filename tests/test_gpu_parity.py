@@ -390,3 +390,29 @@ def test_score_packings_agree_with_oracle(tr_mod, pairs_per_thread):
     tr.set_option("score_pairs", pairs_per_thread)
     res = tr.register(inst["src"], inst["dst"])
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+def test_wide_rows_general_paths(tr_mod):
+    # n = 8500: W = 268 > 256 words per row (degree pass general path, 16-word-per-lane SC2 kernels,
+    # 2-row sparse groups); 3DLoMatch-shaped so the oracle's literal SC^2 loop stays within seconds
+    cfg = synth.CONFIGS["C"]
+    inst = synth.workload_instance(cfg, pair=1, n=8500)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=8500)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+@pytest.mark.parametrize("cap", [256, 512])
+def test_heavy_cap_raises_threshold(tr_mod, cap):
+    # more high-degree rows than the dense block holds: the degree threshold is raised until |H| <= cap
+    cfg = synth.CONFIGS["B"]
+    inst = synth.workload_instance(cfg, pair=21, n=2600)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2600)
+    tr.set_option("heavy_cap", cap)
+    tr.set_option("heavy_min_rows", 1)
+    res = tr.register(inst["src"], inst["dst"])
+    from paper_2507_01439_b200._binding import I_STATE
+
+    st = tr.intermediate(0, I_STATE)
+    assert 0 < st["heavy_h"] <= cap
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
