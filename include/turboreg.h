@@ -132,6 +132,8 @@ const char* turboreg_status_string(turboreg_status s);
  *                        0 valid, 1 degenerate, 2 empty slot), S (int32 bits), 0
  *   TURBOREG_I_ERRORS    double [K1*K2][2] (MAE, MSE) per slot, NaN for empty / degenerate slots (needs
  *                        TURBOREG_F_HYP_ERRORS or a RANK flag, else TURBOREG_ERR_INVALID_ARGUMENT)
+ *   TURBOREG_I_EDGES     uint32 [n+1 + E] the compact O2 rows: rowptr[0..n], then E words (j << 16) | Ĝ_ij,
+ *                        row i's upper edges (j > i) in increasing j at rowptr[i]
  *   TURBOREG_I_STATE     int64  [16] per-pair scalars: n, W, edges, positive edges, alpha, c_gt, need,
  *                        num_pivots, nonfinite, ...                                                   */
 #define TURBOREG_I_BITS 1
@@ -142,6 +144,7 @@ const char* turboreg_status_string(turboreg_status s);
 #define TURBOREG_I_HYPS 6
 #define TURBOREG_I_STATE 7
 #define TURBOREG_I_ERRORS 8
+#define TURBOREG_I_EDGES 9
 turboreg_status turboreg_get_intermediates(turboreg_ctx* ctx, int32_t pair, int32_t what, void* dst, size_t bytes,
                                            size_t* needed);
 

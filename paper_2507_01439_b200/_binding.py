@@ -38,7 +38,7 @@ F_HYP_ERRORS = 0x4
 F_RANK_MAE = 0x8
 F_RANK_MSE = 0x10
 
-I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS = 1, 2, 3, 4, 5, 6, 7, 8
+I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS, I_EDGES = 1, 2, 3, 4, 5, 6, 7, 8, 9
 
 
 class Params(ctypes.Structure):
@@ -256,6 +256,10 @@ class TurboReg:
             return buf.view(np.float32).reshape(-1, 16)
         if what == I_ERRORS:
             return buf.view(np.float64).reshape(-1, 2)
+        if what == I_EDGES:
+            v = buf.view(np.uint32)
+            n = int(self.intermediate(pair, I_STATE)["n"])
+            return v[: n + 1].astype(np.int64), v[n + 1:]
         if what == I_STATE:
             s = buf.view(np.int64)
             keys = ["n", "W", "edges", "epos", "alpha", "c_gt", "need", "npiv", "nonfinite", "b1", "above",

@@ -868,6 +868,18 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             }
             return TURBOREG_OK;
         }
+        case TURBOREG_I_EDGES: {  // compact O2 rows: uint32 rowptr[n+1], then the E edge words
+            int32_t E = 0;
+            CK(cudaMemcpy(&E, w.rowptr + pair * w.rp_stride + n, sizeof(int32_t), cudaMemcpyDeviceToHost));
+            need = sizeof(uint32_t) * ((size_t)n + 1 + (size_t)E);
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            uint32_t* o = static_cast<uint32_t*>(dst);
+            CK(cudaMemcpy(o, w.rowptr + pair * w.rp_stride, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
+            if (E) CK(cudaMemcpy(o + n + 1, w.edges + pair * w.edges_stride, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
         case TURBOREG_I_PIVOTS: {
             const int P = st.npiv;
             need = sizeof(int32_t) * 3 * (size_t)P;
