@@ -29,7 +29,9 @@ constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
 constexpr int MMA_EPI_WARPS = 16;  // 4 per TMEM lane quarter; sub-warp k drains 32-column chunks k, k+4
 constexpr int MMA_EPI_SUB = MMA_EPI_WARPS / 4;
 constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larger batches loop over it)
+constexpr int MMA_TABLE_PAIRS = 2048;  // pair table in shared memory (larger batches walk global state)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                               (2 * MMA_TABLE_PAIRS + 1) * 4 /*tile prefix + |H| per pair*/ +
                                2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 32 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
 constexpr int MMA_THREADS = 64 + 32 * MMA_EPI_WARPS;
 
@@ -119,6 +121,22 @@ struct TileCursor {
     }
 };
 
+// The same walk over a shared-memory table built once per CTA (tile-count prefix and |H| per pair), for
+// batches up to MMA_PAIRS_MAX: no dependent global loads at tile boundaries.
+struct TableCursor {
+    const int32_t* pre;  // [batch + 1] exclusive prefix of the pairs' tile counts
+    const int32_t* hh;   // [batch] |H| per pair
+    int p = 0;
+    __device__ bool locate(int batch, int g, int* pp, int* rb, int* cb, int* h) {
+        if (g >= pre[batch]) return false;
+        while (pre[p + 1] <= g) ++p;
+        *pp = p;
+        *h = hh[p];
+        mma_tile_coords(g - pre[p], (*h + MMA_BN - 1) / MMA_BN * MMA_BN, rb, cb);
+        return true;
+    }
+};
+
 __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -135,6 +153,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
     uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [8][32][34] (Ĝ < 65536)
     int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 32 * 34);   // [warps][32] edge-list bases
+    int32_t* s_tpre = s_eb + MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
+    int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
+    const bool table = batch <= MMA_TABLE_PAIRS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -153,6 +174,24 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tptr));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    if (table) {  // tile counts per pair, then their exclusive prefix (warp 0)
+        for (int q = threadIdx.x; q < batch; q += blockDim.x) {
+            const int hq = (ws.desc[q].n == 0) ? 0 : ws.st[q].heavy_h;
+            s_th[q] = hq;
+            s_tpre[q + 1] = hq ? mma_tile_count((hq + MMA_BN - 1) / MMA_BN * MMA_BN) : 0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int carry = 0;
+            for (int q0 = 0; q0 < batch; q0 += 32) {
+                const int c = (q0 + lane < batch) ? s_tpre[q0 + lane + 1] : 0;
+                const int incl = warp_incl_scan(c);
+                if (q0 + lane < batch) s_tpre[q0 + lane + 1] = carry + incl;
+                carry += __shfl_sync(FULL, incl, 31);
+            }
+            if (lane == 0) s_tpre[0] = 0;
+        }
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -161,9 +200,11 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
             TileCursor cur;
+            TableCursor tc{s_tpre, s_th};
             int it = 0;
             int p, rb, cb, h;
-            for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x) {
+            for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
+                 g += gridDim.x) {
                 const int KB = ws.desc[p].W * 32 / MMA_BK;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % MMA_STAGES;
@@ -181,9 +222,11 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
             TileCursor cur;
+            TableCursor tc{s_tpre, s_th};
             int it = 0, lt = 0;
             int p, rb, cb, h;
-            for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x, ++lt) {
+            for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
+                 g += gridDim.x, ++lt) {
                 const int KB = ws.desc[p].W * 32 / MMA_BK;
                 const int acc = lt & 1;
                 if (lt >= 2) mbar_wait(tempty0 + 8 * acc, ((lt >> 1) - 1) & 1);  // epilogue drained it
@@ -213,9 +256,11 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
         const int et = threadIdx.x - 64;  // 0..255
         TileCursor cur;
+        TableCursor tc{s_tpre, s_th};
         int lt = 0;
         int p, rb, cb, h;
-        for (int g = blockIdx.x; cur.locate(ws, batch, g, &p, &rb, &cb, &h); g += gridDim.x, ++lt) {
+        for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
+             g += gridDim.x, ++lt) {
             const int acc = lt & 1;
             int32_t* hl = s_hl + acc * MMA_BN;
             const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
