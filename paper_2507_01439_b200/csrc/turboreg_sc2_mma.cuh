@@ -4,7 +4,7 @@
 // C·C over H is a dense binary contraction, so it runs on the 5th-gen tensor cores:
 //   X = C[H, :] as uint8 0/1 (K-major, [h][K]),  D = X · X^T  (exact: int32 accumulate, K <= 32768)
 // with tcgen05.mma kind::i8 (M=128, N=256, K=32 per instruction), operands staged by TMA
-// (cp.async.bulk.tensor, 128B swizzle) through a 3-stage mbarrier pipeline.
+// (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline.
 // Persistent: one CTA per SM walks the (pair, tile) list of the whole batch; the accumulator is double
 // buffered in TMEM (2 × 256 columns) so the epilogue of tile t overlaps the MMAs of tile t+1.
 // The epilogue (4 warps, tcgen05.ld 32x32b, thread = output row a) does not store D: it keeps the entries
@@ -22,17 +22,17 @@ namespace trk {
 constexpr int MMA_BM = 128;
 constexpr int MMA_BN = 256;
 constexpr int MMA_BK = 128;  // bytes = int8 elements per stage per row
-constexpr int MMA_STAGES = 3;
+constexpr int MMA_STAGES = 4;
 constexpr int MMA_A_BYTES = MMA_BM * MMA_BK;  // 16 KB
 constexpr int MMA_B_BYTES = MMA_BN * MMA_BK;  // 32 KB
 constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
 constexpr int MMA_EPI_WARPS = 16;  // 4 per TMEM lane quarter; sub-warp k drains 32-column chunks k, k+4
 constexpr int MMA_EPI_SUB = MMA_EPI_WARPS / 4;
 constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larger batches loop over it)
-constexpr int MMA_TABLE_PAIRS = 2048;  // pair table in shared memory (larger batches walk global state)
+constexpr int MMA_TABLE_PAIRS = 1024;  // pair table in shared memory (larger batches walk global state)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                                (2 * MMA_TABLE_PAIRS + 1) * 4 /*tile prefix + |H| per pair*/ +
-                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 32 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
+                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
 constexpr int MMA_THREADS = 64 + 32 * MMA_EPI_WARPS;
 
 // Instruction descriptor: c_format S32 (bits 4-5 = 2), a/b format u8 (0), both K-major, N>>3 at bit 17,
@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     const uint32_t full0 = bars, empty0 = bars + 64, tfull0 = bars + 128, tempty0 = bars + 144, tptr = bars + 192;
     uint8_t* gen_tptr = smem_raw + (tptr - base);
     int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
-    uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [8][32][34] (Ĝ < 65536)
-    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 32 * 34);   // [warps][32] edge-list bases
+    uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [warps][16][34] (Ĝ < 65536)
+    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);   // [warps][32] edge-list bases
     int32_t* s_tpre = s_eb + MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
     int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
     const bool table = batch <= MMA_TABLE_PAIRS;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             s_eb[ew * 32 + lane] = arow ? __ldg(ws.rowptr + p * ws.rp_stride + ja) : -1;
             const uint2* up0 = ws.heavy_UP + p * ws.heavy_UP_stride;
             uint32_t* edges = ws.edges + p * ws.edges_stride;
-            uint16_t* vt = s_vt + ew * 32 * 34;  // this warp's 32×32 transpose buffer
+            uint16_t* vt = s_vt + ew * 16 * 34;  // this warp's 16×32 transpose buffer
             const int bt = cb * MMA_BN;
             mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -301,16 +301,19 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 }
                 // transpose through shared memory: afterwards lane = column, loop over the warp's 32 rows, so
                 // the UP reads and edge stores of one row are coalesced
-#pragma unroll
-                for (int k = 0; k < 32; ++k) vt[lane * 34 + k] = (uint16_t)v[k];
-                __syncwarp();
                 const int b = bt + c * 32 + lane;
                 const int jb = hl[c * 32 + lane];
                 const uint32_t bit = 1u << (jb & 31);
                 const int wb = jb >> 5;
                 const int a0 = rb * MMA_BM + q * 32;
 #pragma unroll
-                for (int rh = 0; rh < 32; rh += 16) {
+                for (int rh = 0; rh < 32; rh += 16) {  // rows rh .. rh+15 through a 16-row transpose buffer
+                    __syncwarp();
+                    if ((lane & 16) == rh) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) vt[(lane & 15) * 34 + k] = (uint16_t)v[k];
+                    }
+                    __syncwarp();
                     uint2 u[16];
 #pragma unroll
                     for (int r = 0; r < 16; ++r) {  // 16 rows' words in flight at once
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     for (int r = 0; r < 16; ++r)
                         if (u[r].x & bit)
                             edges[s_eb[ew * 32 + rh + r] + (int)u[r].y + __popc(u[r].x & (bit - 1u))] =
-                                ((uint32_t)jb << 16) | vt[(rh + r) * 34 + lane];
+                                ((uint32_t)jb << 16) | vt[r * 34 + lane];
                 }
                 __syncwarp();
             }
