@@ -313,6 +313,31 @@ def run_cuda(args, rank, world, local_rank):
         lat.append(a.elapsed_time(b))
     tr1.close()
 
+    # ---- single-pair latency of configs A-D, device-resident inputs, median of 10
+    lat_cfg = {}
+    if rank == 0:
+        for key in "ABCD":
+            c = synth.CONFIGS[key]
+            inst = synth.workload_instance(c, pair=0)
+            nk = inst["src"].shape[0]
+            sk = torch.from_numpy(inst["src"]).to(dev)
+            dk = torch.from_numpy(inst["dst"]).to(dev)
+            trk_ = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=nk, max_batch=1, device=local_rank)
+            ok_ = np.zeros(1, np.int64)
+            nk_ = np.full(1, nk, np.int32)
+            for _ in range(3):
+                trk_.register_batch(sk, dk, ok_, nk_, out=o1, stream=stream.cuda_stream)
+            ts = []
+            for _ in range(10):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                trk_.register_batch(sk, dk, ok_, nk_, out=o1, stream=stream.cuda_stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            trk_.close()
+            lat_cfg[f"{key} ({c.name}, N={nk}, K1={c.k1})"] = round(float(np.median(ts)), 4)
+
     # gather per-pair results (the only collective: NCCL all_gather of fixed-size records, outside timing)
     if world > 1:
         from paper_2507_01439_b200.sharding import gather_results
@@ -346,6 +371,7 @@ def run_cuda(args, rank, world, local_rank):
         "roofline_kernels": roofs,
         "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "single_pair_latency_ms": float(np.median(lat)),
+        "single_pair_latency_ms_configs": lat_cfg,
         "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{pairs * world}",
         "wall_s_timed_region": wall,
     }
