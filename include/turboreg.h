@@ -172,6 +172,8 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "pipeline_host_inputs" 1 = a call with host inputs and >= 16 pairs copies them in 4 sub-batches, each
  *                      copy overlapping the previous sub-batch's compatibility pass (default); 0 = one copy
  *                      before one launch sequence
+ *   "sc2_chunks"       32-word chunks of a dense row per SC^2 work item: 0 = auto (whole rows for batches
+ *                      >= 32 pairs, single chunks below), 1..64 fixed
  *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1
  *   "cuda_graph"       1 = replay the launch sequence from a CUDA graph captured per (batch, max n) shape
  *                      (default; calls with stage/kernel timing always launch directly); 0 = launch directly

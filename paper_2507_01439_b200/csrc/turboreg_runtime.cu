@@ -111,6 +111,7 @@ struct turboreg_ctx {
     int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
     int num_sms = 148;
     int32_t opt_score_pairs = 2;
+    int32_t opt_sc2_chunks = 0;  // 0 = auto
 };
 
 namespace {
@@ -412,14 +413,15 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int sc2_bpp = std::max(trk::SC2_BLOCKS_PER_PAIR,
                                      std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
         const dim3 gp((unsigned)sc2_bpp, B);
+        const int cpi = c->opt_sc2_chunks > 0 ? c->opt_sc2_chunks : (batch >= 32 ? 64 : 1);  // chunks per item
         CK(L.run(KID_SC2, [&] {
-            if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws);
-            else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws);
-            else if (wpl <= 4) trk::k_sc2<4><<<gp, 256, trk::sc2_smem_bytes<4>(), s>>>(ws);
-            else if (wpl <= 5) trk::k_sc2<5><<<gp, 256, trk::sc2_smem_bytes<5>(), s>>>(ws);
-            else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws);
-            else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws);
-            else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws);
+            if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws, cpi);
+            else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws, cpi);
+            else if (wpl <= 4) trk::k_sc2<4><<<gp, 256, trk::sc2_smem_bytes<4>(), s>>>(ws, cpi);
+            else if (wpl <= 5) trk::k_sc2<5><<<gp, 256, trk::sc2_smem_bytes<5>(), s>>>(ws, cpi);
+            else if (wpl <= 8) trk::k_sc2<8><<<gp, 256, trk::sc2_smem_bytes<8>(), s>>>(ws, cpi);
+            else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws, cpi);
+            else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws, cpi);
         }));
         // rows per warp group of the instantiation chosen below: light_rows<WPL>() of the rounded-up WPL
         const int lgr = wpl > 8 ? trk::light_rows<16>() : trk::light_rows<8>();
@@ -645,6 +647,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "pipeline_host_inputs") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->use_chunks = value != 0;
+    } else if (k == "sc2_chunks") {
+        if (value < 0 || value > 64) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_sc2_chunks = (int32_t)value;
     } else if (k == "score_pairs") {
         if (value < 1 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_score_pairs = (int32_t)value;

@@ -142,7 +142,7 @@ __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* li
 }
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws) {
+__global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
     constexpr int G = 4;
     constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
@@ -175,7 +175,11 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws) {
     const int32_t* rowptr = ws.rowptr + p * ws.rp_stride;
     uint32_t* edges = ws.edges + p * ws.edges_stride;
     const int nw = gridDim.x * SC2_WARPS;
-    for (int kq = blockIdx.x * SC2_WARPS + warp; kq < nd; kq += nw) {
+    // work item = (dense row, group of cpi 32-word chunks of its row): rows with many dense neighbours
+    // are spread over several warps
+    const int ngrp = (nchunks + cpi - 1) / cpi;
+    for (int item = blockIdx.x * SC2_WARPS + warp; item < nd * ngrp; item += nw) {
+        const int kq = item / ngrp, c_lo = (item - kq * ngrp) * cpi, c_hi = min(nchunks, c_lo + cpi);
         const int i = ws.dense_list[p * ws.row_stride + kq];
         const uint32_t* ri = bits + (int64_t)i * W;
         const int hi = hpos[i];
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws) {
         // (2) sparse neighbours on both sides (queued, one edge per lane) and (3) dense-dense upper
         // neighbours that are not both heavy (warp-cooperative popcount)
         int nq = 0;
-        for (int c = 0; c < nchunks; ++c) {
+        for (int c = c_lo; c < c_hi; ++c) {
             const int w = c * 32 + lane;
             const uint32_t lmw = (w < W) ? lm[w] : 0u;
             uint32_t ul = ((w < W) ? sr[w] : 0u) & lmw;

@@ -416,3 +416,14 @@ def test_heavy_cap_raises_threshold(tr_mod, cap):
     st = tr.intermediate(0, I_STATE)
     assert 0 < st["heavy_h"] <= cap
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+@pytest.mark.parametrize("cpi", [1, 2, 64])
+def test_sc2_row_split_agrees_with_oracle(tr_mod, cpi):
+    # dense rows split into work items of cpi 32-word chunks (small batches) or whole rows (large batches)
+    cfg = synth.CONFIGS["B"]
+    inst = synth.workload_instance(cfg, pair=23, n=2300)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2300)
+    tr.set_option("sc2_chunks", cpi)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
