@@ -95,3 +95,22 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(b, "_lib", None)
     with pytest.raises(ImportError):
         b.library()
+
+
+def test_parameter_validation_without_gpu(lib):
+    import paper_2507_01439_b200._binding as b
+
+    h = ctypes.c_void_p()
+    # (tau, tau_base, k1, k2, thr, graph_mode, flags): every case is rejected before any CUDA call
+    cases = [
+        (0.01, 0.0, 10, 2, 0.1, 2, 0),                                  # unknown graph mode
+        (0.01, 0.0, 10000, 2, 0.1, 1, 0),                               # SC^2 mode above the canonical-sort cap
+        (0.01, 0.0, 10, 2, 0.1, 0, b.F_RANK_MAE | b.F_RANK_MSE),        # two ranking metrics
+        (0.01, 0.0, 10, 2, 0.1, 0, 0x100),                              # unknown flag
+        (0.01, 0.005, 10, 2, 0.1, 0, 0),                                # tau_base below tau
+        (0.01, 0.0, 10, 0, 0.1, 0, 0),                                  # k2 < 1
+        (0.01, 0.0, 10, 2, 0.0, 0, 0),                                  # inlier threshold <= 0
+    ]
+    for c in cases:
+        prm = b.Params(*c)
+        assert lib.turboreg_create(ctypes.byref(prm), 0, 100, 1, ctypes.byref(h)) == 1, c
