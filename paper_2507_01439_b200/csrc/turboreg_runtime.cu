@@ -444,7 +444,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_ALPHA, [&] { trk::k_alpha<<<B, 256, 0, s>>>(ws); }));
     CK(L.run(KID_COLLECT, [&] { trk::k_collect<<<gflat, 256, 0, s>>>(ws); }));
     CK(L.run(KID_PIVOT_SORT, [&] {
-        trk::k_pivot_sort<<<B, 1024, trk::PIV_CAP * sizeof(unsigned long long), s>>>(ws);
+        trk::k_pivot_sort<<<B, 1024, trk::PIV_CAP * sizeof(unsigned long long) + trk::SORT_RP_CAP * sizeof(int32_t), s>>>(ws);
     }));
     CK(L.run(KID_SEL_COUNT, [&] { trk::k_select_count<<<gsel, 256, 0, s>>>(ws); }));
     CK(L.run(KID_SEL_SCAN, [&] { trk::k_select_scan<<<B, 1024, 0, s>>>(ws); }));
@@ -612,7 +612,7 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
         cudaFuncSetAttribute(trk::k_sc2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::sc2_smem_bytes<32>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_pivot_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             trk::PIV_CAP * (int)sizeof(unsigned long long)) != cudaSuccess ||
+                             trk::PIV_CAP * (int)sizeof(unsigned long long) + trk::SORT_RP_CAP * 4) != cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2_light<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<5>()) !=
             cudaSuccess ||
         cudaFuncSetAttribute(trk::k_sc2_light<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, trk::light_smem_bytes<8>()) !=

@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(256) k_collect(WS ws) {
     const int alpha = st->alpha;
     const int E = st->edges;
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
-    const int32_t* rp = ws.rowptr + p * ws.rp_stride;
     unsigned long long* cand = ws.cand + (int64_t)p * PIV_CAP;
     const int lane = threadIdx.x & 31;
     for (int e0 = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; __any_sync(FULL, e0 < E);
@@ -129,21 +128,17 @@ __global__ void __launch_bounds__(256) k_collect(WS ws) {
 #pragma unroll
         for (int k = 0; k < EDGE_VEC; ++k) {
             if (!((m >> k) & 1u)) continue;
-            const int e = e0 + k;
-            int lo = 0, hi = n;  // row of edge e: rp[lo] <= e < rp[hi]
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (__ldg(rp + mid) <= e) lo = mid; else hi = mid;
-            }
+            // (i, j) lexicographic = edge position order (rows are contiguous, j increasing within a row),
+            // so the key carries the position; k_pivot_sort resolves (i, j) for the K1 winners only
             const int slot = base++;
             if (slot < PIV_CAP)
-                cand[slot] = ((unsigned long long)(0x7fff - (int)(v[k] & 0xffffu)) << 30) |
-                             ((unsigned long long)lo << 15) | (v[k] >> 16);
+                cand[slot] = ((unsigned long long)(0x7fff - (int)(v[k] & 0xffffu)) << 30) | (unsigned)(e0 + k);
         }
     }
 }
 
 // One block per pair: bitonic sort of the candidates, the first min(K1, #candidates) become the pivots.
+constexpr int SORT_RP_CAP = 16384;  // rowptr entries staged in shared memory after the keys
 __global__ void __launch_bounds__(1024) k_pivot_sort(WS ws) {
     extern __shared__ unsigned long long s_key[];
     const int p = blockIdx.x;
@@ -171,11 +166,28 @@ __global__ void __launch_bounds__(1024) k_pivot_sort(WS ws) {
             __syncthreads();
         }
     }
+    // keys are ((0x7fff - w) << 30 | edge position): the row of a winner comes from a binary search of its
+    // position in rowptr (staged in shared memory when it fits), j from the edge word
     const int P = min(ws.k1, m);
+    const int n = ws.desc[p].n;
+    const int32_t* rpg = ws.rowptr + p * ws.rp_stride;
+    int32_t* s_rp = reinterpret_cast<int32_t*>(s_key + PIV_CAP);
+    const bool staged = n + 1 <= SORT_RP_CAP;
+    if (staged)
+        for (int k = threadIdx.x; k <= n; k += blockDim.x) s_rp[k] = rpg[k];
+    __syncthreads();
+    const int32_t* rp = staged ? s_rp : rpg;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
     int4* piv = ws.piv + p * ws.piv_stride;
     for (int k = threadIdx.x; k < P; k += blockDim.x) {
         const unsigned long long key = s_key[k];
-        piv[k] = make_int4((int)((key >> 15) & 0x7fff), (int)(key & 0x7fff), 0x7fff - (int)(key >> 30), 0);
+        const int e = (int)(key & 0x3fffffffu);
+        int lo = 0, hi = n;  // row of edge e: rp[lo] <= e < rp[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (rp[mid] <= e) lo = mid; else hi = mid;
+        }
+        piv[k] = make_int4(lo, (int)(edges[e] >> 16), 0x7fff - (int)(key >> 30), 0);
     }
     if (threadIdx.x == 0) st->npiv = P;
 }
