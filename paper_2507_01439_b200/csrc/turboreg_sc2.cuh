@@ -506,12 +506,15 @@ __device__ __forceinline__ void load_edges8(const uint32_t* edges, int e, int E,
 }
 
 __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
-    __shared__ int s_hist[256];
+    // one histogram column per lane (bin-major, lane-minor: s_hist[bin * 32 + lane]): the 32 lanes of a
+    // warp never collide on an address or a bank, so the runs of equal bins need no warp aggregation
+    __shared__ int s_hist[256 * 32];
     const int p = blockIdx.y;
     if (ws.desc[p].n == 0) return;
     PairState* st = ws.st + p;
     const int E = st->edges;
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_hist[b] = 0;
+    const int lane = threadIdx.x & 31;
+    for (int b = threadIdx.x; b < 256 * 32; b += blockDim.x) s_hist[b] = 0;
     __syncthreads();
     const uint32_t* edges = ws.edges + p * ws.edges_stride;
     for (int e = (blockIdx.x * blockDim.x + threadIdx.x) * EDGE_VEC; e < E; e += gridDim.x * blockDim.x * EDGE_VEC) {
@@ -524,17 +527,19 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
             const uint32_t w = v[k] & 0xffffu;
             const int bin = w ? (int)(w >> 7) : -1;
             if (bin != run_bin) {
-                if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
+                if (run_bin >= 0) atomicAdd(&s_hist[run_bin * 32 + lane], run);  // other warps may share it
                 run_bin = bin;
                 run = 0;
             }
             ++run;
         }
-        if (run_bin >= 0) atomicAdd(&s_hist[run_bin], run);
+        if (run_bin >= 0) atomicAdd(&s_hist[run_bin * 32 + lane], run);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < 256; b += blockDim.x)
-        if (s_hist[b]) atomicAdd(&st->hist_hi[b], s_hist[b]);
+    for (int b = threadIdx.x >> 5; b < 256; b += blockDim.x >> 5) {  // warp per bin: sum the 32 columns
+        const int c = (int)__reduce_add_sync(FULL, (unsigned)s_hist[b * 32 + lane]);
+        if (lane == 0 && c) atomicAdd(&st->hist_hi[b], c);
+    }
 }
 
 // ------------------------------------------------------------------------------------------ a3 heavy split
