@@ -96,6 +96,7 @@ struct WS {
     int32_t pair_base;    // index of pair 0 of this view in the batch (TMA coordinates address the whole batch)
     uint16_t* uprefix;    // SC^2 mode only: [n][W] exclusive prefix popcount of U_i per word (stride bits_stride)
     double2* herr;        // [K1*K2] per hypothesis (Σ sqrtf(s), Σ s) over the pair's correspondences (r20)
+    int32_t x_fp4;        // heavy_X holds packed e2m1 (block-scaled fp4 tensor-core path) instead of uint8
     int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
 };
 

@@ -774,13 +774,17 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
 // X[a][k] = C[H_a][k] as uint8 0/1 over all columns (rows a in [|H|, round_up(|H|, 256)) are zero), and
 // for a < |H| the upper words of row H_a with their exclusive prefix popcounts (UP), from which the
 // tensor-core epilogue reads the O2 test and the edge-list rank of every (H_a, H_b).  One warp per X row.
+template <bool FP4>
 __global__ void __launch_bounds__(256) k_expand(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     if (d.n == 0) return;
     const int h = ws.st[p].heavy_h;
     if (h == 0) return;
-    const int hp = (h + 255) / 256 * 256;
+    // rows the tiles read: int8 128×256 tiles reach round_up(h, 256); fp4 128×240 tiles (whose B tile is
+    // loaded as 256 rows) reach round_up(h, 240) + 16
+    const int xrows = (int)(ws.heavy_X_stride / ws.heavy_Kcap);  // allocated X rows (beyond: TMA zero fill)
+    const int hp = min(xrows, FP4 ? max((h + 255) / 256 * 256, (h + 239) / 240 * 240 + 16) : (h + 255) / 256 * 256);
     const int a = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (a >= hp) return;
     const int W = d.W;
@@ -793,15 +797,28 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
         const int w = w0 + lane;
         const uint32_t v = (row && w < W) ? row[w] : 0u;
         if (w < W) {
-            uint32_t b[8];
+            if constexpr (FP4) {  // e2m1: bit k -> nibble k = 0x2 (1.0) or 0 (0.0), 16 bytes per word
+                uint32_t b[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint32_t nib = (v >> (4 * q)) & 0xfu;
-                b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+                for (int q = 0; q < 4; ++q) {  // spread byte q's 8 bits to 8 nibbles, then x2 (= 0b0010)
+                    uint32_t x = (v >> (8 * q)) & 0xffu;
+                    x = (x | (x << 12)) & 0x000f000fu;
+                    x = (x | (x << 6)) & 0x03030303u;
+                    x = (x | (x << 3)) & 0x11111111u;
+                    b[q] = x << 1;
+                }
+                reinterpret_cast<uint4*>(X)[w] = make_uint4(b[0], b[1], b[2], b[3]);
+            } else {
+                uint32_t b[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t nib = (v >> (4 * q)) & 0xfu;
+                    b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
+                dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
+                dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
             }
-            uint4* dst = reinterpret_cast<uint4*>(X + 32 * w);
-            dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
-            dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
         }
         if (row) {
             const uint32_t u = (w < W) ? upper_mask(v, w, ia) : 0u;
@@ -810,6 +827,10 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
             if (w < W) up[w] = make_uint2(u, (uint32_t)(carry + incl - cnt));
             carry += __shfl_sync(FULL, incl, 31);
         }
+    }
+    if constexpr (FP4) {  // the last 128-byte K block of an fp4 row may extend past 16 W bytes: zero it
+        const int tail = (16 * W + 127) / 128 * 128;
+        for (int b = 16 * W + 16 * lane; b < tail; b += 16 * 32) *reinterpret_cast<uint4*>(X + b) = make_uint4(0, 0, 0, 0);
     }
 }
 

@@ -76,22 +76,33 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// Block-scaled instruction descriptor (CUTLASS UMMA::InstrDescriptorBlockScaled): a/b format E2M1 (1) at
+// bits 7 / 10, N>>3 at 17, scale format UE8M0 at 23, M>>4 at 24, scale-factor ids 0, K = 64.
+constexpr uint32_t MMA_IDESC_MXF4 = (1u << 7) | (1u << 10) | ((uint32_t)(240 >> 3) << 17) | (1u << 23) |
+                                    ((uint32_t)(MMA_BM >> 4) << 24);
+__device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t tmem_sf, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(tmem_sf));
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// Tiles (rb, cb) of one pair: the 128×256 blocks that touch the strict upper triangle (some b > a):
-// cb >= rb/2.  Count for a padded heavy count hp (multiple of 256).
-__device__ __forceinline__ int mma_tile_count(int hp) {
-    const int RB = hp / MMA_BM, CB = hp / MMA_BN;
+// Tiles (rb, cb) of one pair: 128-row × TN-column blocks (TN = 256 for int8, 240 for the block-scaled
+// fp4 path) that touch the strict upper triangle (some b > a): cb >= rb·128 / TN.
+__device__ __forceinline__ int mma_tile_count(int h, int TN) {
+    const int RB = (h + MMA_BM - 1) / MMA_BM, CB = (h + TN - 1) / TN;
     int t = 0;
-    for (int rb = 0; rb < RB; ++rb) t += CB - rb / 2;
+    for (int rb = 0; rb < RB; ++rb) t += CB - rb * MMA_BM / TN;
     return t;
 }
-__device__ __forceinline__ void mma_tile_coords(int t, int hp, int* rb_out, int* cb_out) {
-    const int RB = hp / MMA_BM, CB = hp / MMA_BN;
+__device__ __forceinline__ void mma_tile_coords(int t, int h, int TN, int* rb_out, int* cb_out) {
+    const int RB = (h + MMA_BM - 1) / MMA_BM, CB = (h + TN - 1) / TN;
     for (int rb = 0; rb < RB; ++rb) {
-        const int c0 = rb / 2;
+        const int c0 = rb * MMA_BM / TN;
         const int cnt = CB - c0;
         if (t < cnt) { *rb_out = rb; *cb_out = c0 + t; return; }
         t -= cnt;
@@ -101,13 +112,13 @@ __device__ __forceinline__ void mma_tile_coords(int t, int hp, int* rb_out, int*
 // Global tile g of the batch -> (pair, rb, cb): linear walk over pairs with a running prefix (each role
 // walks its own tiles in increasing g, so the cursor only moves forward).
 struct TileCursor {
-    int p = 0, base = 0, cnt = -1;
+    int p = 0, base = 0, cnt = -1, TN = MMA_BN;
     __device__ bool locate(const WS& ws, int batch, int g, int* pp, int* rb, int* cb, int* h) {
         for (;;) {
             if (p >= batch) return false;
             if (cnt < 0) {
                 const int hh = (ws.desc[p].n == 0) ? 0 : ws.st[p].heavy_h;
-                cnt = hh ? mma_tile_count((hh + MMA_BN - 1) / MMA_BN * MMA_BN) : 0;
+                cnt = hh ? mma_tile_count(hh, TN) : 0;
             }
             if (g < base + cnt) break;
             base += cnt;
@@ -116,7 +127,7 @@ struct TileCursor {
         }
         *pp = p;
         *h = ws.st[p].heavy_h;
-        mma_tile_coords(g - base, (*h + MMA_BN - 1) / MMA_BN * MMA_BN, rb, cb);
+        mma_tile_coords(g - base, *h, TN, rb, cb);
         return true;
     }
 };
@@ -126,13 +137,14 @@ struct TileCursor {
 struct TableCursor {
     const int32_t* pre;  // [batch + 1] exclusive prefix of the pairs' tile counts
     const int32_t* hh;   // [batch] |H| per pair
+    int TN;
     int p = 0;
     __device__ bool locate(int batch, int g, int* pp, int* rb, int* cb, int* h) {
         if (g >= pre[batch]) return false;
         while (pre[p + 1] <= g) ++p;
         *pp = p;
         *h = hh[p];
-        mma_tile_coords(g - pre[p], (*h + MMA_BN - 1) / MMA_BN * MMA_BN, rb, cb);
+        mma_tile_coords(g - pre[p], *h, TN, rb, cb);
         return true;
     }
 };
@@ -141,7 +153,13 @@ __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// FP4: X holds packed e2m1 (1.0 / 0.0 per bit, two per byte) and the contraction runs as
+// tcgen05.mma kind::mxf4.block_scale (K = 64 per instruction, every block scale 2^0 in TMEM, fp32
+// accumulate — exact for counts < 2^24) on 128×240 tiles, so the two accumulators (columns 0 and 256)
+// leave TMEM columns 496.. for the scale factors.
+template <bool FP4>
 __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constant__ CUtensorMap tmX, WS ws, int batch) {
+    constexpr int TN = FP4 ? 240 : MMA_BN;  // tile columns
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t tiles = (base + 1023u) & ~1023u;  // 1024-byte aligned for the 128B swizzle
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         for (int q = threadIdx.x; q < batch; q += blockDim.x) {
             const int hq = (ws.desc[q].n == 0) ? 0 : ws.st[q].heavy_h;
             s_th[q] = hq;
-            s_tpre[q + 1] = hq ? mma_tile_count((hq + MMA_BN - 1) / MMA_BN * MMA_BN) : 0;
+            s_tpre[q + 1] = hq ? mma_tile_count(hq, TN) : 0;
         }
         __syncthreads();
         if (warp == 0) {
@@ -196,16 +214,32 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(gen_tptr);
+    if constexpr (FP4) {  // block scales: UE8M0 127 (= 1.0) in every byte of columns 496..511
+        if (warp >= 2 && warp < 6) {
+            const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 496u;
+            const uint32_t one = 0x7f7f7f7fu;
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                    taddr),
+                "r"(one)
+                : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
             TileCursor cur;
-            TableCursor tc{s_tpre, s_th};
+            cur.TN = TN;
+            TableCursor tc{s_tpre, s_th, TN};
             int it = 0;
             int p, rb, cb, h;
             for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
                  g += gridDim.x) {
-                const int KB = ws.desc[p].W * 32 / MMA_BK;
+                const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % MMA_STAGES;
                     const int round = it / MMA_STAGES;
@@ -214,20 +248,21 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     const uint32_t b_dst = a_dst + MMA_A_BYTES;
                     mbar_expect_tx(full0 + 8 * s, MMA_STAGE_BYTES);
                     tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, ws.pair_base + p);
-                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN, ws.pair_base + p);
-                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * MMA_BN + 128, ws.pair_base + p);
+                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN, ws.pair_base + p);
+                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN + 128, ws.pair_base + p);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
             TileCursor cur;
-            TableCursor tc{s_tpre, s_th};
+            cur.TN = TN;
+            TableCursor tc{s_tpre, s_th, TN};
             int it = 0, lt = 0;
             int p, rb, cb, h;
             for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
                  g += gridDim.x, ++lt) {
-                const int KB = ws.desc[p].W * 32 / MMA_BK;
+                const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 const int acc = lt & 1;
                 if (lt >= 2) mbar_wait(tempty0 + 8 * acc, ((lt >> 1) - 1) & 1);  // epilogue drained it
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -240,8 +275,12 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     const uint32_t b_src = a_src + MMA_A_BYTES;
 #pragma unroll
                     for (int k = 0; k < MMA_BK / 32; ++k) {
-                        umma_i8(tacc, umma_desc_sw128(a_src + 32 * k), umma_desc_sw128(b_src + 32 * k), MMA_IDESC,
-                                (kb | k) ? 1u : 0u);
+                        if constexpr (FP4)
+                            umma_mxf4(tacc, umma_desc_sw128(a_src + 32 * k), umma_desc_sw128(b_src + 32 * k),
+                                      MMA_IDESC_MXF4, tmem + 496u, (kb | k) ? 1u : 0u);
+                        else
+                            umma_i8(tacc, umma_desc_sw128(a_src + 32 * k), umma_desc_sw128(b_src + 32 * k), MMA_IDESC,
+                                    (kb | k) ? 1u : 0u);
                     }
                     umma_commit(empty0 + 8 * s);  // frees the smem stage once these MMAs completed
                 }
@@ -256,7 +295,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
         const int et = threadIdx.x - 64;  // 0..255
         TileCursor cur;
-        TableCursor tc{s_tpre, s_th};
+        cur.TN = TN;
+        TableCursor tc{s_tpre, s_th, TN};
         int lt = 0;
         int p, rb, cb, h;
         for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
@@ -265,8 +305,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             int32_t* hl = s_hl + acc * MMA_BN;
             const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
             for (int k = et; k < MMA_BN; k += 32 * MMA_EPI_WARPS) {
-                const int b = cb * MMA_BN + k;
-                hl[k] = (b < h) ? __ldg(hlist + b) : -1;
+                const int b = cb * TN + k;
+                hl[k] = (k < TN && b < h) ? __ldg(hlist + b) : -1;
             }
             named_bar(1, 32 * MMA_EPI_WARPS);  // heavy ids of this tile's columns visible to all epilogue warps
             const int a = rb * MMA_BM + q * 32 + lane;  // this thread's TMEM lane = output row
@@ -277,7 +317,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             const uint2* up0 = ws.heavy_UP + p * ws.heavy_UP_stride;
             uint32_t* edges = ws.edges + p * ws.edges_stride;
             uint16_t* vt = s_vt + ew * 16 * 34;  // this warp's 16×32 transpose buffer
-            const int bt = cb * MMA_BN;
+            const int bt = cb * TN;
             mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -311,7 +351,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     __syncwarp();
                     if ((lane & 16) == rh) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) vt[(lane & 15) * 34 + k] = (uint16_t)v[k];
+                        for (int k = 0; k < 32; ++k)
+                            vt[(lane & 15) * 34 + k] = FP4 ? (uint16_t)__uint_as_float(v[k]) : (uint16_t)v[k];
                     }
                     __syncwarp();
                     uint2 u[16];

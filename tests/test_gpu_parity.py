@@ -427,3 +427,17 @@ def test_sc2_row_split_agrees_with_oracle(tr_mod, cpi):
     tr.set_option("sc2_chunks", cpi)
     res = tr.register(inst["src"], inst["dst"])
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
+@pytest.mark.parametrize("fp4", [0, 1])
+@pytest.mark.parametrize("key,n", [("B", 2600), ("D", 2100), ("E", None)])
+def test_tensor_core_formats_agree_with_oracle(tr_mod, fp4, key, n):
+    # int8 operands (kind::i8) vs packed e2m1 operands with unit block scales (kind::mxf4.block_scale)
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=29, n=n)
+    nn = inst["src"].shape[0]
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn)
+    tr.set_option("mma_fp4", fp4)
+    tr.set_option("heavy_min_rows", 1)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
