@@ -178,6 +178,8 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "sc2_chunks"       32-word chunks of a dense row per SC^2 work item: 0 = auto (whole rows for batches
  *                      >= 32 pairs, single chunks below), 1..64 fixed
  *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1
+ *   "concurrent_sc2"   1 = the sparse-row SC^2 kernel runs on a second stream alongside the dense-row kernel
+ *                      (default; calls with stage/kernel timing stay on one stream); 0 = one stream
  *   "cuda_graph"       1 = replay the launch sequence from a CUDA graph captured per (batch, max n) shape
  *                      (default; calls with stage/kernel timing always launch directly); 0 = launch directly
  *   "compat_variant"   compat-graph tiling: 0 = row pairs in f32x2 lanes x 2 column tiles per warp

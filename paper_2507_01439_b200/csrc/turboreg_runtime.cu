@@ -71,6 +71,9 @@ struct turboreg_ctx {
     int32_t max_n = 0, max_batch = 0, Wmax = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-input sub-batches
+    cudaStream_t side_stream = nullptr;  // the sparse-row SC^2 kernel, concurrent with the dense-row one
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool use_fork = true;
     cudaEvent_t ev_start = nullptr, ev_chunk[NCHUNK] = {};
     bool use_chunks = true;
     // device workspace
@@ -423,6 +426,14 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
                                      std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
         const dim3 gp((unsigned)sc2_bpp, B);
         const int cpi = c->opt_sc2_chunks > 0 ? c->opt_sc2_chunks : (batch >= 32 ? 64 : 1);  // chunks per item
+        // the sparse-row kernel needs only the row classes and lists: it runs on the side stream while the
+        // dense-row kernel runs here (both are latency-bound; timed calls keep one stream for the events)
+        const bool fork = c->use_fork && !timed;
+        cudaStream_t sl = fork ? c->side_stream : s;
+        if (fork) {
+            CK(cudaEventRecord(c->ev_fork, s));
+            CK(cudaStreamWaitEvent(sl, c->ev_fork, 0));
+        }
         CK(L.run(KID_SC2, [&] {
             if (wpl <= 1) trk::k_sc2<1><<<gp, 256, trk::sc2_smem_bytes<1>(), s>>>(ws, cpi);
             else if (wpl <= 2) trk::k_sc2<2><<<gp, 256, trk::sc2_smem_bytes<2>(), s>>>(ws, cpi);
@@ -436,14 +447,18 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int lgr = wpl > 8 ? trk::light_rows<16>() : trk::light_rows<8>();
         const dim3 gl((unsigned)((maxn_batch + 8 * lgr - 1) / (8 * lgr)), B);
         CK(L.run(KID_SC2_LIGHT, [&] {
-            if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), s>>>(ws);
-            else if (wpl <= 2) trk::k_sc2_light<2><<<gl, 256, trk::light_smem_bytes<2>(), s>>>(ws);
-            else if (wpl <= 4) trk::k_sc2_light<4><<<gl, 256, trk::light_smem_bytes<4>(), s>>>(ws);
-            else if (wpl <= 5) trk::k_sc2_light<5><<<gl, 256, trk::light_smem_bytes<5>(), s>>>(ws);
-            else if (wpl <= 8) trk::k_sc2_light<8><<<gl, 256, trk::light_smem_bytes<8>(), s>>>(ws);
-            else if (wpl <= 16) trk::k_sc2_light<16><<<gl, 256, trk::light_smem_bytes<16>(), s>>>(ws);
-            else trk::k_sc2_light<32><<<gl, 256, trk::light_smem_bytes<32>(), s>>>(ws);
+            if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), sl>>>(ws);
+            else if (wpl <= 2) trk::k_sc2_light<2><<<gl, 256, trk::light_smem_bytes<2>(), sl>>>(ws);
+            else if (wpl <= 4) trk::k_sc2_light<4><<<gl, 256, trk::light_smem_bytes<4>(), sl>>>(ws);
+            else if (wpl <= 5) trk::k_sc2_light<5><<<gl, 256, trk::light_smem_bytes<5>(), sl>>>(ws);
+            else if (wpl <= 8) trk::k_sc2_light<8><<<gl, 256, trk::light_smem_bytes<8>(), sl>>>(ws);
+            else if (wpl <= 16) trk::k_sc2_light<16><<<gl, 256, trk::light_smem_bytes<16>(), sl>>>(ws);
+            else trk::k_sc2_light<32><<<gl, 256, trk::light_smem_bytes<32>(), sl>>>(ws);
         }));
+        if (fork) {
+            CK(cudaEventRecord(c->ev_join, sl));
+            CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+        }
     }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
     const int sel_bpp = std::max(trk::SEL_BLOCKS_PER_PAIR, std::min((4 * c->num_sms + batch - 1) / batch, 256));
@@ -584,6 +599,9 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     // torch's default stream) are complete before our kernels read them.
     if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreate(&c->own_stream) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess) {
         st = TURBOREG_ERR_CUDA;
     }
@@ -667,6 +685,9 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "score_pairs") {
         if (value < 1 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_score_pairs = (int32_t)value;
+    } else if (k == "concurrent_sc2") {
+        if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->use_fork = value != 0;
     } else if (k == "cuda_graph") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->use_graphs = value != 0;
@@ -707,6 +728,9 @@ void turboreg_destroy(turboreg_ctx* c) {
     if (c->h_results) cudaFreeHost(c->h_results);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->side_stream) cudaStreamDestroy(c->side_stream);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
     for (auto e : c->ev_chunk)
         if (e) cudaEventDestroy(e);
