@@ -566,7 +566,7 @@ __device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int
         }
     }
 }
-__global__ void __launch_bounds__(256) k_degree(WS ws) {
+__global__ void __launch_bounds__(256, 5) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
     const int p = blockIdx.y;
@@ -589,46 +589,73 @@ __global__ void __launch_bounds__(256) k_degree(WS ws) {
         mine += deg;
         mx = max(mx, deg);
     };
-    if (W <= 256) {  // the whole row in registers; the next row's words are in flight meanwhile
-        const int w0 = 8 * lane;
-        uint32_t vn[8];
-        if (row0 + warp < row1) deg_load8(bits + (int64_t)(row0 + warp) * W, w0, W, vn);
-        for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
-            uint32_t v[8];
+    if (W <= 256) {  // the whole row in registers (WPL = ceil(W/32) words per lane, no idle lanes)
+        auto rows = [&](auto wpl) {
+            constexpr int WPL = decltype(wpl)::value;
+            const int w0 = WPL * lane;
+            uint32_t vn[WPL];
+            auto load = [&](int i) {
+                const uint32_t* ri = bits + (int64_t)i * W;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = vn[k];
-            if (i + SEL_WARPS < row1) deg_load8(bits + (int64_t)(i + SEL_WARPS) * W, w0, W, vn);
-            int cnt = 0;
+                for (int k = 0; k < WPL; ++k) vn[k] = (w0 + k < W) ? __ldg(ri + w0 + k) : 0u;
+            };
+            if (row0 + warp < row1) load(row0 + warp);
+            for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
+                uint32_t v[WPL];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) cnt += __popc(v[k]);
-            const int incl = warp_incl_scan(cnt);
-            const int deg = __shfl_sync(FULL, incl, 31);
-            // |U_i| = deg - #neighbours below i: the lane holding word i>>5 counts them from its prefix
-            int below = incl - cnt;
-            {
-                const int k0 = (i >> 5) & 7;
-                const uint32_t mb = (1u << (i & 31)) - 1u;
+                for (int k = 0; k < WPL; ++k) v[k] = vn[k];
+                if (i + SEL_WARPS < row1) load(i + SEL_WARPS);
+                int cnt = 0;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) below += (k < k0) ? __popc(v[k]) : (k == k0 ? __popc(v[k] & mb) : 0);
-            }
-            const int ucnt = deg - __shfl_sync(FULL, below, (i >> 8) & 31);
-            if (deg <= LIST_MAX) deg_extract8(v, w0, incl - cnt, lists + (int64_t)i * LIST_MAX);
-            if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
-                int uc[8], ul = 0;
+                for (int k = 0; k < WPL; ++k) cnt += __popc(v[k]);
+                const int incl = warp_incl_scan(cnt);
+                const int deg = __shfl_sync(FULL, incl, 31);
+                // |U_i| = deg - #neighbours below i: the lane holding word i>>5 counts them from its prefix
+                const int wi = i >> 5, li = wi / WPL, k0 = wi - li * WPL;
+                int below = incl - cnt;
+                {
+                    const uint32_t mb = (1u << (i & 31)) - 1u;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) { uc[k] = __popc(upper_mask(v[k], w0 + k, i)); ul += uc[k]; }
-                int run = warp_incl_scan(ul) - ul;
-                uint32_t pk[4];
-#pragma unroll
-                for (int k = 0; k < 8; k += 2) {
-                    pk[k >> 1] = (uint32_t)run | ((uint32_t)(run + uc[k]) << 16);
-                    run += uc[k] + uc[k + 1];
+                    for (int k = 0; k < WPL; ++k) below += (k < k0) ? __popc(v[k]) : (k == k0 ? __popc(v[k] & mb) : 0);
                 }
-                uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
-                if (w0 < W) *reinterpret_cast<uint2*>(up) = make_uint2(pk[0], pk[1]);
-                if (w0 + 4 < W) *reinterpret_cast<uint2*>(up + 4) = make_uint2(pk[2], pk[3]);
+                const int ucnt = deg - __shfl_sync(FULL, below, li);
+                if (deg <= LIST_MAX) {
+                    uint16_t* L = lists + (int64_t)i * LIST_MAX;
+                    int pos = incl - cnt;
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) {
+                        uint32_t x = v[k];
+                        while (x) {
+                            const int b = __ffs(x) - 1;
+                            x &= x - 1u;
+                            L[pos++] = (uint16_t)((w0 + k) * 32 + b);
+                        }
+                    }
+                }
+                if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
+                    int uc[WPL], ul = 0;
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) { uc[k] = __popc(upper_mask(v[k], w0 + k, i)); ul += uc[k]; }
+                    int run = warp_incl_scan(ul) - ul;
+                    uint16_t* up = ws.uprefix + p * ws.bits_stride + (int64_t)i * W + w0;
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) {
+                        if (w0 + k < W) up[k] = (uint16_t)run;
+                        run += uc[k];
+                    }
+                }
+                finish_row(i, deg, ucnt);
             }
-            finish_row(i, deg, ucnt);
+        };
+        switch ((W + 31) >> 5) {
+            case 1: rows(std::integral_constant<int, 1>{}); break;
+            case 2: rows(std::integral_constant<int, 2>{}); break;
+            case 3: rows(std::integral_constant<int, 3>{}); break;
+            case 4: rows(std::integral_constant<int, 4>{}); break;
+            case 5: rows(std::integral_constant<int, 5>{}); break;
+            case 6: rows(std::integral_constant<int, 6>{}); break;
+            case 7: rows(std::integral_constant<int, 7>{}); break;
+            default: rows(std::integral_constant<int, 8>{}); break;
         }
     } else {  // n > 8192: count first, extract in a second pass if sparse
         for (int i = row0 + warp; i < row1; i += SEL_WARPS) {
