@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             s_eb[ew * 32 + lane] = arow ? __ldg(ws.rowptr + p * ws.rp_stride + ja) : -1;
             const uint2* up0 = ws.heavy_UP + p * ws.heavy_UP_stride;
             uint32_t* edges = ws.edges + p * ws.edges_stride;
+            asm("" : "+l"(edges));  // keep the base in registers (ptxas otherwise recomputes it per store)
             uint16_t* vt = s_vt + ew * 16 * 34;  // this warp's 16×32 transpose buffer
             const int bt = cb * TN;
             mbar_wait(tfull0 + 8 * acc, (lt >> 1) & 1);
@@ -344,28 +345,37 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 const int b = bt + c * 32 + lane;
                 const int jb = hl[c * 32 + lane];
                 const uint32_t bit = 1u << (jb & 31);
-                const int wb = jb >> 5;
+                const uint32_t jhi = (uint32_t)jb << 16, bm1 = bit - 1u;
                 const int a0 = rb * MMA_BM + q * 32;
+                // rows r < lim of this warp are heavy rows (a0 + r < h) below the lane's column (b > a0 + r)
+                const int lim = jb >= 0 ? min(b - a0, h - a0) : 0;
+                const char* upl = reinterpret_cast<const char*>(up0 + (size_t)a0 * W + (jb >= 0 ? (jb >> 5) : 0));
+                const size_t W8 = (size_t)W * sizeof(uint2);
 #pragma unroll
                 for (int rh = 0; rh < 32; rh += 16) {  // rows rh .. rh+15 through a 16-row transpose buffer
                     __syncwarp();
-                    if ((lane & 16) == rh) {
+                    if ((lane & 16) == rh) {  // two 16-bit values per 32-bit store
+                        uint32_t* vr = reinterpret_cast<uint32_t*>(vt + (lane & 15) * 34);
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            vt[(lane & 15) * 34 + k] = FP4 ? (uint16_t)__uint_as_float(v[k]) : (uint16_t)v[k];
+                        for (int k = 0; k < 32; k += 2) {
+                            const uint32_t lo = FP4 ? (uint32_t)__uint_as_float(v[k]) : v[k];
+                            const uint32_t hi = FP4 ? (uint32_t)__uint_as_float(v[k + 1]) : v[k + 1];
+                            vr[k >> 1] = (lo & 0xffffu) | (hi << 16);
+                        }
                     }
                     __syncwarp();
                     uint2 u[16];
+                    const char* pr = upl + rh * W8;
+                    // 16 rows' words in flight at once; unconditional (rows < heavy_cap, a multiple of 128, are
+                    // inside the buffer) and masked by lim afterwards
 #pragma unroll
-                    for (int r = 0; r < 16; ++r) {  // 16 rows' words in flight at once
-                        const bool ok = s_eb[ew * 32 + rh + r] >= 0 && jb >= 0 && b > a0 + rh + r;
-                        u[r] = ok ? __ldg(up0 + (int64_t)(a0 + rh + r) * W + wb) : make_uint2(0u, 0u);
+                    for (int r = 0; r < 16; ++r, pr += W8) u[r] = __ldg(reinterpret_cast<const uint2*>(pr));
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        const uint32_t x = u[r].x;
+                        const uint32_t slot = (uint32_t)(s_eb[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
+                        if (rh + r < lim && (x & bit)) edges[slot] = jhi | vt[r * 34 + lane];
                     }
-#pragma unroll
-                    for (int r = 0; r < 16; ++r)
-                        if (u[r].x & bit)
-                            edges[s_eb[ew * 32 + rh + r] + (int)u[r].y + __popc(u[r].x & (bit - 1u))] =
-                                ((uint32_t)jb << 16) | vt[r * 34 + lane];
                 }
                 __syncwarp();
             }
