@@ -32,7 +32,7 @@ constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larg
 constexpr int MMA_TABLE_PAIRS = 1024;  // pair table in shared memory (larger batches walk global state)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                                (2 * MMA_TABLE_PAIRS + 1) * 4 /*tile prefix + |H| per pair*/ +
-                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4;
+                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + 2 * MMA_EPI_WARPS * 32 * 4;
 constexpr int MMA_THREADS = 64 + 32 * MMA_EPI_WARPS;
 
 // Instruction descriptor: c_format S32 (bits 4-5 = 2), a/b format u8 (0), both K-major, N>>3 at bit 17,
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     uint8_t* gen_tptr = smem_raw + (tptr - base);
     int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
     uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [warps][16][34] (Ĝ < 65536)
-    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);   // [warps][32] edge-list bases
-    int32_t* s_tpre = s_eb + MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
+    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);   // [2][warps][32] edge-list bases
+    int32_t* s_tpre = s_eb + 2 * MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
     int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
     const bool table = batch <= MMA_TABLE_PAIRS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -297,23 +297,44 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         TileCursor cur;
         cur.TN = TN;
         TableCursor tc{s_tpre, s_th, TN};
-        int lt = 0;
+        auto locate = [&](int gq, int* pp, int* rbp, int* cbp, int* hp) {
+            return table ? tc.locate(batch, gq, pp, rbp, cbp, hp) : cur.locate(ws, batch, gq, pp, rbp, cbp, hp);
+        };
+        // per-tile metadata, double buffered (index acc): heavy ids of the tile's columns (s_hl) and the
+        // edge-list base of each row (s_eb); tile t+1's are loaded while tile t is drained
         int p, rb, cb, h;
-        for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
-             g += gridDim.x, ++lt) {
-            const int acc = lt & 1;
-            int32_t* hl = s_hl + acc * MMA_BN;
+        int g = blockIdx.x;
+        bool have = locate(g, &p, &rb, &cb, &h);
+        if (have) {
             const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
-            for (int k = et; k < MMA_BN; k += 32 * MMA_EPI_WARPS) {
-                const int b = cb * TN + k;
-                hl[k] = (k < TN && b < h) ? __ldg(hlist + b) : -1;
+            if (et < MMA_BN) s_hl[et] = (et < TN && cb * TN + et < h) ? __ldg(hlist + cb * TN + et) : -1;
+            const int a = rb * MMA_BM + q * 32 + lane;
+            s_eb[ew * 32 + lane] = a < h ? __ldg(ws.rowptr + p * ws.rp_stride + __ldg(hlist + a)) : -1;
+        }
+        named_bar(1, 32 * MMA_EPI_WARPS);
+        for (int lt = 0; have; ++lt) {
+            const int acc = lt & 1;
+            const int32_t* hl = s_hl + acc * MMA_BN;
+            const int32_t* ebuf = s_eb + acc * (MMA_EPI_WARPS * 32);
+            int pn, rbn, cbn, hn;
+            const bool next = locate(g + gridDim.x, &pn, &rbn, &cbn, &hn);
+            int hl_n = -1, ja_n = -1, eb_n = -1;
+            if (next) {
+                const int32_t* hln = ws.heavy_list + pn * ws.heavy_cap;
+                if (et < MMA_BN && et < TN && cbn * TN + et < hn) hl_n = __ldg(hln + cbn * TN + et);
+                const int an = rbn * MMA_BM + q * 32 + lane;
+                if (an < hn) ja_n = __ldg(hln + an);
+                const int c0 = cbn * TN, c1 = min(hn, c0 + TN) - 1;
+                if (sub == 0 && an < min(hn, c1)) {  // L2 prefetch of the next tile's (U word, prefix) row segment
+                    const int64_t Wn = ws.desc[pn].W;
+                    const int64_t w0 = __ldg(hln + c0) >> 5, w1 = __ldg(hln + c1) >> 5;
+                    const int64_t s0 = ((an * Wn + w0) * 8) & ~15ll, e0 = ((an * Wn + w1 + 1) * 8 + 15) & ~15ll;
+                    const char* upn = reinterpret_cast<const char*>(ws.heavy_UP + pn * ws.heavy_UP_stride);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(upn + s0), "r"((uint32_t)(e0 - s0))
+                                 : "memory");
+                }
             }
-            named_bar(1, 32 * MMA_EPI_WARPS);  // heavy ids of this tile's columns visible to all epilogue warps
-            const int a = rb * MMA_BM + q * 32 + lane;  // this thread's TMEM lane = output row
             const int W = ws.desc[p].W;
-            const bool arow = a < h;
-            const int ja = arow ? __ldg(hlist + a) : 0;
-            s_eb[ew * 32 + lane] = arow ? __ldg(ws.rowptr + p * ws.rp_stride + ja) : -1;
             const uint2* up0 = ws.heavy_UP + p * ws.heavy_UP_stride;
             uint32_t* edges = ws.edges + p * ws.edges_stride;
             asm("" : "+l"(edges));  // keep the base in registers (ptxas otherwise recomputes it per store)
@@ -373,13 +394,21 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
 #pragma unroll
                     for (int r = 0; r < 16; ++r) {
                         const uint32_t x = u[r].x;
-                        const uint32_t slot = (uint32_t)(s_eb[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
+                        const uint32_t slot = (uint32_t)(ebuf[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
                         if (rh + r < lim && (x & bit)) edges[slot] = jhi | vt[r * 34 + lane];
                     }
                 }
                 __syncwarp();
+                if (c == sub && ja_n >= 0) eb_n = __ldg(ws.rowptr + pn * ws.rp_stride + ja_n);
             }
-            named_bar(1, 32 * MMA_EPI_WARPS);  // everyone done with hl[acc] before it is refilled two tiles later
+            if (next) {  // tile t+1's metadata into the other buffer (its last readers finished at tile t-1's barrier)
+                if (et < MMA_BN) s_hl[(acc ^ 1) * MMA_BN + et] = hl_n;
+                s_eb[(acc ^ 1) * (MMA_EPI_WARPS * 32) + ew * 32 + lane] = eb_n;
+            }
+            named_bar(1, 32 * MMA_EPI_WARPS);  // visible to all epilogue warps; buffer acc free for tile t+2
+            g += gridDim.x;
+            p = pn, rb = rbn, cb = cbn, h = hn;
+            have = next;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
