@@ -35,6 +35,7 @@ CFG = synth.CONFIGS["E"]
 PAIRS_PER_GPU = 203  # ceil(1623 / 8): the 3DMatch pair count split over the 8-GPU box
 L2_FLUSH_BYTES = 256 << 20
 SMS = 148
+MMA_FP4 = 1  # dense SC^2 block as tcgen05.mma kind::mxf4 (the library default); 0 = kind::i8
 
 
 def peaks():
@@ -125,10 +126,11 @@ def algorithmic_work(tr, res, pairs):
         n, W, h = st["n"], st["W"], st["heavy_h"]
         tests += n * (n - 1) // 2
         edges += st["edges"]
-        if h:
-            hp = -(-h // 256) * 256
-            tiles = sum(hp // 256 - rb // 2 for rb in range(hp // 128))
-            mma_ops += tiles * 2 * 128 * 256 * 32 * W
+        if h:  # upper 128 x TN tiles (k_sc2_mma: cb >= rb*128 // TN), K = 32W
+            tn = 240 if MMA_FP4 else 256
+            cbs = -(-h // tn)
+            tiles = sum(cbs - rb * 128 // tn for rb in range(-(-h // 128)))
+            mma_ops += tiles * 2 * 128 * tn * 32 * W
     score_tests = int(sum(int(r["hypotheses_evaluated"]) for r in res)) * CFG.n
     return {"compat_tests": tests, "mma_ops": mma_ops, "score_tests": score_tests, "edges": edges}
 
@@ -137,7 +139,8 @@ def rooflines(kern, work, steps, pk, pairs):
     """Per-kernel roofline entries (achieved algorithmic rate ÷ peak) from CUDA-event kernel times."""
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     fp32_peak = SMS * 128 * sm_max * 1e6 / 1e12  # Tops/s, one fp32 op per lane per clock
-    int8_peak = 2.0 * float(pk.get("bf16_tflops", 1590.0))  # guide's nominal int8/bf16 ratio 4.5/2.25
+    # dense-block peak from the measured bf16 figure x the guide's nominal ratio: fp4 9/2.25, int8 4.5/2.25
+    mma_peak = (4.0 if MMA_FP4 else 2.0) * float(pk.get("bf16_tflops", 1590.0))
     out = {}
 
     def entry(name, bound, units, peak, unit, per_unit):
@@ -154,8 +157,8 @@ def rooflines(kern, work, steps, pk, pairs):
 
     entry("k_compat", "alu", work["compat_tests"] * 20, fp32_peak, "Tops/s (fp32)",
           "20 fp32 ops of the Eq. 1 tree per pair test; N(N-1)/2 tests per pair")
-    entry("k_sc2_mma", "tensor", work["mma_ops"], int8_peak, "TOPS (int8)",
-          "2*128*256*K ops per upper MMA tile of the dense block, K = 32W")
+    entry("k_sc2_mma", "tensor", work["mma_ops"], mma_peak, "TOPS (fp4 e2m1)" if MMA_FP4 else "TOPS (int8)",
+          "2*128*TN*K ops per upper MMA tile of the dense block, K = 32W, TN = %d" % (240 if MMA_FP4 else 256))
     entry("k_score", "alu", work["score_tests"] * 24, 2 * fp32_peak, "TFLOP/s (fp32, FMA = 2)",
           "24 flops per residual test (12 FMA-equivalents); hypotheses x N tests per pair")
     return out
@@ -234,6 +237,7 @@ def run_cuda(args, rank, world, local_rank):
     torch.cuda.set_stream(stream)
     tr = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=pairs, device=local_rank,
                   kernel_timing=True)
+    tr.set_option("mma_fp4", MMA_FP4)  # the library default, stated so the roofline below counts the right tiles
 
     def step():
         tr.register_batch(src_d, dst_d, off, nn, out=out_d, stream=stream.cuda_stream)

@@ -173,8 +173,8 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *                      copy overlapping the previous sub-batch's compatibility pass (default); 0 = one copy
  *                      before one launch sequence
  *   "mma_fp4"          1 = run the dense block as kind::mxf4.block_scale on packed e2m1 operands (unit block
- *                      scales, fp32 accumulate; exact) with 128x240 tiles; 0 = kind::i8 (default: faster end to
- *                      end because the epilogue's edge emission bounds the fp4 kernel)
+ *                      scales, fp32 accumulate; exact below 2^24) with 128x240 tiles (default); 0 = kind::i8
+ *                      with 128x256 tiles (same results)
  *   "sc2_chunks"       32-word chunks of a dense row per SC^2 work item: 0 = auto (whole rows for batches
  *                      >= 32 pairs, single chunks below), 1..64 fixed
  *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1

@@ -111,7 +111,7 @@ struct turboreg_ctx {
     int32_t heavy_cap_alloc = 0;
     CUtensorMap tmX, tmX4;  // X as uint8 rows / as packed e2m1 rows (half the bytes)
     bool tmX_ok = false, tmX4_ok = false;
-    int32_t opt_mma_fp4 = 0;  // block-scaled fp4 block: 1.65x faster contraction, but the edge emission then bounds it
+    int32_t opt_mma_fp4 = 1;  // block-scaled fp4 dense block (default); 0 = kind::i8
     int32_t opt_compat_variant = 0, opt_sc2_path = 0, opt_heavy_min_rows = 128, opt_heavy_min_deg = 32, opt_heavy_cap = 0;
     int num_sms = 148;
     int32_t opt_score_pairs = 2;
