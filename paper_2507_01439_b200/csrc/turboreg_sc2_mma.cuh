@@ -293,35 +293,41 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         const int sub = ew >> 2;
         constexpr int NCH = MMA_BN / 32;
         const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
-        const int et = threadIdx.x - 64;  // 0..255
         TileCursor cur;
         cur.TN = TN;
         TableCursor tc{s_tpre, s_th, TN};
         auto locate = [&](int gq, int* pp, int* rbp, int* cbp, int* hp) {
             return table ? tc.locate(batch, gq, pp, rbp, cbp, hp) : cur.locate(ws, batch, gq, pp, rbp, cbp, hp);
         };
-        // per-tile metadata, double buffered (index acc): heavy ids of the tile's columns (s_hl) and the
-        // edge-list base of each row (s_eb); tile t+1's are loaded while tile t is drained
+        // per-warp tile metadata in registers (no block barrier between tiles): the heavy ids of this warp's
+        // columns (lane = column of chunks sub and sub + MMA_EPI_SUB) and its rows' edge-list bases (lane =
+        // row, in this warp's shared-memory slot); tile t+1's are loaded while tile t is drained
+        static_assert(MMA_BN / 32 == 2 * MMA_EPI_SUB, "two chunks per epilogue warp");
+        auto col_id = [&](const int32_t* hlq, int cbq, int hq, int c) {
+            const int k = c * 32 + lane;
+            return (k < TN && cbq * TN + k < hq) ? __ldg(hlq + cbq * TN + k) : -1;
+        };
         int p, rb, cb, h;
         int g = blockIdx.x;
         bool have = locate(g, &p, &rb, &cb, &h);
+        int jb0 = -1, jb1 = -1;
         if (have) {
             const int32_t* hlist = ws.heavy_list + p * ws.heavy_cap;
-            if (et < MMA_BN) s_hl[et] = (et < TN && cb * TN + et < h) ? __ldg(hlist + cb * TN + et) : -1;
+            jb0 = col_id(hlist, cb, h, sub);
+            jb1 = col_id(hlist, cb, h, sub + MMA_EPI_SUB);
             const int a = rb * MMA_BM + q * 32 + lane;
             s_eb[ew * 32 + lane] = a < h ? __ldg(ws.rowptr + p * ws.rp_stride + __ldg(hlist + a)) : -1;
         }
-        named_bar(1, 32 * MMA_EPI_WARPS);
+        __syncwarp();
         for (int lt = 0; have; ++lt) {
             const int acc = lt & 1;
-            const int32_t* hl = s_hl + acc * MMA_BN;
-            const int32_t* ebuf = s_eb + acc * (MMA_EPI_WARPS * 32);
             int pn, rbn, cbn, hn;
             const bool next = locate(g + gridDim.x, &pn, &rbn, &cbn, &hn);
-            int hl_n = -1, ja_n = -1, eb_n = -1;
+            int jbn0 = -1, jbn1 = -1, ja_n = -1, eb_n = -1;
             if (next) {
                 const int32_t* hln = ws.heavy_list + pn * ws.heavy_cap;
-                if (et < MMA_BN && et < TN && cbn * TN + et < hn) hl_n = __ldg(hln + cbn * TN + et);
+                jbn0 = col_id(hln, cbn, hn, sub);
+                jbn1 = col_id(hln, cbn, hn, sub + MMA_EPI_SUB);
                 const int an = rbn * MMA_BM + q * 32 + lane;
                 if (an < hn) ja_n = __ldg(hln + an);
                 const int c0 = cbn * TN, c1 = min(hn, c0 + TN) - 1;
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 // transpose through shared memory: afterwards lane = column, loop over the warp's 32 rows, so
                 // the UP reads and edge stores of one row are coalesced
                 const int b = bt + c * 32 + lane;
-                const int jb = hl[c * 32 + lane];
+                const int jb = (c == sub) ? jb0 : jb1;
                 const uint32_t bit = 1u << (jb & 31);
                 const uint32_t jhi = (uint32_t)jb << 16, bm1 = bit - 1u;
                 const int a0 = rb * MMA_BM + q * 32;
@@ -394,20 +400,18 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
 #pragma unroll
                     for (int r = 0; r < 16; ++r) {
                         const uint32_t x = u[r].x;
-                        const uint32_t slot = (uint32_t)(ebuf[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
+                        const uint32_t slot = (uint32_t)(s_eb[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
                         if (rh + r < lim && (x & bit)) edges[slot] = jhi | vt[r * 34 + lane];
                     }
                 }
                 __syncwarp();
                 if (c == sub && ja_n >= 0) eb_n = __ldg(ws.rowptr + pn * ws.rp_stride + ja_n);
             }
-            if (next) {  // tile t+1's metadata into the other buffer (its last readers finished at tile t-1's barrier)
-                if (et < MMA_BN) s_hl[(acc ^ 1) * MMA_BN + et] = hl_n;
-                s_eb[(acc ^ 1) * (MMA_EPI_WARPS * 32) + ew * 32 + lane] = eb_n;
-            }
-            named_bar(1, 32 * MMA_EPI_WARPS);  // visible to all epilogue warps; buffer acc free for tile t+2
             g += gridDim.x;
             p = pn, rb = rbn, cb = cbn, h = hn;
+            jb0 = jbn0, jb1 = jbn1;
+            s_eb[ew * 32 + lane] = eb_n;  // private to this warp: its reads of tile t are done
+            __syncwarp();
             have = next;
         }
     }
