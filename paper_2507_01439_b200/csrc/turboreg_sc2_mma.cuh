@@ -385,9 +385,14 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                         uint32_t* vr = reinterpret_cast<uint32_t*>(vt + (lane & 15) * 34);
 #pragma unroll
                         for (int k = 0; k < 32; k += 2) {
-                            const uint32_t lo = FP4 ? (uint32_t)__uint_as_float(v[k]) : v[k];
-                            const uint32_t hi = FP4 ? (uint32_t)__uint_as_float(v[k + 1]) : v[k + 1];
-                            vr[k >> 1] = (lo & 0xffffu) | (hi << 16);
+                            uint32_t lo = v[k], hi = v[k + 1];
+                            if constexpr (FP4) {  // exact integer-valued fp32 (< 2^23): + 2^23 puts it in the low mantissa bits
+                                unsigned long long pr2 = (unsigned long long)lo | ((unsigned long long)hi << 32);
+                                asm("add.rn.f32x2 %0, %0, %1;" : "+l"(pr2) : "l"(0x4b0000004b000000ull));
+                                lo = (uint32_t)pr2;
+                                hi = (uint32_t)(pr2 >> 32);
+                            }
+                            vr[k >> 1] = __byte_perm(lo, hi, 0x5410);  // low halves of both
                         }
                     }
                     __syncwarp();
