@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     int32_t* s_tpre = s_eb + 2 * MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
     int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
     const bool table = batch <= MMA_TABLE_PAIRS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp: provably uniform
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < MMA_STAGES; ++s) {
