@@ -253,8 +253,8 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
             const f2_t D = f2_fma(B, mone, A);
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t nTq = f2_mul(f2_add(absD, kap2), f2_mul(S, nc19));
-            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
+            // |q| − Tq with one rounding: the sign is exactly that of |q| − fl(|D| + κ)·S·2^-19
+            const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
             const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
             const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
@@ -359,8 +359,8 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
             const f2_t D = f2_fma(B, mone, A);
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
-            const f2_t nTq = f2_mul(f2_add(absD, kap2), f2_mul(S, nc19));
-            const f2_t b = f2_add(nTq, q & 0x7fffffff7fffffffull);  // |q| − Tq
+            // |q| − Tq with one rounding: the sign is exactly that of |q| − fl(|D| + κ)·S·2^-19
+            const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
             const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
             const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
