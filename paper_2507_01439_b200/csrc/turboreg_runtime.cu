@@ -389,8 +389,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         CK(L.run(KID_COMPAT, [&] {
             const dim3 g((unsigned)(bpp * split), B);
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws, split);
-            else if (c->opt_compat_variant == 1) trk::k_compat<false, 4, 8, 1><<<g, 256, 0, s>>>(ws, split);
-            else if (c->opt_compat_variant == 2) trk::k_compat<false, 4, 16, -1><<<g, 256, 0, s>>>(ws, split);
+            else if (c->opt_compat_variant == 1) trk::k_compat<false, 5, 16, 1><<<g, 256, 0, s>>>(ws, split);
+            else if (c->opt_compat_variant == 2) trk::k_compat<false, 5, 16, -1><<<g, 256, 0, s>>>(ws, split);
             else trk::k_compat<false, 5, 16, -2><<<g, 256, 0, s>>>(ws, split);
         }));
     }
