@@ -6,6 +6,7 @@ import oracle
 import synth
 from tests.gpu_compare import compare_pair, rot_angle_rad
 from tests.helpers import py_triangles
+from paper_2507_01439_b200._binding import I_STATE
 
 pytestmark = pytest.mark.gpu
 
@@ -336,6 +337,30 @@ def test_heavy_block_batch_mixed(tr_mod):
         if sizes[p] >= 3:
             r = {k: res[p][k] for k in res.dtype.names}
             compare_pair(tr, p, srcs[p], dsts[p], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+
+
+def test_heavy_block_batch_beyond_smem_table(tr_mod):
+    # batches larger than the tensor-core kernel's shared-memory tile table (1024 pairs) walk the per-pair
+    # state in global memory instead; every pair's result must equal the all-popcount path's, and sampled
+    # pairs on both sides of pair 1024 must equal the oracle
+    cfg = synth.CONFIGS["B"]
+    pairs, nn = 1100, 400
+    insts = [synth.workload_instance(cfg, pair=2000 + p, n=nn) for p in range(pairs)]
+    src = np.concatenate([x["src"] for x in insts])
+    dst = np.concatenate([x["dst"] for x in insts])
+    off = np.arange(pairs, dtype=np.int64) * nn
+    n = np.full(pairs, nn, np.int32)
+    tc = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn, max_batch=pairs)
+    tc.set_option("heavy_min_rows", 1)
+    pc = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn, max_batch=pairs)
+    pc.set_option("sc2_path", 1)
+    rt = tc.register_batch(src, dst, off, n)
+    rp = pc.register_batch(src, dst, off, n)
+    assert rt.tobytes() == rp.tobytes()
+    assert int(tc.intermediate(pairs - 1, I_STATE)["heavy_h"]) > 0  # the tensor-core block ran
+    for p in (3, 1023, 1024, pairs - 1):
+        r = {k: rt[p][k] for k in rt.dtype.names}
+        compare_pair(tc, p, insts[p]["src"], insts[p]["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
 
 
 def test_graph_replay_matches_direct_launches(tr_mod):
