@@ -289,8 +289,11 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
 
 // Row classes for the SC^2 assembly: sparse rows (a list, not heavy) go to k_sc2_light, the rest to k_sc2.
 __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
-    __shared__ int s_w[32];
-    __shared__ int s_carry;
+    // one pass, 4 consecutive rows per thread (all loads issued up front): a block scan of (light flag,
+    // upper degree) gives both the light/dense lists and the CSR row pointers
+    constexpr int RPT = 4;
+    __shared__ int s_wf[32], s_wu[32];
+    __shared__ int s_cf, s_cu;
     const int p = blockIdx.x;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -298,60 +301,65 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int32_t* deg = ws.deg_full + p * ws.row_stride;
     const int32_t* hpos = ws.hpos + p * ws.row_stride;
+    const int32_t* udeg = ws.deg + p * ws.row_stride;
     int32_t* L = ws.light_list + p * ws.row_stride;
     int32_t* Dn = ws.dense_list + p * ws.row_stride;
-    if (t == 0) s_carry = 0;
-    __syncthreads();
-    for (int r0 = 0; r0 < n; r0 += 1024) {
-        const int i = r0 + t;
-        const int f = (i < n && hpos[i] < 0 && deg[i] <= LIST_MAX) ? 1 : 0;
-        int x = warp_incl_scan(f);
-        if (lane == 31) s_w[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            int y = s_w[lane];
-            int yi = warp_incl_scan(y);
-            s_w[lane] = yi - y;
-        }
-        __syncthreads();
-        const int pos = s_carry + s_w[warp] + x - f;
-        if (i < n) {
-            if (f) L[pos] = i;
-            else Dn[i - pos] = i;
-        }
-        const unsigned fb = __ballot_sync(FULL, f);
-        if (lane == 0 && ((r0 + warp * 32) >> 5) < d.W)
-            ws.light_mask[p * (ws.bits_stride / ws.row_stride) + ((r0 + warp * 32) >> 5)] = fb;
-        __syncthreads();
-        if (t == 1023) s_carry = pos + f;
-        __syncthreads();
-    }
-    if (t == 0) { ws.st[p].n_light = s_carry; ws.st[p].n_dense = n - s_carry; }
-    // compact CSR row pointers of the O2 edge lists: exclusive scan of the upper degrees
-    __syncthreads();
-    if (t == 0) s_carry = 0;
-    __syncthreads();
-    const int32_t* udeg = ws.deg + p * ws.row_stride;
     int32_t* rp = ws.rowptr + p * ws.rp_stride;
-    for (int r0 = 0; r0 < n; r0 += 1024) {
-        const int i = r0 + t;
-        const int f = (i < n) ? udeg[i] : 0;
-        int x = warp_incl_scan(f);
-        if (lane == 31) s_w[warp] = x;
+    uint32_t* lmask = ws.light_mask + p * (ws.bits_stride / ws.row_stride);
+    if (t == 0) s_cf = s_cu = 0;
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += 1024 * RPT) {
+        const int ib = r0 + t * RPT;
+        int fl[RPT], ud[RPT], fs = 0, us = 0;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int i = ib + k;
+            fl[k] = (i < n && hpos[i] < 0 && deg[i] <= LIST_MAX) ? 1 : 0;
+            ud[k] = i < n ? udeg[i] : 0;
+            fs += fl[k];
+            us += ud[k];
+        }
+        const int xf = warp_incl_scan(fs), xu = warp_incl_scan(us);
+        if (lane == 31) { s_wf[warp] = xf; s_wu[warp] = xu; }
         __syncthreads();
         if (warp == 0) {
-            int y = s_w[lane];
-            int yi = warp_incl_scan(y);
-            s_w[lane] = yi - y;
+            const int yf = s_wf[lane], yu = s_wu[lane];
+            const int zf = warp_incl_scan(yf), zu = warp_incl_scan(yu);
+            s_wf[lane] = zf - yf;
+            s_wu[lane] = zu - yu;
         }
         __syncthreads();
-        const int pos = s_carry + s_w[warp] + x - f;
-        if (i < n) rp[i] = pos;
+        int pf = s_cf + s_wf[warp] + xf - fs, pu = s_cu + s_wu[warp] + xu - us;
+        uint32_t nib = 0;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int i = ib + k;
+            if (i < n) {
+                if (fl[k]) L[pf] = i;
+                else Dn[i - pf] = i;
+                rp[i] = pu;
+            }
+            pf += fl[k];
+            pu += ud[k];
+            nib |= (uint32_t)fl[k] << k;
+        }
+        // light-row bitset: 8 threads x 4 rows = one 32-bit word
+        uint32_t wbits = nib << (RPT * (lane & 7));
+        wbits |= __shfl_xor_sync(FULL, wbits, 1);
+        wbits |= __shfl_xor_sync(FULL, wbits, 2);
+        wbits |= __shfl_xor_sync(FULL, wbits, 4);
+        const int w = ib >> 5;
+        if ((lane & 7) == 0 && w < d.W) lmask[w] = wbits;  // words past n (up to W) are written as 0
         __syncthreads();
-        if (t == 1023) s_carry = pos + f;
+        if (t == 1023) { s_cf = pf; s_cu = pu; }
         __syncthreads();
     }
-    if (t == 0) { rp[n] = s_carry; ws.st[p].edges = s_carry; }
+    if (t == 0) {
+        ws.st[p].n_light = s_cf;
+        ws.st[p].n_dense = n - s_cf;
+        rp[n] = s_cu;
+        ws.st[p].edges = s_cu;
+    }
 }
 
 // SC^2 edges of the sparse rows, packed for full lanes: a warp takes LG sparse rows (bitmaps and lists
