@@ -726,6 +726,9 @@ __global__ void __launch_bounds__(256, 5) k_degree(WS ws) {
 // |H| <= heavy_cap; |H| < heavy_min_rows ⇒ no tensor-core block.  Ordered compaction (H in index order, so
 // i < j ⇔ hpos(i) < hpos(j)).
 __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
+    // rows 0 .. 8191 are held in registers (8 consecutive rows per thread, loaded once for every count and
+    // the compaction); longer rows' tails are re-read
+    constexpr int RC = 8, NC = 1024 * RC;
     __shared__ int s_w[32];
     __shared__ int s_carry, s_cnt;
     const int p = blockIdx.x;
@@ -736,11 +739,16 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int32_t* deg = ws.deg_full + p * ws.row_stride;
     int32_t* hpos = ws.hpos + p * ws.row_stride;
+    int dv[RC];
+#pragma unroll
+    for (int k = 0; k < RC; ++k) dv[k] = (t * RC + k < n) ? deg[t * RC + k] : -1;
     auto count_ge = [&](int th) {  // #rows with degree >= th (block-wide)
         if (t == 0) s_cnt = 0;
         __syncthreads();
         int c = 0;
-        for (int i = t; i < n; i += 1024) c += deg[i] >= th;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) c += dv[k] >= th;
+        for (int i = NC + t; i < n; i += 1024) c += deg[i] >= th;
         c = __reduce_add_sync(FULL, (unsigned)c);
         if (lane == 0 && c) atomicAdd(&s_cnt, c);
         __syncthreads();
@@ -765,22 +773,46 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     {
         const int thr2 = max(ws.heavy_min_deg, LIST_MAX + 1);
         if (thr2 < thr) {
-            if (t == 0) s_cnt = 0;
-            __syncthreads();
-            int c = 0;
-            for (int i = t; i < n; i += 1024) c += deg[i] >= thr2;
-            c = __reduce_add_sync(FULL, (unsigned)c);
-            if (lane == 0 && c) atomicAdd(&s_cnt, c);
-            __syncthreads();
-            const int cnt2 = s_cnt;
-            __syncthreads();
+            const int cnt2 = count_ge(thr2);
             if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
         }
     }
     const bool use = ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
     if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; }
-    __syncthreads();
-    for (int r0 = 0; r0 < n; r0 += 1024) {
+    int32_t* hl = ws.heavy_list + p * ws.heavy_cap;
+    uint32_t* hmask = ws.heavy_mask + p * (ws.bits_stride / ws.row_stride);
+    // ordered compaction of the register-held rows: block scan of the per-thread counts
+    {
+        int fs = 0;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) fs += (use && dv[k] >= thr) ? 1 : 0;
+        const int x = warp_incl_scan(fs);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const int y = s_w[lane];
+            s_w[lane] = warp_incl_scan(y) - y;
+        }
+        __syncthreads();
+        int pos = s_w[warp] + x - fs;
+        uint32_t byte = 0;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) {
+            const int i = t * RC + k;
+            const bool f = use && dv[k] >= thr;
+            if (i < n) hpos[i] = f ? pos : -1;
+            if (f) hl[pos++] = i;
+            byte |= (uint32_t)f << k;
+        }
+        uint32_t wbits = byte << (RC * (lane & 3));  // 4 threads x 8 rows = one 32-bit word
+        wbits |= __shfl_xor_sync(FULL, wbits, 1);
+        wbits |= __shfl_xor_sync(FULL, wbits, 2);
+        const int w = (t * RC) >> 5;
+        if ((lane & 3) == 0 && w < d.W) hmask[w] = wbits;
+        if (t == 1023) s_carry = pos;
+        __syncthreads();
+    }
+    for (int r0 = NC; r0 < n; r0 += 1024) {
         const int i = r0 + t;
         const int f = (use && i < n && deg[i] >= thr) ? 1 : 0;
         int x = warp_incl_scan(f);
@@ -794,11 +826,11 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
         __syncthreads();
         const int pos = s_carry + s_w[warp] + x - f;
         if (i < n) hpos[i] = f ? pos : -1;
-        if (f) ws.heavy_list[p * ws.heavy_cap + pos] = i;
+        if (f) hl[pos] = i;
         const unsigned fb = __ballot_sync(FULL, f);
         if (lane == 0) {
             const int wi = (r0 + warp * 32) >> 5;
-            if (wi < d.W) ws.heavy_mask[p * (ws.bits_stride / ws.row_stride) + wi] = fb;
+            if (wi < d.W) hmask[wi] = fb;
         }
         __syncthreads();
         if (t == 1023) s_carry = pos + f;
