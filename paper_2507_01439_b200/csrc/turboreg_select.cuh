@@ -149,22 +149,53 @@ __global__ void __launch_bounds__(1024) k_pivot_sort(WS ws) {
         if (threadIdx.x == 0) st->cand_overflow = 1;
         return;
     }
-    int m2 = 1;
+    int m2 = 64;
     while (m2 < m) m2 <<= 1;
     const unsigned long long* cand = ws.cand + (int64_t)p * PIV_CAP;
     for (int k = threadIdx.x; k < m2; k += blockDim.x) s_key[k] = (k < m) ? cand[k] : ~0ull;
     __syncthreads();
-    for (int size = 2; size <= m2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int k = threadIdx.x; k < m2 / 2; k += blockDim.x) {
-                const int lo = 2 * k - (k & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const unsigned long long a = s_key[lo], b = s_key[hi];
-                if ((a > b) == up) { s_key[lo] = b; s_key[hi] = a; }
+    // bitonic sort; for m2 <= 2048 each warp holds 64 consecutive keys in registers (lane: keys base + lane
+    // and base + lane + 32), so strides <= 32 run on shuffles and only strides >= 64 go through shared memory
+    auto smem_stage = [&](int size, int stride) {
+        for (int k = threadIdx.x; k < m2 / 2; k += blockDim.x) {
+            const int lo = 2 * k - (k & (stride - 1));
+            const int hi = lo + stride;
+            const bool up = (lo & size) == 0;
+            const unsigned long long a = s_key[lo], b = s_key[hi];
+            if ((a > b) == up) { s_key[lo] = b; s_key[hi] = a; }
+        }
+        __syncthreads();
+    };
+    if (m2 <= 2048) {
+        const int lane = threadIdx.x & 31, base = 64 * (threadIdx.x >> 5);
+        const bool act = base < m2;
+        const int ea = base + lane, eb = ea + 32;
+        unsigned long long a = ~0ull, b = ~0ull;
+        auto reg_stages = [&](int size) {  // strides min(size/2, 32) .. 1 of one bitonic merge step
+            for (int stride = min(size >> 1, 32); stride > 0; stride >>= 1) {
+                if (stride == 32) {
+                    if ((a > b) == ((ea & size) == 0)) { const unsigned long long x = a; a = b; b = x; }
+                } else {
+                    const unsigned long long pa = __shfl_xor_sync(FULL, a, stride), pb = __shfl_xor_sync(FULL, b, stride);
+                    a = (((ea & stride) == 0) == ((ea & size) == 0)) ? min(a, pa) : max(a, pa);
+                    b = (((eb & stride) == 0) == ((eb & size) == 0)) ? min(b, pb) : max(b, pb);
+                }
             }
+        };
+        if (act) { a = s_key[ea]; b = s_key[eb]; }
+        for (int size = 2; size <= 64; size <<= 1) reg_stages(size);
+        if (act) { s_key[ea] = a; s_key[eb] = b; }
+        __syncthreads();
+        for (int size = 128; size <= m2; size <<= 1) {
+            for (int stride = size >> 1; stride >= 64; stride >>= 1) smem_stage(size, stride);
+            if (act) { a = s_key[ea]; b = s_key[eb]; }
+            reg_stages(size);
+            if (act) { s_key[ea] = a; s_key[eb] = b; }
             __syncthreads();
         }
+    } else {
+        for (int size = 2; size <= m2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) smem_stage(size, stride);
     }
     // keys are ((0x7fff - w) << 30 | edge position): the row of a winner comes from a binary search of its
     // position in rowptr (staged in shared memory when it fits), j from the edge word
