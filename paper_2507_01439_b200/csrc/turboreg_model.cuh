@@ -346,9 +346,9 @@ struct DevResult {  // mirrors turboreg_result
     int64_t num_edges;
 };
 
-__global__ void __launch_bounds__(256) k_finalize(WS ws) {
-    __shared__ unsigned long long s_red[8];
-    __shared__ int s_cnt[2][8];
+__global__ void __launch_bounds__(1024) k_finalize(WS ws) {
+    __shared__ unsigned long long s_red[32];
+    __shared__ int s_cnt[2][32];
     const int q = blockIdx.x;
     const PairDesc d = ws.desc[q];
     const PairState* st = ws.st + q;
@@ -362,9 +362,9 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     // ties below, as in the oracle's scan of the canonical list
     const int rank = ws.err_mode >> 1;
     const double2* he = ws.herr + q * ws.cl_stride;
-    auto key_of = [&](int s, const float* h) -> unsigned long long {
-        if (rank == 0)
-            return ((unsigned long long)(unsigned)__float_as_int(h[12]) << 17) | (unsigned)__float_as_int(h[14]);
+    auto quad = [&](int s) { return *reinterpret_cast<const int4*>(hyp + (int64_t)s * 16 + 12); };  // count, flag, S
+    auto key_of = [&](int s, const int4 h) -> unsigned long long {
+        if (rank == 0) return ((unsigned long long)(unsigned)h.x << 17) | (unsigned)h.z;
         const double e = rank == 1 ? he[s].x : he[s].y;
         return ~(unsigned long long)__double_as_longlong(e);
     };
@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     int ncl = 0, nev = 0;
     if (d.n > 0) {
         for (int s = t; s < K; s += blockDim.x) {
-            const float* h = hyp + (int64_t)s * 16;
-            const int flag = __float_as_int(h[13]);
+            const int4 h = quad(s);
+            const int flag = h.y;
             if (flag != 2) ++ncl;
             if (flag == 0) {
                 ++nev;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     if (t == 0) {
         unsigned long long b = 0ull;
         int a = 0, e = 0;
-        for (int w = 0; w < 8; ++w) { b = s_red[w] > b ? s_red[w] : b; a += s_cnt[0][w]; e += s_cnt[1][w]; }
+        for (int w = 0; w < 32; ++w) { b = s_red[w] > b ? s_red[w] : b; a += s_cnt[0][w]; e += s_cnt[1][w]; }
         s_red[0] = b; s_cnt[0][0] = a; s_cnt[1][0] = e;
     }
     __syncthreads();
@@ -403,15 +403,15 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
         int ms = -1;
         if (d.n > 0 && nev > 0)
             for (int s = t; s < K; s += blockDim.x) {
-                const float* h = hyp + (int64_t)s * 16;
-                if (__float_as_int(h[13]) == 0 && key_of(s, h) == best1) ms = max(ms, __float_as_int(h[14]));
+                const int4 h = quad(s);
+                if (h.y == 0 && key_of(s, h) == best1) ms = max(ms, h.z);
             }
         ms = (int)__reduce_max_sync(FULL, (unsigned)(ms + 1)) - 1;
         if (lane == 0) s_cnt[0][warp] = ms;
         __syncthreads();
         if (t == 0) {
             int m = -1;
-            for (int w = 0; w < 8; ++w) m = max(m, s_cnt[0][w]);
+            for (int w = 0; w < 32; ++w) m = max(m, s_cnt[0][w]);
             s_cnt[0][0] = m;
         }
         __syncthreads();
@@ -421,11 +421,11 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     unsigned long long bestt = ~0ull;
     if (d.n > 0 && nev > 0) {
         for (int s = t; s < K; s += blockDim.x) {
-            const float* h = hyp + (int64_t)s * 16;
-            if (__float_as_int(h[13]) != 0) continue;
+            const int4 h = quad(s);
+            if (h.y != 0) continue;
             const unsigned long long key = key_of(s, h);
             if (key != best1) continue;
-            if (rank != 0 && __float_as_int(h[14]) != bestS) continue;
+            if (rank != 0 && h.z != bestS) continue;
             const int4 c = cl[s];
             const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
             if (tk < bestt) bestt = tk;
@@ -438,15 +438,16 @@ __global__ void __launch_bounds__(256) k_finalize(WS ws) {
     __syncthreads();
     if (t == 0) {
         unsigned long long b = ~0ull;
-        for (int w = 0; w < 8; ++w) b = s_red[w] < b ? s_red[w] : b;
+        for (int w = 0; w < 32; ++w) b = s_red[w] < b ? s_red[w] : b;
         s_red[0] = b;
     }
     __syncthreads();
     bestt = s_red[0];
     if (bestt != ~0ull) {  // the slot holding the winning triple (duplicates carry identical values)
         for (int s = t; s < K; s += blockDim.x) {
-            if (__float_as_int(hyp[(int64_t)s * 16 + 13]) != 0) continue;
-            if (key_of(s, hyp + (int64_t)s * 16) != best1) continue;
+            const int4 h = quad(s);
+            if (h.y != 0) continue;
+            if (key_of(s, h) != best1) continue;
             const int4 c = cl[s];
             const unsigned long long tk = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | c.z;
             if (tk == bestt) atomicMin(&s_slot, s);

@@ -510,7 +510,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
                 else trk::k_score<false, 1><<<g, trk::SCORE_THREADS, 0, s>>>(ws, segs);
             }
         }));
-        CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 256, 0, s>>>(ws); }));
+        CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 1024, 0, s>>>(ws); }));
     }
     return TURBOREG_OK;
 }
