@@ -385,7 +385,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int T = (maxn_batch + 31) / 32;
         // small batches: several blocks share a block-row pair so the grid still covers ~2 waves
         const int bpp = (T + 1) / 2;
-        const int split = std::max(1, std::min(8, (2 * c->num_sms + bpp * batch - 1) / (bpp * batch)));
+        const int split = std::max(1, std::min(16, (5 * c->num_sms + bpp * batch - 1) / (bpp * batch)));
         CK(L.run(KID_COMPAT, [&] {
             const dim3 g((unsigned)(bpp * split), B);
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws, split);
