@@ -233,7 +233,7 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
     const f2_t s_hi2 = f2_pack(s_hi, s_hi);
     const f2_t kap2 = f2_pack(kap, kap);
     // per test, in bit 31:  cc: S > s_hi (q decides);  b: |q| < Tq (q unsure);  q: q < 0.
-    // decided x = ~b & cc;  edge e = x & q;  sacc keeps bit 31 while all decided.
+    // decided = ~b & cc (bit 31);  edge = sign(q);  sacc keeps bit 31 while all decided.
     uint32_t colw[NT], sacc = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < NT; ++k) colw[k] = 0u;
@@ -257,10 +257,11 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
             const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
             const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
-            const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
-            colw[2 * m] = __funnelshift_l(x0 & f2_lo(q), colw[2 * m], 1);
-            colw[2 * m + 1] = __funnelshift_l(x1 & f2_hi(q), colw[2 * m + 1], 1);
-            sacc &= x0 & x1;
+            // edge bit = sign(q): only read when every test of the lane is decided (else the lane redoes all)
+            colw[2 * m] = __funnelshift_l(f2_lo(q), colw[2 * m], 1);
+            colw[2 * m + 1] = __funnelshift_l(f2_hi(q), colw[2 * m + 1], 1);
+            sacc &= ~f2_lo(b) & k0;
+            sacc &= ~f2_hi(b) & k1;
         }
     }
 #pragma unroll
@@ -363,10 +364,11 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
             const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
             const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
-            const uint32_t x0 = ~f2_lo(b) & k0, x1 = ~f2_hi(b) & k1;
-            colw[k] = __funnelshift_l(x0 & f2_lo(q), colw[k], 1);
-            colw[k] = __funnelshift_l(x1 & f2_hi(q), colw[k], 1);
-            sacc &= x0 & x1;
+            // edge bit = sign(q): only read when every test of the lane is decided (else the lane redoes all)
+            colw[k] = __funnelshift_l(f2_lo(q), colw[k], 1);
+            colw[k] = __funnelshift_l(f2_hi(q), colw[k], 1);
+            sacc &= ~f2_lo(b) & k0;
+            sacc &= ~f2_hi(b) & k1;
         }
     }
 #pragma unroll
