@@ -443,11 +443,20 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else if (wpl <= 16) trk::k_sc2<16><<<gp, 256, trk::sc2_smem_bytes<16>(), s>>>(ws, cpi);
             else trk::k_sc2<32><<<gp, 256, trk::sc2_smem_bytes<32>(), s>>>(ws, cpi);
         }));
-        // rows per warp group of the instantiation chosen below: light_rows<WPL>() of the rounded-up WPL
-        const int lgr = wpl > 8 ? trk::light_rows<16>() : trk::light_rows<8>();
+        // rows per warp group: light_rows<WPL>() of the rounded-up WPL, or 2 when that grid would not give
+        // every SM two blocks (small batches)
+        const int lg_def = wpl > 8 ? trk::light_rows<16>() : trk::light_rows<8>();
+        const bool lg_small = lg_def > 2 && (int64_t)((maxn_batch + 8 * lg_def - 1) / (8 * lg_def)) * batch < 2 * c->num_sms;
+        const int lgr = lg_small ? 2 : lg_def;
         const dim3 gl((unsigned)((maxn_batch + 8 * lgr - 1) / (8 * lgr)), B);
         CK(L.run(KID_SC2_LIGHT, [&] {
-            if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), sl>>>(ws);
+            if (lg_small) {
+                if (wpl <= 1) trk::k_sc2_light<1, 2><<<gl, 256, trk::light_smem_bytes<1, 2>(), sl>>>(ws);
+                else if (wpl <= 2) trk::k_sc2_light<2, 2><<<gl, 256, trk::light_smem_bytes<2, 2>(), sl>>>(ws);
+                else if (wpl <= 4) trk::k_sc2_light<4, 2><<<gl, 256, trk::light_smem_bytes<4, 2>(), sl>>>(ws);
+                else if (wpl <= 5) trk::k_sc2_light<5, 2><<<gl, 256, trk::light_smem_bytes<5, 2>(), sl>>>(ws);
+                else trk::k_sc2_light<8, 2><<<gl, 256, trk::light_smem_bytes<8, 2>(), sl>>>(ws);
+            } else if (wpl <= 1) trk::k_sc2_light<1><<<gl, 256, trk::light_smem_bytes<1>(), sl>>>(ws);
             else if (wpl <= 2) trk::k_sc2_light<2><<<gl, 256, trk::light_smem_bytes<2>(), sl>>>(ws);
             else if (wpl <= 4) trk::k_sc2_light<4><<<gl, 256, trk::light_smem_bytes<4>(), sl>>>(ws);
             else if (wpl <= 5) trk::k_sc2_light<5><<<gl, 256, trk::light_smem_bytes<5>(), sl>>>(ws);

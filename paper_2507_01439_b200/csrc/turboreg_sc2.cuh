@@ -375,12 +375,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 
 template <int WPL>
 constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
-template <int WPL>
+template <int WPL, int LG = light_rows<WPL>()>
 constexpr int light_warp_words() {
-    return light_rows<WPL>() * 32 * WPL + light_rows<WPL>() * (LIST_MAX / 2) + 64 + 64 + 4 * light_rows<WPL>();
+    return LG * 32 * WPL + LG * (LIST_MAX / 2) + 64 + 64 + 4 * LG;
 }
-template <int WPL>
-constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL>() * 4; }
+template <int WPL, int LG = light_rows<WPL>()>
+constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL, LG>() * 4; }
 
 template <int WPL>
 __device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t* bm, const int32_t* meta,
@@ -397,9 +397,9 @@ __device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t*
     }
 }
 
-template <int WPL>
+// LG (sparse rows per warp group): light_rows<WPL>() for batches; 2 when a small batch would leave SMs idle
+template <int WPL, int LG = light_rows<WPL>()>
 __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
-    constexpr int LG = light_rows<WPL>();
     extern __shared__ uint32_t s_dyn[];
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int g0 = (blockIdx.x * 8 + warp) * LG;
     if (g0 >= nl) return;
     const int nr = min(LG, nl - g0);
-    uint32_t* bm = s_dyn + warp * light_warp_words<WPL>();
+    uint32_t* bm = s_dyn + warp * light_warp_words<WPL, LG>();
     uint16_t* ls = reinterpret_cast<uint16_t*>(bm + LG * 32 * WPL);
     uint32_t* qL = bm + LG * 32 * WPL + LG * (LIST_MAX / 2);
     uint32_t* qD = qL + 64;
