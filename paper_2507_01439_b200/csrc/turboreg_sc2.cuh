@@ -860,9 +860,24 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
     uint8_t* X = ws.heavy_X + p * ws.heavy_X_stride + (int64_t)a * ws.heavy_Kcap;
     uint2* up = ws.heavy_UP + p * ws.heavy_UP_stride + (int64_t)a * W;
     int carry = 0;
+    // rows up to 256 words: every word of the row is loaded before the first is expanded
+    constexpr int PRE = 8;
+    uint32_t pre[PRE];
+    if (W <= 32 * PRE) {
+#pragma unroll
+        for (int k = 0; k < PRE; ++k) pre[k] = (row && 32 * k + lane < W) ? __ldg(row + 32 * k + lane) : 0u;
+    }
+#pragma unroll 1
     for (int w0 = 0; w0 < W; w0 += 32) {  // 32 bytes per bit word (two 16-byte stores)
         const int w = w0 + lane;
-        const uint32_t v = (row && w < W) ? row[w] : 0u;
+        uint32_t v;
+        if (W <= 32 * PRE) {
+            v = pre[0];
+#pragma unroll
+            for (int k = 1; k < PRE; ++k) v = (w0 == 32 * k) ? pre[k] : v;
+        } else {
+            v = (row && w < W) ? row[w] : 0u;
+        }
         if (w < W) {
             if constexpr (FP4) {  // e2m1: bit k -> nibble k = 0x2 (1.0) or 0 (0.0), 16 bytes per word
                 uint32_t b[4];
