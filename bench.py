@@ -96,6 +96,57 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class NvmlClockSampler:
+    """The same record from NVML, polled every 5 ms by a thread (nvidia-smi's start-up can miss a short
+    timed region).  Reasons: NVML clock-event bits hw_slowdown 0x8, sw_thermal 0x20, hw_thermal 0x40,
+    sw_power_cap 0x4."""
+
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        self.sm, self.reasons = [], set()
+        self.run = False
+
+    def _poll(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while self.run:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = int(get_reasons(self.h))
+                for k, b in self.BITS.items():
+                    if r & b:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        self.run = True
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self.run = False
+        self.t.join(timeout=2)
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
+
+
+def clock_sampler(index):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 # ------------------------------------------------------------------------------------------ workload
 def make_inputs(rank, pairs, n=None, world=1):
     """This rank's shard of the configs[4] sweep: global pairs shard_range(world·pairs, world, rank)."""
@@ -253,7 +304,7 @@ def run_cuda(args, rank, world, local_rank):
     res = out_d.cpu().numpy().view(RESULT_DTYPE)
     ok = sum(int(r["status"] == 0 and synth.rotation_error_deg(r["R"].reshape(3, 3), g[0]) <= 5) for r, g in zip(res, gts))
 
-    clocks = ClockSampler(local_rank)
+    clocks = clock_sampler(local_rank)
     clocks.start()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
