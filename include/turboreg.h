@@ -102,6 +102,19 @@ turboreg_status turboreg_set_params(turboreg_ctx* ctx, const turboreg_params* pa
 turboreg_status turboreg_register(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n,
                                   turboreg_result* out);
 
+/* Equal-budget 3-point RANSAC baseline (SPEC S:324-332 — not part of TurboReg):
+ * `iters` hypotheses from correspondence triples drawn uniformly without replacement by the counter-based
+ * SplitMix64 generator (draw m = mix(seed + (m+1)·0x9e3779b97f4a7c15); triple k uses draws 3k..3k+2:
+ * a = d0 mod n, b = d1 mod (n-1) skipping a, c = d2 mod (n-2) skipping a and b; sorted ascending), each
+ * fitted and scored exactly like a TurboClique (3-point Kabsch, degeneracy test r11, inlier number r13),
+ * winner by (count desc, (i,j,z) asc).  Same inputs, blocking behaviour and result record as
+ * turboreg_register (clique = winning triple, clique_weight = 0, num_pivots = num_edges = 0,
+ * num_cliques = iters); always ranks by inlier number.  Requires 1 <= iters <= the context's K1·K2
+ * (else TURBOREG_ERR_INVALID_ARGUMENT).  The per-hypothesis intermediates (TURBOREG_I_CLIQUES /
+ * TURBOREG_I_HYPS) of the call hold the sampled triples and their fits. */
+turboreg_status turboreg_ransac(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n, int32_t iters,
+                                uint64_t seed, turboreg_result* out);
+
 /* Register `batch` independent pairs in one pass.  Pair p uses points [offsets[p], offsets[p] + n[p]) of
  * src_xyz / dst_xyz (N×3 float32, host or device).  offsets and n are HOST arrays.  out: `batch`
  * results, HOST or DEVICE pointer.  stream: a cudaStream_t (NULL = the context's own stream).

@@ -94,6 +94,12 @@ def lib():
         _lib.oracle_estimate.argtypes = [P, P, i32, ctypes.POINTER(Params), ctypes.POINTER(Result), P, P, P, P, P, P]
         _lib.oracle_hypothesis_errors.argtypes = [P, P, i32, P, P, P, P]
         _lib.oracle_estimate.restype = i32
+        u64 = ctypes.c_uint64
+        _lib.oracle_splitmix64.argtypes = [u64, u64]
+        _lib.oracle_splitmix64.restype = u64
+        _lib.oracle_ransac_triple.argtypes = [u64, i64, i32, P]
+        _lib.oracle_ransac.argtypes = [P, P, i32, i32, u64, f32, ctypes.POINTER(Result), P, P]
+        _lib.oracle_ransac.restype = i32
     return _lib
 
 
@@ -254,3 +260,46 @@ def hypothesis_errors(src, dst, R, t):
     lib().oracle_hypothesis_errors(_p(src), _p(dst), src.shape[0], _p(_f32(np.asarray(R).reshape(9))),
                                    _p(_f32(np.asarray(t).reshape(3))), ctypes.byref(mae), ctypes.byref(mse))
     return mae.value, mse.value
+
+
+# ------------------------------------------------------------------------------------ NEXT(4) RANSAC
+def splitmix64(seed, k):
+    """k-th output of the counter-based SplitMix64 stream seeded with `seed` (the RANSAC sampler's draws)."""
+    return int(lib().oracle_splitmix64(int(seed) & (2**64 - 1), int(k)))
+
+
+def ransac_triple(seed, k, n):
+    """Correspondence triple k (sorted, distinct) of the RANSAC baseline."""
+    out = np.zeros(3, np.int32)
+    lib().oracle_ransac_triple(int(seed) & (2**64 - 1), int(k), int(n), _p(out))
+    return tuple(int(x) for x in out)
+
+
+def ransac(src, dst, iters, seed, inlier_threshold, trace=False):
+    """Equal-budget 3-point RANSAC baseline: `iters` sampled triples, steps 7-8 per
+    triple, argmax by (count desc, (i,j,z) asc)."""
+    src, dst = _f32(src), _f32(dst)
+    n = src.shape[0]
+    res = Result()
+    cl = hyp = None
+    if trace:
+        cl = np.zeros((max(iters, 1), 4), np.int32)
+        hyp = np.zeros((max(iters, 1), 16), np.float32)
+    lib().oracle_ransac(_p(src), _p(dst), n, int(iters), int(seed) & (2**64 - 1), float(inlier_threshold),
+                        ctypes.byref(res), _p(cl), _p(hyp))
+    out = {
+        "status": res.status,
+        "R": np.array(res.R, np.float32).reshape(3, 3),
+        "t": np.array(res.t, np.float32),
+        "inlier_count": res.inlier_count,
+        "clique": tuple(res.clique),
+        "num_cliques": res.num_cliques,
+        "hypotheses_evaluated": res.hypotheses_evaluated,
+        "best_count_f64": res.best_count_f64,
+        "near_corr": res.near_corr,
+    }
+    if trace:
+        out.update(cliques=cl[:iters].copy(), hyp_R=hyp[:iters, :9].reshape(-1, 3, 3).copy(),
+                   hyp_t=hyp[:iters, 9:12].copy(), hyp_count=hyp[:iters, 12].copy().view(np.int32),
+                   hyp_degenerate=hyp[:iters, 13].copy().view(np.int32))
+    return out

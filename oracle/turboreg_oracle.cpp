@@ -23,6 +23,7 @@
 //   8 inlier number g(T) in fixed-order float32            oracle_count_inliers
 //   8' MAE / MSE of a hypothesis (App. F.1, reading r20)     oracle_hypothesis_errors
 //   9 argmax T* (Eq. 9)                                     oracle_estimate
+//   NEXT(4) equal-budget 3-point RANSAC baseline          oracle_ransac
 // plus a brute-force 3-clique enumerator used only as a test pin (App. B/C).
 //
 // Every reading of a point where the paper is silent is listed in DESIGN.md §"Readings" (r1..r18) and
@@ -499,6 +500,94 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
     res->clique[0] = cl[4 * best]; res->clique[1] = cl[4 * best + 1]; res->clique[2] = cl[4 * best + 2];
     res->clique_weight = best_s;
     shadow_count(src, dst, n, bestR64.data(), bestt64.data(), prm->inlier_threshold, &res->best_count_f64, &res->near_corr);
+    res->status = 0;
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------ NEXT(4)
+// Equal-budget 3-point RANSAC baseline: `iters` hypotheses from uniformly
+// drawn correspondence triples, each fitted and scored exactly as steps 7-8, argmax by (count desc,
+// (i,j,z) asc) (reading r14 with S = 0).  The random numbers come from the counter-based SplitMix64
+// (Steele, Lea & Flood 2014; x_k = mix(seed + (k+1)·0x9e3779b97f4a7c15)), which the CUDA side implements
+// independently: triple k uses draws 3k, 3k+1, 3k+2 — a = r0 mod n, b = r1 mod (n-1) skipping a,
+// c = r2 mod (n-2) skipping a and b — sorted ascending.
+uint64_t oracle_splitmix64(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + (k + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+void oracle_ransac_triple(uint64_t seed, int64_t k, int32_t n, int32_t* out3) {
+    const uint64_t r0 = oracle_splitmix64(seed, 3 * (uint64_t)k), r1 = oracle_splitmix64(seed, 3 * (uint64_t)k + 1),
+                   r2 = oracle_splitmix64(seed, 3 * (uint64_t)k + 2);
+    int64_t a = (int64_t)(r0 % (uint64_t)n);
+    int64_t b = (int64_t)(r1 % (uint64_t)(n - 1));
+    if (b >= a) ++b;  // uniform over the n-1 indices other than a
+    int64_t c = (int64_t)(r2 % (uint64_t)(n - 2));
+    const int64_t lo = std::min(a, b), hi = std::max(a, b);
+    if (c >= lo) ++c;  // uniform over the n-2 indices other than a and b
+    if (c >= hi) ++c;
+    int64_t v[3] = {a, b, c};
+    std::sort(v, v + 3);
+    for (int q = 0; q < 3; ++q) out3[q] = (int32_t)v[q];
+}
+
+int32_t oracle_ransac(const float* src, const float* dst, int32_t n, int32_t iters, uint64_t seed, float thr,
+                      oracle_result* res, int32_t* cliques_out, float* hyp_out) {
+    std::memset(res, 0, sizeof(*res));
+    if (n < 3) { res->status = 2; return 2; }
+    int32_t best = -1, best_cnt = -1;
+    int32_t best_ijz[3] = {0, 0, 0};
+    int32_t nvalid = 0;
+    std::vector<double> bestR64(9), bestt64(3);
+    for (int32_t c = 0; c < iters; ++c) {
+        int32_t idx[3];
+        oracle_ransac_triple(seed, c, n, idx);
+        if (cliques_out) { cliques_out[4 * c] = idx[0]; cliques_out[4 * c + 1] = idx[1]; cliques_out[4 * c + 2] = idx[2]; cliques_out[4 * c + 3] = 0; }
+        float* h = hyp_out ? hyp_out + 16 * (size_t)c : nullptr;
+        if (h) std::memset(h, 0, 16 * sizeof(float));
+        bool degen = oracle_triangle_degenerate(src + 3 * idx[0], src + 3 * idx[1], src + 3 * idx[2]) ||
+                     oracle_triangle_degenerate(dst + 3 * idx[0], dst + 3 * idx[1], dst + 3 * idx[2]);
+        double P[9], Q[9], R64[9], t64[3];
+        for (int k = 0; k < 3; ++k)
+            for (int d = 0; d < 3; ++d) { P[3 * k + d] = src[3 * idx[k] + d]; Q[3 * k + d] = dst[3 * idx[k] + d]; }
+        if (!degen && oracle_kabsch(P, Q, 3, R64, t64) != 0) degen = true;
+        if (degen) {
+            if (h) { int32_t one = 1; std::memcpy(&h[13], &one, 4); }
+            continue;
+        }
+        ++nvalid;
+        float R32[9], t32[3];
+        for (int k = 0; k < 9; ++k) R32[k] = (float)R64[k];
+        for (int k = 0; k < 3; ++k) t32[k] = (float)t64[k];
+        const int32_t cnt = oracle_count_inliers(src, dst, n, R32, t32, thr);
+        if (h) {
+            std::memcpy(h, R32, sizeof(R32));
+            std::memcpy(h + 9, t32, sizeof(t32));
+            std::memcpy(&h[12], &cnt, 4);
+        }
+        const bool ijz_less = std::lexicographical_compare(idx, idx + 3, best_ijz, best_ijz + 3);
+        if (best < 0 || cnt > best_cnt || (cnt == best_cnt && ijz_less)) {
+            best = c; best_cnt = cnt;
+            std::memcpy(best_ijz, idx, sizeof(idx));
+            std::memcpy(res->R, R32, sizeof(R32));
+            std::memcpy(res->t, t32, sizeof(t32));
+            std::memcpy(bestR64.data(), R64, sizeof(R64));
+            std::memcpy(bestt64.data(), t64, sizeof(t64));
+        }
+    }
+    res->num_cliques = iters;
+    res->hypotheses_evaluated = nvalid;
+    if (best < 0) {
+        std::memset(res->R, 0, sizeof(res->R));
+        std::memset(res->t, 0, sizeof(res->t));
+        res->status = 5;
+        return 5;
+    }
+    res->inlier_count = best_cnt;
+    std::memcpy(res->clique, best_ijz, sizeof(best_ijz));
+    shadow_count(src, dst, n, bestR64.data(), bestt64.data(), thr, &res->best_count_f64, &res->near_corr);
     res->status = 0;
     return 0;
 }

@@ -100,6 +100,7 @@ def library():
     lib.turboreg_create.argtypes = [ctypes.POINTER(Params), ctypes.c_int, i32, i32, ctypes.POINTER(P)]
     lib.turboreg_set_params.argtypes = [P, ctypes.POINTER(Params)]
     lib.turboreg_register.argtypes = [P, P, P, i32, ctypes.POINTER(Result)]
+    lib.turboreg_ransac.argtypes = [P, P, P, i32, i32, ctypes.c_uint64, ctypes.POINTER(Result)]
     lib.turboreg_register_batch.argtypes = [P, P, P, P, P, i32, P, P]
     lib.turboreg_destroy.argtypes = [P]
     lib.turboreg_destroy.restype = None
@@ -202,6 +203,19 @@ class TurboReg:
         st = self._lib.turboreg_register(self._h, ps, pd, n, ctypes.byref(res))
         if st not in (0, 2, 3, 4, 5):
             raise TurboRegError(st, "register")
+        return result_to_dict(res)
+
+    def ransac(self, src, dst, iters, seed=0):
+        """Equal-budget 3-point RANSAC baseline on one pair: ``iters`` <= K1·K2 sampled
+        triples (counter-based SplitMix64 from ``seed``), fitted and scored like TurboCliques.  Returns the
+        same dict as :meth:`register`."""
+        ps, ks = _ptr(src, np.float32)
+        pd, kd = _ptr(dst, np.float32)
+        res = Result()
+        st = self._lib.turboreg_ransac(self._h, ps, pd, int(src.shape[0]), int(iters), int(seed) & (2**64 - 1),
+                                       ctypes.byref(res))
+        if st not in (0, 2, 3, 4, 5):
+            raise TurboRegError(st, "ransac")
         return result_to_dict(res)
 
     def register_batch(self, src, dst, offsets, n, out=None, stream=None):

@@ -143,6 +143,40 @@ __global__ void __launch_bounds__(1024) k_canon(WS ws) {
     for (int k = base + threadIdx.x; k < K; k += blockDim.x) cl[k] = make_int4(-1, -1, -1, 0);
 }
 
+// ------------------------------------------------------------------------------------------ NEXT(4)
+// Equal-budget 3-point RANSAC baseline: slot k of the clique list gets the sorted
+// distinct triple drawn from the counter-based SplitMix64 stream (x_m = mix(seed + (m+1)·γ), draws 3k..3k+2:
+// a = x mod n, b = x' mod (n-1) skipping a, c = x'' mod (n-2) skipping a and b), S = 0; k_kabsch, k_score
+// and k_finalize then run unchanged on ws.k1 = iters, ws.k2 = 1.
+__device__ __forceinline__ uint64_t sm64_draw(uint64_t seed, uint64_t m) {
+    uint64_t x = seed + (m + 1ull) * 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__global__ void __launch_bounds__(256) k_ransac_sample(WS ws, unsigned long long seed) {
+    const int q = blockIdx.y;
+    const PairDesc d = ws.desc[q];
+    const int K = ws.k1 * ws.k2;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) { ws.st[q].npiv = 0; ws.st[q].edges = 0; }
+    if (k >= K) return;
+    int4 c = make_int4(-1, -1, -1, 0);
+    const int n = d.n;
+    if (n >= 3) {
+        const uint64_t m = 3ull * (uint64_t)k;
+        long long a = (long long)(sm64_draw(seed, m) % (uint64_t)n);
+        long long b = (long long)(sm64_draw(seed, m + 1) % (uint64_t)(n - 1));
+        b += (b >= a);
+        long long e = (long long)(sm64_draw(seed, m + 2) % (uint64_t)(n - 2));
+        e += (e >= min(a, b));
+        e += (e >= max(a, b));
+        const long long lo = min(a, min(b, e)), hi = max(a, max(b, e));
+        c = make_int4((int)lo, (int)(a + b + e - lo - hi), (int)hi, 0);
+    }
+    ws.cliq[q * ws.cl_stride + k] = c;
+}
+
 __global__ void __launch_bounds__(128) k_kabsch(WS ws) {
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];

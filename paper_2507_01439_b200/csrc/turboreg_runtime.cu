@@ -48,14 +48,15 @@ enum KernelId {
     KID_KABSCH,
     KID_SCORE,
     KID_FINALIZE,
+    KID_RANSAC,
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
                                        "k_expand",   "k_sc2_mma",      "k_emit_hh",     "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
-                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize"};
+                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize",    "k_ransac_sample"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 1};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -74,6 +75,8 @@ struct turboreg_ctx {
     cudaStream_t side_stream = nullptr;  // the sparse-row SC^2 kernel, concurrent with the dense-row one
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool use_fork = true;
+    int32_t ransac_iters = 0;       // > 0 while turboreg_ransac runs: the RUN_RANSAC path
+    unsigned long long ransac_seed = 0;
     cudaEvent_t ev_start = nullptr, ev_chunk[NCHUNK] = {};
     bool use_chunks = true;
     // device workspace
@@ -361,7 +364,7 @@ void harvest_events(turboreg_ctx* c, float* stage_ms) {
     c->ev_used = 0;
 }
 
-enum RunMode { RUN_FULL = 0, RUN_FROM_ADJ = 1 };
+enum RunMode { RUN_FULL = 0, RUN_FROM_ADJ = 1, RUN_RANSAC = 2 };
 
 // phase: PH_ALL = the whole path; PH_HEAD = state reset + ingest + compat (per pipelined sub-batch);
 // PH_TAIL = everything after compat.
@@ -377,6 +380,30 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     if (phase != PH_TAIL) {
         CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
         CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 16, s));
+    }
+    if (mode == RUN_RANSAC) {  // NEXT(4): ingest, sampled triples, then the model stage on them
+        CK(L.run(KID_INGEST, [&] {
+            trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
+        }));
+        trk::WS wr = ws;
+        wr.k1 = c->ransac_iters;
+        wr.k2 = 1;
+        wr.err_mode = 0;  // inlier-number ranking
+        const int64_t KC = c->ransac_iters;
+        CK(L.run(KID_RANSAC, [&] {
+            trk::k_ransac_sample<<<dim3((unsigned)((KC + 255) / 256), B), 256, 0, s>>>(wr, c->ransac_seed);
+        }));
+        CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(wr); }));
+        CK(L.run(KID_SCORE, [&] {
+            const int npk = c->opt_score_pairs;
+            const int hb = (int)((KC + trk::SCORE_HT * npk - 1) / (trk::SCORE_HT * npk));
+            const int segs = std::max(2, std::min(16, (7 * c->num_sms + hb * batch - 1) / (hb * batch)));
+            const dim3 g((unsigned)(hb * segs), B);
+            if (npk == 2) trk::k_score<false, 2><<<g, trk::SCORE_THREADS, 0, s>>>(wr, segs);
+            else trk::k_score<false, 1><<<g, trk::SCORE_THREADS, 0, s>>>(wr, segs);
+        }));
+        CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 1024, 0, s>>>(wr); }));
+        return TURBOREG_OK;
     }
     if (mode == RUN_FULL && phase != PH_TAIL) {
         CK(L.run(KID_INGEST, [&] {
@@ -530,7 +557,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
 turboreg_status run_pipeline(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode,
                              int32_t p0 = 0, int phase = PH_ALL) {
     const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
-    if (timed || !c->use_graphs) return launch_all(c, batch, maxn_batch, s, mode, p0, phase);
+    if (timed || !c->use_graphs || mode == RUN_RANSAC)  // RANSAC: iters / seed are launch arguments
+        return launch_all(c, batch, maxn_batch, s, mode, p0, phase);
     turboreg_ctx::GraphEntry* ge = nullptr;
     for (auto& g : c->graphs)
         if (g.batch == batch && g.maxn == maxn_batch && g.mode == (int32_t)mode && g.p0 == p0 && g.phase == phase)
@@ -830,7 +858,7 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
         if (nchunk > 1) CK(cudaEventRecord(c->ev_chunk[k], cs));
     }
     if (nchunk == 1) {
-        turboreg_status st = run_pipeline(c, batch, maxn_batch, s, RUN_FULL);
+        turboreg_status st = run_pipeline(c, batch, maxn_batch, s, c->ransac_iters > 0 ? RUN_RANSAC : RUN_FULL);
         if (st != TURBOREG_OK) return st;
     } else {  // compat of sub-batch k overlaps the copy of sub-batch k+1; the rest runs on the whole batch
         for (int k = 0; k < nchunk; ++k) {
@@ -872,6 +900,16 @@ turboreg_status turboreg_register(turboreg_ctx* c, const float* src, const float
     if (st != TURBOREG_OK) return st;
     *out = tmp;
     return (turboreg_status)tmp.status;
+}
+
+turboreg_status turboreg_ransac(turboreg_ctx* c, const float* src, const float* dst, int32_t n, int32_t iters,
+                                uint64_t seed, turboreg_result* out) {
+    if (!c || !out || iters < 1 || (int64_t)iters > (int64_t)c->ws.cl_stride) return TURBOREG_ERR_INVALID_ARGUMENT;
+    c->ransac_iters = iters;
+    c->ransac_seed = (unsigned long long)seed;
+    const turboreg_status st = turboreg_register(c, src, dst, n, out);
+    c->ransac_iters = 0;
+    return st;
 }
 
 turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_t what, void* dst, size_t bytes,
