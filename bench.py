@@ -393,6 +393,37 @@ def run_cuda(args, rank, world, local_rank):
             trk_.close()
             lat_cfg[f"{key} ({c.name}, N={nk}, K1={c.k1})"] = round(float(np.median(ts)), 4)
 
+    # ---- NEXT(4) context: equal-budget 3-point RANSAC (K1*K2 sampled triples) vs TurboReg on config-C pairs
+    # (3DLoMatch-shaped, 5 % inliers), host inputs, wall-clock per call; not part of the timed step
+    ransac = None
+    if rank == 0:
+        c = synth.CONFIGS["C"]
+        budget = c.k1 * c.k2
+        trr = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=c.n, max_batch=1, device=local_rank)
+        rec_t = rec_r = 0
+        inl_t, inl_r, t_t, t_r = [], [], [], []
+        npairs = 10
+        for q in range(npairs):
+            inst = synth.workload_instance(c, pair=500 + q)
+            trr.register(inst["src"], inst["dst"])  # warm (graph capture on the first call)
+            t0 = time.perf_counter()
+            rt = trr.register(inst["src"], inst["dst"])
+            t1 = time.perf_counter()
+            rr = trr.ransac(inst["src"], inst["dst"], budget, seed=q)
+            t2 = time.perf_counter()
+            t_t.append(t1 - t0)
+            t_r.append(t2 - t1)
+            inl_t.append(rt["inlier_count"])
+            inl_r.append(rr["inlier_count"])
+            rec_t += int(rt["status"] == 0 and synth.rotation_error_deg(rt["R"].reshape(3, 3), inst["R"]) <= 5)
+            rec_r += int(rr["status"] == 0 and synth.rotation_error_deg(rr["R"].reshape(3, 3), inst["R"]) <= 5)
+        trr.close()
+        ransac = {"config": f"C ({c.name}), {npairs} pairs, budget K1*K2 = {budget} hypotheses each",
+                  "turboreg": {"recovered_re_le_5deg": rec_t, "mean_inliers": float(np.mean(inl_t)),
+                               "ms_per_pair_host_io": round(1e3 * float(np.median(t_t)), 3)},
+                  "ransac": {"recovered_re_le_5deg": rec_r, "mean_inliers": float(np.mean(inl_r)),
+                             "ms_per_pair_host_io": round(1e3 * float(np.median(t_r)), 3)}}
+
     # gather per-pair results (the only collective: NCCL all_gather of fixed-size records, outside timing)
     if world > 1:
         from paper_2507_01439_b200.sharding import gather_results
@@ -427,6 +458,7 @@ def run_cuda(args, rank, world, local_rank):
         "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "single_pair_latency_ms": float(np.median(lat)),
         "single_pair_latency_ms_configs": lat_cfg,
+        "ransac_equal_budget": ransac,
         "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{pairs * world}",
         "wall_s_timed_region": wall,
     }
