@@ -102,6 +102,15 @@ turboreg_status turboreg_set_params(turboreg_ctx* ctx, const turboreg_params* pa
 turboreg_status turboreg_register(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n,
                                   turboreg_result* out);
 
+/* Point-cloud resolution for the τ initialisation τ = 0.25 · pr (
+ * SPEC S:163-171 estimate_resolution): *out_pr = the median over the n points of the distance to each
+ * point's nearest other point, distances in the float32 tree of reading r1, the lower median (element
+ * (n-1)/2 of the sorted distances, reading r22).  xyz: n×3 float32 row-major, HOST or DEVICE (detected);
+ * blocking.  Errors: n < 2 or a null pointer → TURBOREG_ERR_INVALID_ARGUMENT; n > max_n →
+ * TURBOREG_ERR_TOO_MANY_POINTS; a non-finite coordinate → TURBOREG_ERR_NONFINITE_INPUT (*out_pr untouched).
+ * Uses the context's device and input staging area (not concurrently with another call on it). */
+turboreg_status turboreg_point_resolution(turboreg_ctx* ctx, const float* xyz, int32_t n, float* out_pr);
+
 /* Equal-budget 3-point RANSAC baseline (SPEC S:324-332 — not part of TurboReg):
  * `iters` hypotheses from correspondence triples drawn uniformly without replacement by the counter-based
  * SplitMix64 generator (draw m = mix(seed + (m+1)·0x9e3779b97f4a7c15); triple k uses draws 3k..3k+2:

@@ -100,6 +100,8 @@ def lib():
         _lib.oracle_ransac_triple.argtypes = [u64, i64, i32, P]
         _lib.oracle_ransac.argtypes = [P, P, i32, i32, u64, f32, ctypes.POINTER(Result), P, P]
         _lib.oracle_ransac.restype = i32
+        _lib.oracle_point_resolution.argtypes = [P, i32]
+        _lib.oracle_point_resolution.restype = f32
     return _lib
 
 
@@ -303,3 +305,11 @@ def ransac(src, dst, iters, seed, inlier_threshold, trace=False):
                    hyp_t=hyp[:iters, 9:12].copy(), hyp_count=hyp[:iters, 12].copy().view(np.int32),
                    hyp_degenerate=hyp[:iters, 13].copy().view(np.int32))
     return out
+
+
+# ------------------------------------------------------------------------------------ NEXT(3) resolution
+def point_resolution(xyz):
+    """Median nearest-neighbour distance of a point cloud (lower median, float32 distances, reading r22);
+    the τ initialisation of P:322 is 0.25 × this."""
+    xyz = _f32(xyz)
+    return float(lib().oracle_point_resolution(_p(xyz), xyz.shape[0]))

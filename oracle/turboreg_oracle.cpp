@@ -23,6 +23,7 @@
 //   8 inlier number g(T) in fixed-order float32            oracle_count_inliers
 //   8' MAE / MSE of a hypothesis (App. F.1, reading r20)     oracle_hypothesis_errors
 //   9 argmax T* (Eq. 9)                                     oracle_estimate
+//   NEXT(3) point-cloud resolution for τ = 0.25 pr              oracle_point_resolution
 //   NEXT(4) equal-budget 3-point RANSAC baseline          oracle_ransac
 // plus a brute-force 3-clique enumerator used only as a test pin (App. B/C).
 //
@@ -502,6 +503,27 @@ int32_t oracle_estimate(const float* src, const float* dst, int32_t n, const ora
     shadow_count(src, dst, n, bestR64.data(), bestt64.data(), prm->inlier_threshold, &res->best_count_f64, &res->near_corr);
     res->status = 0;
     return 0;
+}
+
+// ------------------------------------------------------------------------------------------ NEXT(3)
+// Point-cloud resolution for the τ initialisation τ = 0.25 · pr (SPEC S:163-171
+// estimate_resolution): the median over points of the distance to each point's nearest other point,
+// brute force in the float32 tree of reading r1, the lower median (element (n-1)/2 of the sorted
+// distances, reading r22).  Returns -1 for n < 2.
+float oracle_point_resolution(const float* xyz, int32_t n) {
+    if (n < 2) return -1.f;
+    std::vector<float> nn((size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        float best = INFINITY;
+        for (int32_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            const float d = f32_dist(xyz + 3 * (size_t)i, xyz + 3 * (size_t)j);
+            if (d < best) best = d;
+        }
+        nn[i] = best;
+    }
+    std::sort(nn.begin(), nn.end());
+    return nn[(size_t)(n - 1) / 2];
 }
 
 // ------------------------------------------------------------------------------------------ NEXT(4)

@@ -101,6 +101,7 @@ def library():
     lib.turboreg_set_params.argtypes = [P, ctypes.POINTER(Params)]
     lib.turboreg_register.argtypes = [P, P, P, i32, ctypes.POINTER(Result)]
     lib.turboreg_ransac.argtypes = [P, P, P, i32, i32, ctypes.c_uint64, ctypes.POINTER(Result)]
+    lib.turboreg_point_resolution.argtypes = [P, P, i32, ctypes.POINTER(ctypes.c_float)]
     lib.turboreg_register_batch.argtypes = [P, P, P, P, P, i32, P, P]
     lib.turboreg_destroy.argtypes = [P]
     lib.turboreg_destroy.restype = None
@@ -204,6 +205,15 @@ class TurboReg:
         if st not in (0, 2, 3, 4, 5):
             raise TurboRegError(st, "register")
         return result_to_dict(res)
+
+    def point_resolution(self, xyz):
+        """Median nearest-neighbour distance of a point cloud (n×3 float32, host numpy or CUDA torch): the
+        τ initialisation of P:322 is 0.25 × this."""
+        p, keep = _ptr(xyz, np.float32)
+        out = ctypes.c_float()
+        _check(self._lib.turboreg_point_resolution(self._h, p, int(xyz.shape[0]), ctypes.byref(out)),
+               "point_resolution")
+        return float(out.value)
 
     def ransac(self, src, dst, iters, seed=0):
         """Equal-budget 3-point RANSAC baseline on one pair: ``iters`` <= K1·K2 sampled

@@ -143,6 +143,66 @@ __global__ void __launch_bounds__(1024) k_canon(WS ws) {
     for (int k = base + threadIdx.x; k < K; k += blockDim.x) cl[k] = make_int4(-1, -1, -1, 0);
 }
 
+// ------------------------------------------------------------------------------------------ NEXT(3)
+// Point-cloud resolution pr for the τ initialisation τ = 0.25·pr: nn[i] = distance from
+// point i to its nearest other point in the float32 tree of reading r1 (the minimum is taken on the squared
+// distance — correctly rounded sqrt is monotone, so sqrt(min) = min(sqrt)), then the lower median
+// (reading r22) by a 4-pass radix select on the (non-negative) float bit patterns.
+constexpr int NN_TILE = 1024;
+__global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, float* nn, int* nonfinite) {
+    __shared__ float4 s_p[NN_TILE];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    float xi = 0.f, yi = 0.f, zi = 0.f;
+    if (i < n) {
+        xi = xyz[3 * (int64_t)i];
+        yi = xyz[3 * (int64_t)i + 1];
+        zi = xyz[3 * (int64_t)i + 2];
+        if (!isfinite(xi) || !isfinite(yi) || !isfinite(zi)) atomicOr(nonfinite, 1);
+    }
+    float best = __int_as_float(0x7f800000);  // +inf
+    for (int j0 = 0; j0 < n; j0 += NN_TILE) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < NN_TILE; t += blockDim.x) {
+            const int j = j0 + t;
+            s_p[t] = j < n ? make_float4(xyz[3 * (int64_t)j], xyz[3 * (int64_t)j + 1], xyz[3 * (int64_t)j + 2], 0.f)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        const int m = min(NN_TILE, n - j0);
+        for (int t = 0; t < m; ++t) {
+            const float4 q = s_p[t];
+            const float dx = __fsub_rn(xi, q.x), dy = __fsub_rn(yi, q.y), dz = __fsub_rn(zi, q.z);
+            const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+            if (j0 + t != i) best = fminf(best, d2);
+        }
+    }
+    if (i < n) nn[i] = __fsqrt_rn(best);
+}
+__global__ void __launch_bounds__(1024) k_select_kth(const float* v, int n, int k, float* out) {
+    __shared__ unsigned s_h[256];
+    __shared__ unsigned s_prefix, s_mask, s_k;
+    if (threadIdx.x == 0) { s_prefix = 0u; s_mask = 0u; s_k = (unsigned)k; }
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) s_h[b] = 0u;
+        __syncthreads();
+        const unsigned prefix = s_prefix, mask = s_mask;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned u = __float_as_uint(v[i]);
+            if ((u & mask) == prefix) atomicAdd(&s_h[(u >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned kk = s_k, b = 0;
+            while (s_h[b] <= kk) { kk -= s_h[b]; ++b; }
+            s_k = kk;
+            s_prefix = prefix | (b << shift);
+            s_mask = mask | (255u << shift);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = __uint_as_float(s_prefix);
+}
+
 // ------------------------------------------------------------------------------------------ NEXT(4)
 // Equal-budget 3-point RANSAC baseline: slot k of the clique list gets the sorted
 // distinct triple drawn from the counter-based SplitMix64 stream (x_m = mix(seed + (m+1)·γ), draws 3k..3k+2:

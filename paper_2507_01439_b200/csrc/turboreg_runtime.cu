@@ -902,6 +902,33 @@ turboreg_status turboreg_register(turboreg_ctx* c, const float* src, const float
     return (turboreg_status)tmp.status;
 }
 
+turboreg_status turboreg_point_resolution(turboreg_ctx* c, const float* xyz, int32_t n, float* out_pr) {
+    if (!c || !xyz || !out_pr || n < 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+    if (n > c->max_n) return TURBOREG_ERR_TOO_MANY_POINTS;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->own_stream;
+    const float* pts = xyz;
+    if (!is_device_ptr(xyz)) {  // stage through the context's input area
+        CK(cudaMemcpyAsync(c->d_inputs, xyz, sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, s));
+        pts = c->d_inputs;
+    }
+    float* nn = c->d_inputs + (size_t)3 * c->max_n * c->max_batch;  // the second half of the staging area
+    int* flag = c->d_counters;
+    float* res = reinterpret_cast<float*>(c->d_counters + 1);
+    CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 2, s));
+    trk::k_nn_dist<<<(n + 255) / 256, 256, 0, s>>>(pts, n, nn, flag);
+    CK(cudaGetLastError());
+    trk::k_select_kth<<<1, 1024, 0, s>>>(nn, n, (n - 1) / 2, res);
+    CK(cudaGetLastError());
+    int h[2];
+    CK(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->launches += 2;
+    if (h[0]) return TURBOREG_ERR_NONFINITE_INPUT;
+    std::memcpy(out_pr, &h[1], sizeof(float));
+    return TURBOREG_OK;
+}
+
 turboreg_status turboreg_ransac(turboreg_ctx* c, const float* src, const float* dst, int32_t n, int32_t iters,
                                 uint64_t seed, turboreg_result* out) {
     if (!c || !out || iters < 1 || (int64_t)iters > (int64_t)c->ws.cl_stride) return TURBOREG_ERR_INVALID_ARGUMENT;

@@ -1,6 +1,6 @@
-"""Equal-budget 3-point RANSAC baseline through the C ABI vs the oracle: the
+"""NEXT rows through the C ABI vs the oracle.  Equal-budget 3-point RANSAC baseline: the
 sampled triples and every per-hypothesis count bit-exact, fits within the transform tolerance, the same
-winner.  Needs a B200: `pytest -m gpu`."""
+winner; point-cloud resolution (row 3) bit-exact.  Needs a B200: `pytest -m gpu`."""
 import numpy as np
 import pytest
 
@@ -74,3 +74,38 @@ def test_ransac_budget_is_checked(TR):
     with pytest.raises(TurboRegError):
         tr.ransac(inst["src"], inst["dst"], 0, 0)
     assert tr.ransac(inst["src"], inst["dst"], 20, 0)["num_cliques"] == 20
+
+
+# ------------------------------------------------------------------------------------ NEXT(3) resolution
+@pytest.mark.parametrize("n,seed", [(2, 0), (3, 1), (1000, 2), (5000, 3), (32768, 4)])
+def test_point_resolution_matches_oracle(TR, n, seed):
+    rng = np.random.default_rng(seed)
+    xyz = rng.uniform(-1.5, 1.5, size=(n, 3)).astype(np.float32)
+    if n >= 1000:
+        xyz[5] = xyz[17]  # a duplicate point: nearest distance 0
+    tr = TR(0.012, 10, 2, 0.1, max_n=max(n, 3))
+    got = tr.point_resolution(xyz)
+    if n <= 5000:
+        assert got == oracle.point_resolution(xyz)  # bit-exact (same float32 tree, same order statistic)
+    else:  # n = 32768: the oracle's O(n^2) loop is slow; check the order statistic on sampled points
+        spatial = pytest.importorskip("scipy.spatial")
+        d, _ = spatial.cKDTree(xyz.astype(np.float64)).query(xyz.astype(np.float64), k=2)
+        ref = np.sort(d[:, 1])[(n - 1) // 2]
+        assert abs(got - ref) <= 4e-7 * ref
+    import torch
+
+    assert tr.point_resolution(torch.from_numpy(xyz).cuda()) == got  # device input
+
+
+def test_point_resolution_errors(TR):
+    from paper_2507_01439_b200._binding import TurboRegError
+
+    tr = TR(0.012, 10, 2, 0.1, max_n=100)
+    with pytest.raises(TurboRegError):
+        tr.point_resolution(np.zeros((1, 3), np.float32))
+    with pytest.raises(TurboRegError):
+        tr.point_resolution(np.zeros((101, 3), np.float32))
+    bad = np.zeros((10, 3), np.float32)
+    bad[3, 1] = np.nan
+    with pytest.raises(TurboRegError):
+        tr.point_resolution(bad)
