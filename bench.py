@@ -418,7 +418,25 @@ def run_cuda(args, rank, world, local_rank):
             rec_t += int(rt["status"] == 0 and synth.rotation_error_deg(rt["R"].reshape(3, 3), inst["R"]) <= 5)
             rec_r += int(rr["status"] == 0 and synth.rotation_error_deg(rr["R"].reshape(3, 3), inst["R"]) <= 5)
         trr.close()
+        # NEXT(3): point-cloud resolution (tau = 0.25 pr) of device-resident clouds, CUDA-event timed
+        res_ms = {}
+        for npts in (5000, 32768):
+            trp = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=npts, max_batch=1, device=local_rank)
+            cloud = torch.from_numpy(
+                np.random.default_rng(npts).uniform(-1.5, 1.5, size=(npts, 3)).astype(np.float32)).to(dev)
+            trp.point_resolution(cloud)
+            ts = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                trp.point_resolution(cloud)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            trp.close()
+            res_ms[f"N={npts}"] = round(float(np.median(ts)), 4)
         ransac = {"config": f"C ({c.name}), {npairs} pairs, budget K1*K2 = {budget} hypotheses each",
+                  "point_resolution_ms": res_ms,
                   "turboreg": {"recovered_re_le_5deg": rec_t, "mean_inliers": float(np.mean(inl_t)),
                                "ms_per_pair_host_io": round(1e3 * float(np.median(t_t)), 3)},
                   "ransac": {"recovered_re_le_5deg": rec_r, "mean_inliers": float(np.mean(inl_r)),

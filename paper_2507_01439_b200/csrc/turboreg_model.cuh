@@ -146,10 +146,13 @@ __global__ void __launch_bounds__(1024) k_canon(WS ws) {
 // ------------------------------------------------------------------------------------------ NEXT(3)
 // Point-cloud resolution pr for the τ initialisation τ = 0.25·pr: nn[i] = distance from
 // point i to its nearest other point in the float32 tree of reading r1 (the minimum is taken on the squared
-// distance — correctly rounded sqrt is monotone, so sqrt(min) = min(sqrt)), then the lower median
-// (reading r22) by a 4-pass radix select on the (non-negative) float bit patterns.
+// distance — correctly rounded sqrt is monotone, so sqrt(min) = min(sqrt) and sqrt(k-th) = k-th(sqrt)), then
+// the lower median (reading r22) by a 4-pass radix select on the (non-negative) float bit patterns.
 constexpr int NN_TILE = 1024;
-__global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, float* nn, int* nonfinite) {
+// grid (point blocks, j splits): split y scans candidates [y·span, (y+1)·span) and folds its minimum squared
+// distance into nn2[i] (float bits; non-negative floats order like their bit patterns, so an integer
+// atomicMin is the float minimum).  nn2 must start at +inf.
+__global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, int span, int* nn2, int* nonfinite) {
     __shared__ float4 s_p[NN_TILE];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     float xi = 0.f, yi = 0.f, zi = 0.f;
@@ -157,18 +160,19 @@ __global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, float*
         xi = xyz[3 * (int64_t)i];
         yi = xyz[3 * (int64_t)i + 1];
         zi = xyz[3 * (int64_t)i + 2];
-        if (!isfinite(xi) || !isfinite(yi) || !isfinite(zi)) atomicOr(nonfinite, 1);
+        if (blockIdx.y == 0 && (!isfinite(xi) || !isfinite(yi) || !isfinite(zi))) atomicOr(nonfinite, 1);
     }
     float best = __int_as_float(0x7f800000);  // +inf
-    for (int j0 = 0; j0 < n; j0 += NN_TILE) {
+    const int jb = blockIdx.y * span, je = min(n, jb + span);
+    for (int j0 = jb; j0 < je; j0 += NN_TILE) {
         __syncthreads();
         for (int t = threadIdx.x; t < NN_TILE; t += blockDim.x) {
             const int j = j0 + t;
-            s_p[t] = j < n ? make_float4(xyz[3 * (int64_t)j], xyz[3 * (int64_t)j + 1], xyz[3 * (int64_t)j + 2], 0.f)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            s_p[t] = j < je ? make_float4(xyz[3 * (int64_t)j], xyz[3 * (int64_t)j + 1], xyz[3 * (int64_t)j + 2], 0.f)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
-        const int m = min(NN_TILE, n - j0);
+        const int m = min(NN_TILE, je - j0);
         for (int t = 0; t < m; ++t) {
             const float4 q = s_p[t];
             const float dx = __fsub_rn(xi, q.x), dy = __fsub_rn(yi, q.y), dz = __fsub_rn(zi, q.z);
@@ -176,9 +180,14 @@ __global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, float*
             if (j0 + t != i) best = fminf(best, d2);
         }
     }
-    if (i < n) nn[i] = __fsqrt_rn(best);
+    if (i < n) atomicMin(nn2 + i, __float_as_int(best));
 }
-__global__ void __launch_bounds__(1024) k_select_kth(const float* v, int n, int k, float* out) {
+__global__ void k_fill_inf(int* v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = 0x7f800000;
+}
+// k-th smallest (0-based) of n non-negative float bit patterns; *out = sqrt of it (the distance)
+__global__ void __launch_bounds__(1024) k_select_kth(const int* v, int n, int k, float* out) {
     __shared__ unsigned s_h[256];
     __shared__ unsigned s_prefix, s_mask, s_k;
     if (threadIdx.x == 0) { s_prefix = 0u; s_mask = 0u; s_k = (unsigned)k; }
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(1024) k_select_kth(const float* v, int n, int 
         __syncthreads();
         const unsigned prefix = s_prefix, mask = s_mask;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const unsigned u = __float_as_uint(v[i]);
+            const unsigned u = (unsigned)v[i];
             if ((u & mask) == prefix) atomicAdd(&s_h[(u >> shift) & 255u], 1u);
         }
         __syncthreads();
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(1024) k_select_kth(const float* v, int n, int 
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = __uint_as_float(s_prefix);
+    if (threadIdx.x == 0) *out = __fsqrt_rn(__uint_as_float(s_prefix));
 }
 
 // ------------------------------------------------------------------------------------------ NEXT(4)

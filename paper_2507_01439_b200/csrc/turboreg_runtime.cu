@@ -912,18 +912,23 @@ turboreg_status turboreg_point_resolution(turboreg_ctx* c, const float* xyz, int
         CK(cudaMemcpyAsync(c->d_inputs, xyz, sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, s));
         pts = c->d_inputs;
     }
-    float* nn = c->d_inputs + (size_t)3 * c->max_n * c->max_batch;  // the second half of the staging area
+    int* nn2 = reinterpret_cast<int*>(c->d_inputs + (size_t)3 * c->max_n * c->max_batch);  // staging, 2nd half
     int* flag = c->d_counters;
     float* res = reinterpret_cast<float*>(c->d_counters + 1);
     CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 2, s));
-    trk::k_nn_dist<<<(n + 255) / 256, 256, 0, s>>>(pts, n, nn, flag);
+    trk::k_fill_inf<<<(n + 255) / 256, 256, 0, s>>>(nn2, n);
+    // candidate splits so the grid covers ~4 blocks per SM (each split at least one shared-memory tile)
+    const int pb = (n + 255) / 256;
+    const int splits = std::max(1, std::min((4 * c->num_sms + pb - 1) / pb, (n + trk::NN_TILE - 1) / trk::NN_TILE));
+    const int span = (n + splits - 1) / splits;
+    trk::k_nn_dist<<<dim3((unsigned)pb, (unsigned)splits), 256, 0, s>>>(pts, n, span, nn2, flag);
     CK(cudaGetLastError());
-    trk::k_select_kth<<<1, 1024, 0, s>>>(nn, n, (n - 1) / 2, res);
+    trk::k_select_kth<<<1, 1024, 0, s>>>(nn2, n, (n - 1) / 2, res);
     CK(cudaGetLastError());
     int h[2];
     CK(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    c->launches += 2;
+    c->launches += 3;
     if (h[0]) return TURBOREG_ERR_NONFINITE_INPUT;
     std::memcpy(out_pr, &h[1], sizeof(float));
     return TURBOREG_OK;
