@@ -40,7 +40,7 @@ constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 *
 //   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
 // Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
 constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
-constexpr int SC2_BLOCKS_PER_PAIR = 32;  // 256 warps stride over a pair's dense rows
+constexpr int SC2_BLOCKS_PER_PAIR = 64;  // 512 warps stride over a pair's dense rows
 constexpr int SC2_CLAIM = 4;
 
 // |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned, zero padded) against row
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
 
 // The pivot passes stream the pair's compact O2 edge array (E words) with a grid stride: coalesced,
 // no per-row bookkeeping.
-constexpr int SEL_BLOCKS_PER_PAIR = 32;
+constexpr int SEL_BLOCKS_PER_PAIR = 16;
 
 // Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4).
 // The three edge passes below stream the pair's compact O2 edge array (edges_stride is a multiple of 4
