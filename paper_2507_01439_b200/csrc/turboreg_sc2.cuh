@@ -15,9 +15,9 @@ namespace trk {
 // The result (j << 16 | Ĝ_ij) goes to edges[rowptr(i) + rank]; positive weights feed a 256-bin histogram
 // of Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
 constexpr int SC2_WARPS = 8;
-constexpr int SC2_ROWS_PER_BLOCK = 64;
+constexpr int DEG_ROWS_PER_BLOCK = 64;  // k_degree: rows per 8-warp block
 constexpr int SEL_WARPS = 8;
-constexpr int SEL_ROWS_PER_BLOCK = 64;
+constexpr int SEL_ROWS_PER_BLOCK = 128;
 constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
 constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
 // Row i as a byte map (one byte per column) trades the per-row expansion (~40 instructions per word) for
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(256, 5) k_degree(WS ws) {
     const uint32_t* bits = ws.bits + p * ws.bits_stride;
     unsigned mine = 0;
     int mx = 0;
-    const int row0 = blockIdx.x * SEL_ROWS_PER_BLOCK, row1 = min(row0 + SEL_ROWS_PER_BLOCK, n);
+    const int row0 = blockIdx.x * DEG_ROWS_PER_BLOCK, row1 = min(row0 + DEG_ROWS_PER_BLOCK, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
     auto finish_row = [&](int i, int deg, int ucnt) {  // ucnt: the row's total |U_i|
         uint16_t* L = lists + (int64_t)i * LIST_MAX;
