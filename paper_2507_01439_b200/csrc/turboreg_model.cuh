@@ -173,11 +173,24 @@ __global__ void __launch_bounds__(256) k_nn_dist(const float* xyz, int n, int sp
         }
         __syncthreads();
         const int m = min(NN_TILE, je - j0);
-        for (int t = 0; t < m; ++t) {
+        // two candidates per f32x2 op (each lane half is the same IEEE op as the scalar tree); the point's own
+        // slot is masked after the arithmetic
+        const f2_t X = f2_pack(xi, xi), Y = f2_pack(yi, yi), Z = f2_pack(zi, zi);
+        const int self = i - j0;
+        int t = 0;
+#pragma unroll 8
+        for (; t + 1 < m; t += 2) {
+            const float4 qa = s_p[t], qb = s_p[t + 1];
+            const f2_t dx = f2_sub(X, f2_pack(qa.x, qb.x)), dy = f2_sub(Y, f2_pack(qa.y, qb.y)),
+                       dz = f2_sub(Z, f2_pack(qa.z, qb.z));
+            const f2_t d2 = f2_add(f2_add(f2_mul(dx, dx), f2_mul(dy, dy)), f2_mul(dz, dz));
+            const float lo = (t == self) ? best : lo_f(d2), hi = (t + 1 == self) ? best : hi_f(d2);
+            best = fminf(best, fminf(lo, hi));
+        }
+        if (t < m && t != self) {
             const float4 q = s_p[t];
             const float dx = __fsub_rn(xi, q.x), dy = __fsub_rn(yi, q.y), dz = __fsub_rn(zi, q.z);
-            const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-            if (j0 + t != i) best = fminf(best, d2);
+            best = fminf(best, __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)));
         }
     }
     if (i < n) atomicMin(nn2 + i, __float_as_int(best));
