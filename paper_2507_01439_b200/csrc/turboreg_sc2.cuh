@@ -422,10 +422,11 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int32_t* light = ws.light_list + p * ws.row_stride;
     // stage the group's bitmaps and lists with asynchronous 16-byte copies (all rows in flight at once);
     // per-row meta (i, d, lo)
-    int my_i = 0, my_d = 0;
+    int my_i = 0, my_d = 0, my_lo = 0;
     if (lane < nr) {
         my_i = light[g0 + lane];
         my_d = deg_full[my_i];
+        my_lo = my_d - ws.deg[p * ws.row_stride + my_i];  // neighbours below i: degree minus |U_i|
         meta[4 * lane] = my_i;
         meta[4 * lane + 1] = my_d;
     }
@@ -443,14 +444,6 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
-    int my_lo = 0;
-    for (int r = 0; r < nr; ++r) {
-        const int i = __shfl_sync(FULL, my_i, r), di = __shfl_sync(FULL, my_d, r);
-        int c = 0;
-        for (int t = lane; t < di; t += 32) c += (int)ls[r * LIST_MAX + t] <= i;
-        c = __reduce_add_sync(FULL, (unsigned)c);
-        if (lane == r) my_lo = c;
-    }
     if (lane < nr) {
         meta[4 * lane] = my_i; meta[4 * lane + 1] = my_d; meta[4 * lane + 2] = my_lo;
     }
