@@ -143,12 +143,13 @@ __global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws
     const int K1 = ws.k1, K2 = ws.k2;
     if (pv >= K1) return;
     int4* out = ws.cliq + q * ws.cl_stride + (int64_t)pv * K2;
+    // the pivot slot is read before |P| is known (both loads in flight; slots >= |P| are never used)
+    const int4 pvt = ws.piv[q * ws.piv_stride + pv];
     const int P = ws.st[q].npiv;
     if (pv >= P) {
         for (int r = lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
         return;
     }
-    const int4 pvt = ws.piv[q * ws.piv_stride + pv];
     const int i = pvt.x, j = pvt.y, wij = pvt.z;
     const uint32_t* bits = ws.bits + q * ws.bits_stride;
     const uint32_t* ri = bits + (int64_t)i * W;
