@@ -875,12 +875,11 @@ __global__ void __launch_bounds__(256) k_expand(WS ws) {
             if constexpr (FP4) {  // e2m1: bit k -> nibble k = 0x2 (1.0) or 0 (0.0), 16 bytes per word
                 uint32_t b[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {  // spread byte q's 8 bits to 8 nibbles, then x2 (= 0b0010)
+                for (int q = 0; q < 4; ++q) {  // byte q's 8 bits -> 8 nibbles: bit pairs select bytes of a table
                     uint32_t x = (v >> (8 * q)) & 0xffu;
-                    x = (x | (x << 12)) & 0x000f000fu;
-                    x = (x | (x << 6)) & 0x03030303u;
-                    x = (x | (x << 3)) & 0x11111111u;
-                    b[q] = x << 1;
+                    x = (x | (x << 4)) & 0x0f0fu;  // selector nibble m = bits 2m, 2m+1
+                    x = (x | (x << 2)) & 0x3333u;
+                    b[q] = __byte_perm(0x22200200u, 0u, x);  // 00 -> 0x00, 01 -> 0x02, 10 -> 0x20, 11 -> 0x22
                 }
                 reinterpret_cast<uint4*>(X)[w] = make_uint4(b[0], b[1], b[2], b[3]);
             } else {
