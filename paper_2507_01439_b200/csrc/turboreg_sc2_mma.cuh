@@ -32,7 +32,7 @@ constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larg
 constexpr int MMA_TABLE_PAIRS = 1024;  // pair table in shared memory (larger batches walk global state)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                                (2 * MMA_TABLE_PAIRS + 1) * 4 /*tile prefix + |H| per pair*/ +
-                               2 * MMA_BN * 4 /*heavy ids of the tile columns, 2 buffers*/ + MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + 2 * MMA_EPI_WARPS * 32 * 4;
+                               MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4 /*row bases*/;
 constexpr int MMA_THREADS = 64 + 32 * MMA_EPI_WARPS;
 
 // Instruction descriptor: c_format S32 (bits 4-5 = 2), a/b format u8 (0), both K-major, N>>3 at bit 17,
@@ -168,10 +168,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     // tmem_empty[2] at bars + 144; tmem ptr at bars + 192
     const uint32_t full0 = bars, empty0 = bars + 64, tfull0 = bars + 128, tempty0 = bars + 144, tptr = bars + 192;
     uint8_t* gen_tptr = smem_raw + (tptr - base);
-    int32_t* s_hl = reinterpret_cast<int32_t*>(smem_raw + (bars + 256 - base));  // [2][MMA_BN]
-    uint16_t* s_vt = reinterpret_cast<uint16_t*>(s_hl + 2 * MMA_BN);              // [warps][16][34] (Ĝ < 65536)
-    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);   // [2][warps][32] edge-list bases
-    int32_t* s_tpre = s_eb + 2 * MMA_EPI_WARPS * 32;                                  // [batch + 1] tile prefix
+    uint16_t* s_vt = reinterpret_cast<uint16_t*>(smem_raw + (bars + 256 - base));  // [warps][16][34] (Ĝ < 65536)
+    int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);     // [warps][32] edge-list bases
+    int32_t* s_tpre = s_eb + MMA_EPI_WARPS * 32;                                    // [batch + 1] tile prefix
     int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
     const bool table = batch <= MMA_TABLE_PAIRS;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp: provably uniform
