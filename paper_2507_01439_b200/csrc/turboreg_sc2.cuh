@@ -567,7 +567,7 @@ __device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int
         }
     }
 }
-__global__ void __launch_bounds__(256, 5) k_degree(WS ws) {
+__global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
     const int p = blockIdx.y;
