@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
 // for a < |H| the upper words of row H_a with their exclusive prefix popcounts (UP), from which the
 // tensor-core epilogue reads the O2 test and the edge-list rank of every (H_a, H_b).  One warp per X row.
 template <bool FP4>
-__global__ void __launch_bounds__(256) k_expand(WS ws) {
+__global__ void __launch_bounds__(256, 8) k_expand(WS ws) {
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     if (d.n == 0) return;
