@@ -1,16 +1,21 @@
 #!/usr/bin/env python3
-"""Benchmark: registrations/sec at N=5000 with 1K TurboCliques (K1=1000, K2=2) on 1..8 B200.
+"""Benchmark: registrations/sec at N=5000 with 1K TurboCliques (K1=1000, K2=2) on 1/2/4/8 B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--pairs P] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--sweep 1623 | --pairs P] [--impl reference]
 
-One step = one pass of the whole hot path (compat → SC^2 → pivots → PGS → Kabsch → scoring → argmax)
-over a batch of P synthetic 3DMatch-shaped pairs per GPU (BASELINE.json configs[4] shape with the
-configs[1] parameters; weak scaling: every rank registers its own P pairs).  Inputs are resident in
-HBM when the timed region starts; L2 is flushed (256 MiB write) before every timed step.  Timing is
-CUDA events on the launching stream, max over ranks.  Rank 0 prints one JSON line.
+Workload (BASELINE.json configs[4]): the 1623-pair 3DMatch-shaped sweep (configs[1] parameters,
+N=5000, K1=1000, K2=2), sharded over the N ranks (rank r registers pairs shard_range(1623, N, r)): strong
+scaling, the same total work at every N.  `--pairs P` instead gives every rank its own P pairs (weak
+scaling).  One step = one pass of the whole hot path (compat → SC^2 → pivots → PGS → Kabsch → scoring →
+argmax) over the rank's pairs in one batched call, on the library's default path (CUDA-graph replay, the
+sparse-row SC^2 kernel on a side stream).  Inputs are resident in HBM when the timed region starts; L2 is
+flushed (256 MiB write) before every timed step.  Timing is CUDA events on the launching stream with a
+barrier + synchronize on both sides, max over ranks; rank 0 prints one JSON line.  Per-kernel times come
+from a separate pass over the same batch with per-kernel CUDA events (direct launches, one stream).
 
-`--impl reference` times the CPU oracle (oracle/, the only other place this script executes it) on the
-host cores, a bounded sample of the same workload per step.
+`--gpus N` with no torchrun environment re-launches itself under `torch.distributed.run` with N ranks (one
+per GPU, NCCL).  `--impl reference` times the CPU oracle (oracle/, the only other place this script
+executes it) on the host cores, a bounded sample of the same workload per step.
 """
 from __future__ import annotations
 
@@ -32,7 +37,8 @@ import synth  # noqa: E402
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "registrations/s"
 CFG = synth.CONFIGS["E"]
-PAIRS_PER_GPU = 203  # ceil(1623 / 8): the 3DMatch pair count split over the 8-GPU box
+SWEEP = synth.BATCH_PAIRS  # 1623: the 3DMatch pair count, configs[4]
+MAX_DENSITY = 0.125  # per-pair edge capacity: 1/8 of all N(N-1)/2 pairs (config E measures 4.35 %)
 L2_FLUSH_BYTES = 256 << 20
 SMS = 148
 MMA_FP4 = 1  # dense SC^2 block as tcgen05.mma kind::mxf4 (the library default); 0 = kind::i8
@@ -148,27 +154,23 @@ def clock_sampler(index):
 
 
 # ------------------------------------------------------------------------------------------ workload
-def make_inputs(rank, pairs, n=None, world=1):
-    """This rank's shard of the configs[4] sweep: global pairs shard_range(world·pairs, world, rank)."""
-    from paper_2507_01439_b200.sharding import shard_range
-
+def make_inputs(first, pairs, n=None):
+    """Global pairs [first, first + pairs) of the configs[4] sweep (pair p: seed CFG.seed + p)."""
     n = n or CFG.n
-    b, e = shard_range(world * pairs, world, rank)
-    assert e - b == pairs
     src = np.empty((pairs * n, 3), np.float32)
     dst = np.empty((pairs * n, 3), np.float32)
     gts = []
-    for p in range(pairs):
-        inst = synth.workload_instance(CFG, pair=b + p, n=n)
-        src[p * n:(p + 1) * n] = inst["src"]
-        dst[p * n:(p + 1) * n] = inst["dst"]
+    for k in range(pairs):
+        inst = synth.workload_instance(CFG, pair=first + k, n=n)
+        src[k * n:(k + 1) * n] = inst["src"]
+        dst[k * n:(k + 1) * n] = inst["dst"]
         gts.append((inst["R"], inst["t"]))
     return src, dst, gts
 
 
 def algorithmic_work(tr, res, pairs):
     """Algorithmic work of the last call, summed over its pairs: compat pair tests, the
-    dense tensor-core block's int8 MACs, scoring residual tests."""
+    dense tensor-core block's operations, scoring residual tests, O2 edges."""
     from paper_2507_01439_b200._binding import I_STATE
 
     tests = mma_ops = edges = 0
@@ -215,55 +217,157 @@ def rooflines(kern, work, steps, pk, pairs):
     return out
 
 
-def cpu_sample(seconds=12.0, min_pairs=2):
-    """The oracle as it stands, single-threaded, on config-E pairs until `seconds` elapse."""
+# ------------------------------------------------------------------------------------------ host cores / oracle
+def host_cores():
+    """(usable core count, CPU model line) of this host."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+def _oracle_pair(pair):
+    """One config-E pair through the oracle (a worker of the all-core pool); returns seconds."""
+    import oracle
+
+    inst = synth.workload_instance(CFG, pair=pair)
+    t0 = time.perf_counter()
+    r = oracle.estimate(inst["src"], inst["dst"], CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold)
+    dt = time.perf_counter() - t0
+    assert r["status"] == 0
+    return dt
+
+
+def _oracle_pool(workers):
+    import multiprocessing as mp
+
+    return mp.get_context("spawn").Pool(workers)  # spawn: the parent may hold a CUDA context
+
+
+def cpu_sample():
+    """The oracle as it stands on the host: (i) throughput of a process pool over all usable cores on a
+    fixed config-E sample (2 pairs per worker); (ii) single-core latency per config A-D."""
     import oracle
 
     oracle.build()
-    done, t0 = 0, time.perf_counter()
-    while True:
-        inst = synth.workload_instance(CFG, pair=10_000 + done)
-        r = oracle.estimate(inst["src"], inst["dst"], CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold)
-        assert r["status"] == 0
-        done += 1
-        el = time.perf_counter() - t0
-        if done >= min_pairs and el >= seconds:
-            break
-    return {"value": done / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{done} config-E pairs (N=5000, K1=1000, K2=2, seeds {CFG.seed + 10000}..), single thread, "
-                      f"{el:.1f} s"}
+    cores, model = host_cores()
+    workers = max(1, min(cores, 64))
+    npairs = 2 * workers
+    with _oracle_pool(workers) as pool:
+        pool.map(_oracle_pair, range(10_000, 10_000 + workers))  # warm the workers (import, library load)
+        t0 = time.perf_counter()
+        per = pool.map(_oracle_pair, range(20_000, 20_000 + npairs), chunksize=1)
+        wall = time.perf_counter() - t0
+    lat = {}
+    for key in "ABCD":
+        c = synth.CONFIGS[key]
+        inst = synth.workload_instance(c, pair=0)
+        reps = 3 if c.n <= 1000 else 1
+        ts = []
+        for _ in range(reps):
+            t1 = time.perf_counter()
+            oracle.estimate(inst["src"], inst["dst"], c.tau, c.k1, c.k2, c.inlier_threshold)
+            ts.append(time.perf_counter() - t1)
+        lat[f"{key} ({c.name}, N={c.n}, K1={c.k1})"] = round(1e3 * float(np.median(ts)), 2)
+    return {"value": npairs / wall, "unit": UNIT, "cores": workers, "kind": "oracle",
+            "sample": f"{npairs} config-E pairs (N=5000, K1=1000, K2=2, seeds {CFG.seed + 20000}..), a process pool "
+                      f"of {workers} single-threaded oracle workers, {wall:.1f} s wall; mean {np.mean(per):.2f} s per "
+                      f"pair per core",
+            "host": {"usable_cores": cores, "cpu_model": model},
+            "single_core_latency_ms": lat}
 
 
 # ------------------------------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The oracle, as it stands, on all usable host cores: each step registers one config-E pair per worker
+    (a bounded sample of the workload).  Under torchrun only rank 0 runs it."""
     if rank != 0:
         return
     import oracle
 
     oracle.build()
-    cores = 1
+    cores, model = host_cores()
+    workers = max(1, min(cores, 64))
     times = []
-    for step in range(args.warmup + args.steps):
-        inst = synth.workload_instance(CFG, pair=20_000 + step)
-        t0 = time.perf_counter()
-        r = oracle.estimate(inst["src"], inst["dst"], CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold)
-        dt = time.perf_counter() - t0
-        assert r["status"] == 0
-        if step >= args.warmup:
-            times.append(dt)
+    with _oracle_pool(workers) as pool:
+        nxt = 30_000
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_pair, range(nxt, nxt + workers), chunksize=1)
+            dt = time.perf_counter() - t0
+            nxt += workers
+            if step >= args.warmup:
+                times.append(dt)
     total = sum(times)
-    value = len(times) / total
+    value = workers * len(times) / total
+    sample = (f"{workers} config-E pairs per step (one per worker), {len(times)} timed steps, process pool of "
+              f"{workers} single-threaded C++ oracle workers")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * total / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[4] 3DMatch-shaped pairs (N=5000, K1=1000, K2=2); one pair per step",
-                   "pairs_per_step": 1},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{len(times)} config-E pairs, one per step, single-threaded C++ oracle"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"configs[4] 3DMatch-shaped pairs (N=5000, K1=1000, K2=2); bounded sample",
+                   "pairs_per_step": workers},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle", "sample": sample,
+                         "host": {"usable_cores": cores, "cpu_model": model}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ multi-rank plumbing
+def _shard(args, rank, world):
+    """(first global pair, pairs on this rank, pairs over all ranks, scaling)."""
+    from paper_2507_01439_b200.sharding import shard_range
+
+    if args.pairs:
+        return rank * args.pairs, args.pairs, world * args.pairs, "weak"
+    b, e = shard_range(args.sweep, world, rank)
+    return b, e - b, args.sweep, "strong"
+
+
+def _max_over_ranks(x, world, device):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_selftest_gloo(args, rank, world):
+    """CPU check of the spawn / shard / gather / max-over-ranks path (gloo; no GPU, no method arithmetic):
+    every rank fills result records for its shard with values derived from the global pair index, and
+    rank 0 checks the gathered array is every pair exactly once in global order."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_01439_b200._binding import RESULT_DTYPE
+    from paper_2507_01439_b200.sharding import gather_results
+
+    first, pairs, total, scaling = _shard(args, rank, world)
+    rec = np.zeros(pairs, RESULT_DTYPE)
+    rec["inlier_count"] = np.arange(first, first + pairs)
+    rec["num_edges"] = 10**9 + np.arange(first, first + pairs)
+    dt = _max_over_ranks(1.0 + rank, world, torch.device("cpu"))
+    allres = gather_results(rec, total) if world > 1 else rec
+    if rank == 0:
+        ok = bool((allres["inlier_count"] == np.arange(total)).all() and
+                  (allres["num_edges"] == 10**9 + np.arange(total)).all())
+        print(json.dumps({"selftest": "gloo", "n_gpus": world, "world": world, "pairs": total, "scaling": scaling,
+                          "max_over_ranks": dt, "ok": ok}), flush=True)
+    if world > 1:
+        dist.barrier()
 
 
 # ------------------------------------------------------------------------------------------ CUDA arm
@@ -272,12 +376,13 @@ def run_cuda(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2507_01439_b200 import RESULT_DTYPE, TurboReg
+    from paper_2507_01439_b200._binding import F_KERNEL_TIMING
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    pairs = args.pairs
+    first, pairs, total, scaling = _shard(args, rank, world)
     n = CFG.n
-    src_h, dst_h, gts = make_inputs(rank, pairs, world=world)
+    src_h, dst_h, gts = make_inputs(first, pairs)
     off = (np.arange(pairs) * n).astype(np.int64)
     nn = np.full(pairs, n, np.int32)
     src_d = torch.from_numpy(src_h).to(dev)
@@ -287,7 +392,7 @@ def run_cuda(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)  # explicit stream: kernels, events and the L2 flush all on it
     torch.cuda.set_stream(stream)
     tr = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=pairs, device=local_rank,
-                  kernel_timing=True)
+                  max_density=MAX_DENSITY)
     tr.set_option("mma_fp4", MMA_FP4)  # the library default, stated so the roofline below counts the right tiles
 
     def step():
@@ -300,16 +405,17 @@ def run_cuda(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # correctness guard on the warm-up output (planted recovery)
-    res = out_d.cpu().numpy().view(RESULT_DTYPE)
-    ok = sum(int(r["status"] == 0 and synth.rotation_error_deg(r["R"].reshape(3, 3), g[0]) <= 5) for r, g in zip(res, gts))
+    res = out_d.cpu().numpy().view(RESULT_DTYPE).copy()
+    if not (res["status"] == 0).all():
+        raise RuntimeError(f"rank {rank}: pair statuses {np.unique(res['status'], return_counts=True)}")
+    ok = sum(int(synth.rotation_error_deg(r["R"].reshape(3, 3), g[0]) <= 5) for r, g in zip(res, gts))
 
+    # ---- timed region: the default path (CUDA-graph replay + the side stream), device-resident inputs
     clocks = clock_sampler(local_rank)
     clocks.start()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = tr.launch_count
-    tr.profile_begin()
     barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
@@ -321,169 +427,187 @@ def run_cuda(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     wall = time.perf_counter() - wall0
-    kern = tr.profile_end()
     launches = tr.launch_count - launches0
     clk = clocks.stop()
     dev_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms_max = float(t.item())
-    value = world * pairs * args.steps / (dev_ms_max / 1000.0)
+    dev_ms_max = _max_over_ranks(dev_ms, world, dev)
+    value = total * args.steps / (dev_ms_max / 1000.0)
+    assert out_d.cpu().numpy().view(RESULT_DTYPE).tobytes() == res.tobytes(), "results changed between steps"
+
+    # ---- per-kernel times: a separate pass over the same batch with per-kernel CUDA events (direct launches)
+    kp = max(1, min(args.steps, 5))
+    tr.set_params(flags=F_KERNEL_TIMING)
+    step()
+    torch.cuda.synchronize()
+    tr.profile_begin()
+    for k in range(kp):
+        flush.fill_(float(k))
+        step()
+    torch.cuda.synchronize()
+    kern = tr.profile_end()
+    tr.set_params(flags=0)
+    work = algorithmic_work(tr, res, pairs)
 
     # ---- end-to-end through the public API with pinned HOST buffers (H2D + D2H inside the timed region)
     src_p = torch.from_numpy(src_h).pin_memory()
     dst_p = torch.from_numpy(dst_h).pin_memory()
-    tr_e2e = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=pairs, device=local_rank)
     for _ in range(max(1, args.warmup)):
-        tr_e2e.register_batch(src_p, dst_p, off, nn)
+        tr.register_batch(src_p, dst_p, off, nn)
     e2e_times = []
     for k in range(args.steps):
         flush.fill_(float(k))
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        host_res = tr_e2e.register_batch(src_p, dst_p, off, nn)  # blocking: copies in, kernels, result out
+        host_res = tr.register_batch(src_p, dst_p, off, nn)  # blocking: copies in, kernels, result out
         e2e_times.append(time.perf_counter() - t0)
-    te = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * pairs * args.steps / float(te.item())
-    assert (host_res["status"] == 0).all()
-    tr_e2e.close()
-
-    # ---- single-pair latency (configs[1]) for context
-    tr1 = TurboReg(CFG.tau, CFG.k1, CFG.k2, CFG.inlier_threshold, max_n=n, max_batch=1, device=local_rank)
-    s1, d1 = src_d[:n].contiguous(), dst_d[:n].contiguous()
-    o1 = torch.zeros(RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        tr1.register_batch(s1, d1, off[:1], nn[:1], out=o1, stream=stream.cuda_stream)
-    lat = []
-    for _ in range(10):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        tr1.register_batch(s1, d1, off[:1], nn[:1], out=o1, stream=stream.cuda_stream)
-        b.record(stream)
-        torch.cuda.synchronize()
-        lat.append(a.elapsed_time(b))
-    tr1.close()
-
-    # ---- single-pair latency of configs A-D, device-resident inputs, median of 10
-    lat_cfg = {}
-    if rank == 0:
-        for key in "ABCD":
-            c = synth.CONFIGS[key]
-            inst = synth.workload_instance(c, pair=0)
-            nk = inst["src"].shape[0]
-            sk = torch.from_numpy(inst["src"]).to(dev)
-            dk = torch.from_numpy(inst["dst"]).to(dev)
-            trk_ = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=nk, max_batch=1, device=local_rank)
-            ok_ = np.zeros(1, np.int64)
-            nk_ = np.full(1, nk, np.int32)
-            for _ in range(3):
-                trk_.register_batch(sk, dk, ok_, nk_, out=o1, stream=stream.cuda_stream)
-            ts = []
-            for _ in range(10):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                trk_.register_batch(sk, dk, ok_, nk_, out=o1, stream=stream.cuda_stream)
-                b.record(stream)
-                torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            trk_.close()
-            lat_cfg[f"{key} ({c.name}, N={nk}, K1={c.k1})"] = round(float(np.median(ts)), 4)
-
-    # ---- NEXT(4) context: equal-budget 3-point RANSAC (K1*K2 sampled triples) vs TurboReg on config-C pairs
-    # (3DLoMatch-shaped, 5 % inliers), host inputs, wall-clock per call; not part of the timed step
-    ransac = None
-    if rank == 0:
-        c = synth.CONFIGS["C"]
-        budget = c.k1 * c.k2
-        trr = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=c.n, max_batch=1, device=local_rank)
-        rec_t = rec_r = 0
-        inl_t, inl_r, t_t, t_r = [], [], [], []
-        npairs = 10
-        for q in range(npairs):
-            inst = synth.workload_instance(c, pair=500 + q)
-            trr.register(inst["src"], inst["dst"])  # warm (graph capture on the first call)
-            t0 = time.perf_counter()
-            rt = trr.register(inst["src"], inst["dst"])
-            t1 = time.perf_counter()
-            rr = trr.ransac(inst["src"], inst["dst"], budget, seed=q)
-            t2 = time.perf_counter()
-            t_t.append(t1 - t0)
-            t_r.append(t2 - t1)
-            inl_t.append(rt["inlier_count"])
-            inl_r.append(rr["inlier_count"])
-            rec_t += int(rt["status"] == 0 and synth.rotation_error_deg(rt["R"].reshape(3, 3), inst["R"]) <= 5)
-            rec_r += int(rr["status"] == 0 and synth.rotation_error_deg(rr["R"].reshape(3, 3), inst["R"]) <= 5)
-        trr.close()
-        # NEXT(3): point-cloud resolution (tau = 0.25 pr) of device-resident clouds, CUDA-event timed
-        res_ms = {}
-        for npts in (5000, 32768):
-            trp = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=npts, max_batch=1, device=local_rank)
-            cloud = torch.from_numpy(
-                np.random.default_rng(npts).uniform(-1.5, 1.5, size=(npts, 3)).astype(np.float32)).to(dev)
-            trp.point_resolution(cloud)
-            ts = []
-            for _ in range(5):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                trp.point_resolution(cloud)
-                b.record()
-                torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            trp.close()
-            res_ms[f"N={npts}"] = round(float(np.median(ts)), 4)
-        ransac = {"config": f"C ({c.name}), {npairs} pairs, budget K1*K2 = {budget} hypotheses each",
-                  "point_resolution_ms": res_ms,
-                  "turboreg": {"recovered_re_le_5deg": rec_t, "mean_inliers": float(np.mean(inl_t)),
-                               "ms_per_pair_host_io": round(1e3 * float(np.median(t_t)), 3)},
-                  "ransac": {"recovered_re_le_5deg": rec_r, "mean_inliers": float(np.mean(inl_r)),
-                             "ms_per_pair_host_io": round(1e3 * float(np.median(t_r)), 3)}}
+    e2e_value = total * args.steps / _max_over_ranks(sum(e2e_times), world, dev)
+    assert host_res.tobytes() == res.tobytes(), "host-input results differ from device-input results"
+    ws_bytes = tr.workspace_bytes
+    tr.close()
 
     # gather per-pair results (the only collective: NCCL all_gather of fixed-size records, outside timing)
     if world > 1:
         from paper_2507_01439_b200.sharding import gather_results
 
-        allres = gather_results(out_d, world * pairs)
+        allres = gather_results(res, total)
         all_ok = int((allres["status"] == 0).sum())
     else:
         all_ok = int((res["status"] == 0).sum())
 
+    context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 else None
     if rank != 0:
         return
-    work = algorithmic_work(tr, res, pairs)
     pk = peaks()
-    roofs = rooflines(kern, work, args.steps, pk, pairs)
+    roofs = rooflines(kern, work, kp, pk, pairs)
     # the roofline line describes the dominant kernel (by measured time) among those with a defined bound
     dom_name = max(roofs, key=lambda k: kern[k][0]) if roofs else None
     roof = dict(roofs[dom_name], kernel=dom_name) if dom_name else None
+    kms = {k: v[0] / kp for k, v in kern.items() if v[1]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[4]: batch of 3DMatch-shaped pairs (configs[1] parameters)",
-                   "pairs_per_gpu": pairs, "N": n, "K1": CFG.k1, "K2": CFG.k2, "tau_m": CFG.tau,
-                   "inlier_threshold_m": CFG.inlier_threshold, "inlier_ratio": CFG.inlier_ratio,
-                   "l2": "flushed before every timed step (256 MiB write)", "parallelism": f"dp{world} (pairs)"},
+        "config": {"workload": f"configs[4]: {total} 3DMatch-shaped pairs (configs[1] parameters)"
+                               + (f", {args.pairs} per GPU" if args.pairs else f", sharded over {world} GPU(s)"),
+                   "pairs_total": total, "pairs_rank0": pairs, "N": n, "K1": CFG.k1, "K2": CFG.k2,
+                   "tau_m": CFG.tau, "inlier_threshold_m": CFG.inlier_threshold, "inlier_ratio": CFG.inlier_ratio,
+                   "l2": "flushed before every timed step (256 MiB write); inputs 24 B x N per pair",
+                   "parallelism": f"dp{world} (pairs)", "launch_path": "CUDA graph replay + side stream (default)",
+                   "edge_capacity": f"{MAX_DENSITY} of N(N-1)/2 per pair",
+                   "workspace_bytes_per_pair": ws_bytes / pairs},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(src_h.nbytes + dst_h.nbytes),
                 "d2h_bytes_per_step": int(pairs * RESULT_DTYPE.itemsize)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_kernels": roofs,
-        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
-        "single_pair_latency_ms": float(np.median(lat)),
-        "single_pair_latency_ms_configs": lat_cfg,
-        "ransac_equal_budget": ransac,
-        "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{pairs * world}",
+        "kernels_ms_per_step": kms,
+        "kernel_pass": {"what": "per-kernel CUDA events, direct launches on one stream, same batch",
+                        "steps": kp, "sum_ms_per_step": sum(kms.values())},
+        "planted_recovery": f"{ok}/{pairs} (rank 0, RE<=5deg); all ranks status ok {all_ok}/{total}",
         "wall_s_timed_region": wall,
     }
+    line.update(context or {})
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
     print(json.dumps(line), flush=True)
-    tr.close()
+
+
+def _median_latency(fn, stream, reps=10, warm=3):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return round(float(np.median(ts)), 4)
+
+
+def single_pair_context(rank, local_rank, stream, src_d, dst_d):
+    """Context numbers (not the metric): single-pair latency of configs A-D and of large N, RANSAC vs TurboReg
+    at an equal budget, point-cloud resolution timing."""
+    import torch
+
+    from paper_2507_01439_b200 import RESULT_DTYPE, TurboReg
+
+    dev = src_d.device
+    o1 = torch.zeros(RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    one = np.zeros(1, np.int64)
+    lat_cfg = {}
+    for key in "ABCD":
+        c = synth.CONFIGS[key]
+        inst = synth.workload_instance(c, pair=0)
+        nk = inst["src"].shape[0]
+        sk, dk = torch.from_numpy(inst["src"]).to(dev), torch.from_numpy(inst["dst"]).to(dev)
+        t = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=nk, max_batch=1, device=local_rank)
+        nk_ = np.full(1, nk, np.int32)
+        lat_cfg[f"{key} ({c.name}, N={nk}, K1={c.k1})"] = _median_latency(
+            lambda: t.register_batch(sk, dk, one, nk_, out=o1, stream=stream.cuda_stream), stream)
+        t.close()
+    # large N (the NEXT(1) question): one 3DMatch-shaped pair per call, configs[1] parameters
+    lat_big = {}
+    c = synth.CONFIGS["B"]
+    for nb in (10_000, 20_000, 32_768):
+        inst = synth.workload_instance(c, pair=0, n=nb)
+        sk, dk = torch.from_numpy(inst["src"]).to(dev), torch.from_numpy(inst["dst"]).to(dev)
+        t = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=nb, max_batch=1, device=local_rank)
+        nk_ = np.full(1, nb, np.int32)
+        ms = _median_latency(lambda: t.register_batch(sk, dk, one, nk_, out=o1, stream=stream.cuda_stream), stream,
+                             reps=5, warm=2)
+        r = o1.cpu().numpy().view(RESULT_DTYPE)[0]
+        lat_big[f"N={nb}"] = {"ms": ms, "status": int(r["status"]), "edges": int(r["num_edges"]),
+                              "recovered": bool(synth.rotation_error_deg(r["R"].reshape(3, 3), inst["R"]) <= 5)}
+        t.close()
+    # NEXT(4): equal-budget 3-point RANSAC (K1*K2 sampled triples) vs TurboReg on config-C pairs (5 % inliers),
+    # host inputs, wall-clock per call; not part of the timed step
+    c = synth.CONFIGS["C"]
+    budget = c.k1 * c.k2
+    trr = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=c.n, max_batch=1, device=local_rank)
+    rec_t = rec_r = 0
+    inl_t, inl_r, t_t, t_r = [], [], [], []
+    npairs = 10
+    for q in range(npairs):
+        inst = synth.workload_instance(c, pair=500 + q)
+        trr.register(inst["src"], inst["dst"])  # warm (graph capture on the first call)
+        t0 = time.perf_counter()
+        rt = trr.register(inst["src"], inst["dst"])
+        t1 = time.perf_counter()
+        rr = trr.ransac(inst["src"], inst["dst"], budget, seed=q)
+        t2 = time.perf_counter()
+        t_t.append(t1 - t0)
+        t_r.append(t2 - t1)
+        inl_t.append(rt["inlier_count"])
+        inl_r.append(rr["inlier_count"])
+        rec_t += int(rt["status"] == 0 and synth.rotation_error_deg(rt["R"].reshape(3, 3), inst["R"]) <= 5)
+        rec_r += int(rr["status"] == 0 and synth.rotation_error_deg(rr["R"].reshape(3, 3), inst["R"]) <= 5)
+    # NEXT(3): point-cloud resolution (tau = 0.25 pr) of device-resident clouds, CUDA-event timed
+    res_ms = {}
+    for npts in (5000, 32768):
+        cloud = torch.from_numpy(
+            np.random.default_rng(npts).uniform(-1.5, 1.5, size=(npts, 3)).astype(np.float32)).to(dev)
+        trr.point_resolution(cloud)
+        ts = []
+        for _ in range(5):  # blocking call on the context's own stream: wall clock around it
+            t0 = time.perf_counter()
+            trr.point_resolution(cloud)
+            ts.append(time.perf_counter() - t0)
+        res_ms[f"N={npts}"] = round(1e3 * float(np.median(ts)), 4)
+    trr.close()
+    ransac = {"config": f"C ({c.name}), {npairs} pairs, budget K1*K2 = {budget} hypotheses each",
+              "point_resolution_ms": res_ms,
+              "turboreg": {"recovered_re_le_5deg": rec_t, "mean_inliers": float(np.mean(inl_t)),
+                           "ms_per_pair_host_io": round(1e3 * float(np.median(t_t)), 3)},
+              "ransac": {"recovered_re_le_5deg": rec_r, "mean_inliers": float(np.mean(inl_r)),
+                         "ms_per_pair_host_io": round(1e3 * float(np.median(t_r)), 3)}}
+    return {"single_pair_latency_ms_configs": lat_cfg, "single_pair_latency_ms_large_n": lat_big,
+            "ransac_equal_budget": ransac}
 
 
 def ncu_traffic(kernel):
@@ -500,31 +624,66 @@ def ncu_traffic(kernel):
     return None
 
 
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def respawn_under_torchrun(ngpus):
+    """`--gpus N` without a torchrun environment: re-launch this command as N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--pairs", type=int, default=PAIRS_PER_GPU)
+    ap.add_argument("--sweep", type=int, default=SWEEP, help="total pairs of the strong-scaling sweep (configs[4])")
+    ap.add_argument("--pairs", type=int, default=0, help="weak scaling: this many pairs per GPU instead of --sweep")
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--selftest-gloo", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus < 1 or args.steps < 1 or args.warmup < 0:
+        ap.error("bad --gpus/--steps/--warmup")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        respawn_under_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
+    import torch
+    import torch.distributed as dist
 
+    if args.selftest_gloo:
+        if world > 1:
+            dist.init_process_group("gloo")
+        run_selftest_gloo(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    if world > 1:
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {torch.cuda.device_count()} visible")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines show the rank count
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_cuda(args, rank, world, local_rank)
     if world > 1:
-        import torch.distributed as dist
-
         dist.destroy_process_group()
 
 

@@ -45,8 +45,17 @@ typedef enum {
     TURBOREG_ERR_NO_HYPOTHESIS = 5,    /* no pivot, no clique, or every clique degenerate;
                                           R, t are all zeros — never a fabricated transform  — per pair */
     TURBOREG_ERR_CUDA = 6,             /* a CUDA runtime error (whole call)                              */
-    TURBOREG_ERR_OUT_OF_MEMORY = 7     /* workspace allocation failed at create/set_params (whole call) */
+    TURBOREG_ERR_OUT_OF_MEMORY = 7,    /* workspace allocation failed at create/set_params/set_option
+                                          (whole call; the context keeps its previous workspace)        */
+    TURBOREG_ERR_EDGE_CAPACITY = 8     /* the pair's compatibility graph has more undirected edges than the
+                                          per-pair edge capacity fixed at create (turboreg_create_ex):
+                                          nothing after the graph is computed; out.num_edges holds the
+                                          pair's true edge count so the caller can size a new context
+                                                                                            — per pair */
 } turboreg_status;
+
+/* Largest cloud accepted by turboreg_point_resolution (O(n^2) distance evaluations). */
+#define TURBOREG_MAX_CLOUD_POINTS (1 << 21)
 
 /* turboreg_params.flags */
 #define TURBOREG_F_STAGE_TIMING 0x1u  /* fill turboreg_result.stage_ms (CUDA events; adds ~12 events)  */
@@ -86,19 +95,37 @@ typedef struct {
     int64_t num_edges;            /* undirected edges of C(τ)                                            */
 } turboreg_result;
 
-/* Create a context on CUDA device `device` able to register up to `max_batch` pairs of up to `max_n`
- * correspondences per call.  All device workspace is allocated here (no allocation on the register
- * path); its size grows as max_batch · max_n² / 2 · 2 bytes (SC^2 weights) + max_batch · max_n² / 8.
- * On success *out receives the context (caller owns it; release with turboreg_destroy). */
+/* Create a context on CUDA device `device` for the problem of P:116-118 (given the putative correspondences
+ * of a pair, estimate T in SE(3)) with the parameters of Eq. 1 (tau), Eq. 4 (k1), Eq. 7 (k2) and g(.) of
+ * P:284-287 (inlier_threshold); SPEC S:47-51 (EstimatorParams) for the parameter set.  The context can
+ * register up to `max_batch` pairs of up to `max_n` correspondences per call (3 <= max_n <= 32768, the
+ * uint16 index range of the O2 edge lists; 1 <= max_batch <= 65535).  All device workspace is allocated
+ * here, in one allocation (no allocation on the register path): per pair about max_n²/8 bytes of bit rows
+ * (Eq. 1), 4 bytes per O2 edge of capacity (Eq. 2 weights in compact rows, Def. 2), the tensor-core operand
+ * block (≈ 2048 × max_n/2 bytes) and O(max_n + k1·k2) more; turboreg_workspace_bytes reports the total.
+ * turboreg_create reserves the complete-graph edge capacity max_n(max_n−1)/2 (no pair can overflow);
+ * turboreg_create_ex takes `max_edges` per pair instead (0 = complete graph), e.g. a density bound for large
+ * batches — pairs with more edges report TURBOREG_ERR_EDGE_CAPACITY.  On success *out receives the context
+ * (caller owns it; release with turboreg_destroy); on failure nothing is allocated and *out is NULL.
+ * Errors: invalid params / sizes → INVALID_ARGUMENT; no such device → CUDA; allocation → OUT_OF_MEMORY. */
 turboreg_status turboreg_create(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
                                 turboreg_ctx** out);
+turboreg_status turboreg_create_ex(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
+                                   int64_t max_edges, turboreg_ctx** out);
 
-/* Replace the parameters; reallocates the pivot/clique workspace if K1·K2 grows. */
+/* Replace the parameters (same meaning and validation as at create; e.g. tau = 0.25 · the point-cloud
+ * resolution, after turboreg_point_resolution).  Waits for the context's previous call to finish.
+ * A change of k1, k1·k2, graph_mode or whether tau_base is set reallocates the workspace: the new one is
+ * allocated before the old one is freed, and on OUT_OF_MEMORY the context keeps its old parameters and
+ * workspace (still usable).  Errors: INVALID_ARGUMENT (params rejected, nothing changed), OUT_OF_MEMORY. */
 turboreg_status turboreg_set_params(turboreg_ctx* ctx, const turboreg_params* params);
 
-/* Register one pair.  src_xyz, dst_xyz: N×3 float32 row-major (x_i and y_i), HOST or DEVICE pointers
- * (detected).  Blocking: on return *out (host) holds the result.  Per-pair failures (2/3/4/5) are
- * returned as the function value AND in out->status. */
+/* Register one pair: the whole hot path (Fig. 2 caption P:99-107; Alg. 1 P:256-278 then Eq. 9),
+ * result as in SPEC S:53-58 (RegistrationResult).  src_xyz, dst_xyz: N×3 float32 row-major (x_i and y_i,
+ * correspondence order preserved — O2 depends on it), HOST or DEVICE pointers (detected; the caller
+ * keeps ownership).  Runs on the context's own stream and blocks: on return *out (host) holds the result.
+ * Per-pair failures (2/3/4/5/8) are returned as the function value AND in out->status; a device `out`
+ * → INVALID_ARGUMENT. */
 turboreg_status turboreg_register(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n,
                                   turboreg_result* out);
 
@@ -106,9 +133,9 @@ turboreg_status turboreg_register(turboreg_ctx* ctx, const float* src_xyz, const
  * SPEC S:163-171 estimate_resolution): *out_pr = the median over the n points of the distance to each
  * point's nearest other point, distances in the float32 tree of reading r1, the lower median (element
  * (n-1)/2 of the sorted distances, reading r22).  xyz: n×3 float32 row-major, HOST or DEVICE (detected);
- * blocking.  Errors: n < 2 or a null pointer → TURBOREG_ERR_INVALID_ARGUMENT; n > max_n →
- * TURBOREG_ERR_TOO_MANY_POINTS; a non-finite coordinate → TURBOREG_ERR_NONFINITE_INPUT (*out_pr untouched).
- * Uses the context's device and input staging area (not concurrently with another call on it). */
+ * blocking.  Errors: n < 2, n > TURBOREG_MAX_CLOUD_POINTS or a null pointer → TURBOREG_ERR_INVALID_ARGUMENT;
+ * a non-finite coordinate → TURBOREG_ERR_NONFINITE_INPUT (*out_pr untouched).  n is independent of max_n: the call uses
+ * its own device buffers (grown on demand), after the context's previous call has finished. */
 turboreg_status turboreg_point_resolution(turboreg_ctx* ctx, const float* xyz, int32_t n, float* out_pr);
 
 /* Equal-budget 3-point RANSAC baseline (SPEC S:324-332 — not part of TurboReg):
@@ -124,17 +151,24 @@ turboreg_status turboreg_point_resolution(turboreg_ctx* ctx, const float* xyz, i
 turboreg_status turboreg_ransac(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n, int32_t iters,
                                 uint64_t seed, turboreg_result* out);
 
-/* Register `batch` independent pairs in one pass.  Pair p uses points [offsets[p], offsets[p] + n[p]) of
- * src_xyz / dst_xyz (N×3 float32, host or device).  offsets and n are HOST arrays.  out: `batch`
- * results, HOST or DEVICE pointer.  stream: a cudaStream_t (NULL = the context's own stream).
+/* Register `batch` independent pairs in one pass (the pairs of a sweep such as 3DMatch's 1623, are
+ * independent problems of P:116-118).  Pair p uses points [offsets[p], offsets[p] + n[p]) of
+ * src_xyz / dst_xyz (N×3 float32, host or device; the caller guarantees those rows exist — the C ABI cannot
+ * check buffer extents).  offsets and n are HOST arrays.  out: `batch` results (>= batch·sizeof(result)
+ * bytes), HOST or DEVICE pointer.  stream: a cudaStream_t (NULL = the context's own stream).
  * With a host `out` the call blocks until the results are in `out`; with a device `out` and device
- * inputs it is fully asynchronous on `stream`.  Per-pair failures go into out[p].status and the call
- * returns TURBOREG_OK; CUDA errors are returned for the whole call. */
+ * inputs it is asynchronous on `stream` (the caller must keep inputs alive and unmodified until the stream
+ * reaches that point).  Consecutive calls may use different streams: each call's stream first waits for
+ * the previous call on this context (the workspace is shared), and host-side descriptor staging is a ring
+ * that is never overwritten before its copy has run.  A context is not thread-safe; independent contexts
+ * may run concurrently.  Per-pair failures go into out[p].status and the call returns TURBOREG_OK;
+ * argument errors (null pointer, batch outside [1, max_batch], negative offset or n) return
+ * INVALID_ARGUMENT before anything is launched; CUDA errors are returned for the whole call. */
 turboreg_status turboreg_register_batch(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz,
                                         const int64_t* offsets, const int32_t* n, int32_t batch,
                                         turboreg_result* out, void* stream);
 
-/* Release the context and all its device memory.  NULL is ignored. */
+/* Release the context and all its device memory, after its last call has finished.  NULL is ignored. */
 void turboreg_destroy(turboreg_ctx* ctx);
 
 /* Static, human-readable name of a status. */

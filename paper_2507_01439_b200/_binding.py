@@ -30,6 +30,10 @@ class Status(enum.IntEnum):
     NO_HYPOTHESIS = 5
     CUDA = 6
     OUT_OF_MEMORY = 7
+    EDGE_CAPACITY = 8
+
+
+PER_PAIR_STATUSES = (0, 2, 3, 4, 5, 8)  # statuses of a pair (the call itself succeeded)
 
 
 F_STAGE_TIMING = 0x1
@@ -98,6 +102,7 @@ def library():
     lib = ctypes.CDLL(_LIB_PATH)
     P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
     lib.turboreg_create.argtypes = [ctypes.POINTER(Params), ctypes.c_int, i32, i32, ctypes.POINTER(P)]
+    lib.turboreg_create_ex.argtypes = [ctypes.POINTER(Params), ctypes.c_int, i32, i32, i64, ctypes.POINTER(P)]
     lib.turboreg_set_params.argtypes = [P, ctypes.POINTER(Params)]
     lib.turboreg_register.argtypes = [P, P, P, i32, ctypes.POINTER(Result)]
     lib.turboreg_ransac.argtypes = [P, P, P, i32, i32, ctypes.c_uint64, ctypes.POINTER(Result)]
@@ -117,9 +122,9 @@ def library():
     lib.turboreg_launch_count.restype = i64
     lib.turboreg_workspace_bytes.argtypes = [P]
     lib.turboreg_workspace_bytes.restype = u64
-    for name in ("turboreg_create", "turboreg_set_params", "turboreg_register", "turboreg_register_batch",
+    for name in ("turboreg_create", "turboreg_create_ex", "turboreg_set_params", "turboreg_register", "turboreg_register_batch",
                  "turboreg_get_intermediates", "turboreg_pgs_from_adjacency", "turboreg_profile_begin",
-                 "turboreg_profile_end"):
+                 "turboreg_profile_end", "turboreg_point_resolution", "turboreg_ransac"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -132,6 +137,20 @@ def _check(st, what):
 
 def _is_torch_cuda(x):
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _points(x, what):
+    """Validate an (N, 3) point array (numpy or torch); returns N."""
+    shape = tuple(x.shape)
+    if len(shape) != 2 or shape[1] != 3:
+        raise ValueError(f"{what} must have shape (N, 3), got {shape}")
+    return int(shape[0])
+
+
+def _nbytes(x):
+    if type(x).__module__.startswith("torch"):
+        return int(x.numel()) * int(x.element_size())
+    return int(np.asarray(x).nbytes)
 
 
 def _ptr(x, dtype=None):
@@ -155,15 +174,22 @@ class TurboReg:
 
     def __init__(self, tau, k1=1000, k2=2, inlier_threshold=0.1, *, tau_base=0.0, graph_mode=0,
                  max_n=5000, max_batch=1, device=0, stage_timing=False, kernel_timing=False, hyp_errors=False,
-                 rank_metric="in"):
+                 rank_metric="in", max_edges=0, max_density=None):
+        """``max_edges``: per-pair O2 edge capacity (0 = complete graph, never overflows); ``max_density``
+        (fraction of the max_n(max_n-1)/2 possible edges) is the same bound as a ratio.  Pairs with more
+        edges report status EDGE_CAPACITY (include/turboreg.h, turboreg_create_ex)."""
         self._lib = library()
         flags = (F_STAGE_TIMING if stage_timing else 0) | (F_KERNEL_TIMING if kernel_timing else 0)
         flags |= (F_HYP_ERRORS if hyp_errors else 0) | {"in": 0, "mae": F_RANK_MAE, "mse": F_RANK_MSE}[rank_metric]
         self.params = Params(float(tau), float(tau_base), int(k1), int(k2), float(inlier_threshold),
                              int(graph_mode), flags)
+        if max_density is not None:
+            if not 0.0 < float(max_density) <= 1.0:
+                raise ValueError("max_density must be in (0, 1]")
+            max_edges = max(1, int(np.ceil(float(max_density) * max_n * (max_n - 1) / 2)))
         h = ctypes.c_void_p()
-        _check(self._lib.turboreg_create(ctypes.byref(self.params), int(device), int(max_n), int(max_batch),
-                                         ctypes.byref(h)), "create")
+        _check(self._lib.turboreg_create_ex(ctypes.byref(self.params), int(device), int(max_n), int(max_batch),
+                                            int(max_edges), ctypes.byref(h)), "create")
         self._h = h
         self.max_n, self.max_batch, self.device = int(max_n), int(max_batch), int(device)
 
@@ -186,9 +212,14 @@ class TurboReg:
         self.close()
 
     def set_params(self, **kw):
+        """Replace parameters (names of turboreg_params); on failure the context keeps its old ones."""
+        new = Params.from_buffer_copy(self.params)
         for k, v in kw.items():
-            setattr(self.params, k, v)
-        _check(self._lib.turboreg_set_params(self._h, ctypes.byref(self.params)), "set_params")
+            if k not in dict(Params._fields_):
+                raise TypeError(f"unknown parameter {k}")
+            setattr(new, k, v)
+        _check(self._lib.turboreg_set_params(self._h, ctypes.byref(new)), "set_params")
+        self.params = new
 
     def set_option(self, name, value):
         """Tuning/test knobs of include/turboreg.h (sc2_path, heavy_min_rows, heavy_min_degree, heavy_cap)."""
@@ -197,21 +228,24 @@ class TurboReg:
     # ------------------------------------------------------------------------------------------ compute
     def register(self, src, dst):
         """One pair (host numpy or device torch N×3 float32).  Returns a dict; status in ['status']."""
+        n = _points(src, "src")
+        if _points(dst, "dst") != n:
+            raise ValueError("src and dst must have the same number of rows")
         ps, ks = _ptr(src, np.float32)
         pd, kd = _ptr(dst, np.float32)
-        n = int(src.shape[0])
         res = Result()
         st = self._lib.turboreg_register(self._h, ps, pd, n, ctypes.byref(res))
-        if st not in (0, 2, 3, 4, 5):
+        if st not in PER_PAIR_STATUSES:
             raise TurboRegError(st, "register")
         return result_to_dict(res)
 
     def point_resolution(self, xyz):
         """Median nearest-neighbour distance of a point cloud (n×3 float32, host numpy or CUDA torch): the
         τ initialisation of P:322 is 0.25 × this."""
+        n = _points(xyz, "xyz")
         p, keep = _ptr(xyz, np.float32)
         out = ctypes.c_float()
-        _check(self._lib.turboreg_point_resolution(self._h, p, int(xyz.shape[0]), ctypes.byref(out)),
+        _check(self._lib.turboreg_point_resolution(self._h, p, n, ctypes.byref(out)),
                "point_resolution")
         return float(out.value)
 
@@ -219,12 +253,15 @@ class TurboReg:
         """Equal-budget 3-point RANSAC baseline on one pair: ``iters`` <= K1·K2 sampled
         triples (counter-based SplitMix64 from ``seed``), fitted and scored like TurboCliques.  Returns the
         same dict as :meth:`register`."""
+        n = _points(src, "src")
+        if _points(dst, "dst") != n:
+            raise ValueError("src and dst must have the same number of rows")
         ps, ks = _ptr(src, np.float32)
         pd, kd = _ptr(dst, np.float32)
         res = Result()
-        st = self._lib.turboreg_ransac(self._h, ps, pd, int(src.shape[0]), int(iters), int(seed) & (2**64 - 1),
+        st = self._lib.turboreg_ransac(self._h, ps, pd, n, int(iters), int(seed) & (2**64 - 1),
                                        ctypes.byref(res))
-        if st not in (0, 2, 3, 4, 5):
+        if st not in PER_PAIR_STATUSES:
             raise TurboRegError(st, "ransac")
         return result_to_dict(res)
 
@@ -233,9 +270,25 @@ class TurboReg:
 
         ``out``: None → returns a numpy structured array (RESULT_DTYPE, blocking); or a CUDA torch uint8
         tensor of ≥ batch*104 bytes → asynchronous on ``stream`` (default: torch's current stream)."""
-        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
-        n = np.ascontiguousarray(n, dtype=np.int32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64).reshape(-1)
+        n = np.ascontiguousarray(n, dtype=np.int32).reshape(-1)
         batch = int(n.shape[0])
+        # the C ABI cannot see buffer extents: every bound it relies on is checked here, before the call
+        rows = _points(src, "src")
+        if _points(dst, "dst") != rows:
+            raise ValueError("src and dst must have the same number of rows")
+        if offsets.shape[0] != batch or batch < 1:
+            raise ValueError("offsets and n must be non-empty and of equal length")
+        if (offsets < 0).any() or (n < 0).any():
+            raise ValueError("offsets and n must be non-negative")
+        if int((offsets + n).max()) > rows:
+            raise ValueError(f"offsets + n exceed the {rows} rows of src/dst")
+        if out is not None and _nbytes(out) < batch * RESULT_DTYPE.itemsize:
+            raise ValueError(f"out holds {_nbytes(out)} bytes, needs {batch * RESULT_DTYPE.itemsize}")
+        if out is not None and _is_torch_cuda(out) and int(out.device.index or 0) != self.device:
+            raise ValueError(f"out is on {out.device}, the context on cuda:{self.device}")
+        if _is_torch_cuda(src) and int(src.device.index or 0) != self.device:
+            raise ValueError(f"src is on {src.device}, the context on cuda:{self.device}")
         ps, ks = _ptr(src, np.float32)
         pd, kd = _ptr(dst, np.float32)
         if stream is None and (_is_torch_cuda(src) or (out is not None and _is_torch_cuda(out))):

@@ -38,13 +38,14 @@ struct PairState {
     int32_t n_dense;             // the other rows (k_sc2)
     int32_t ncand;               // pivot candidates (weight >= α) collected
     int32_t cand_overflow;       // ncand > PIV_CAP: the ordered count/scan/emit path selects instead
-    int32_t pad[1];
+    int32_t edge_overflow;       // E > the context's per-pair edge capacity: pair skipped (status 8)
     uint32_t bbox[12];     // order keys of max src xyz, -min src xyz, max dst xyz, -min dst xyz (k_ingest)
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
 };
 
 constexpr int PIV_CAP = 8192;  // pivot candidates sorted in shared memory per pair
+constexpr int SCORE_SEGS_MAX = 16;  // correspondence segments of a scoring launch (partial sums per segment)
 
 struct WS {
     const PairDesc* desc;
@@ -62,7 +63,7 @@ struct WS {
     int32_t* row_off;
     int64_t row_stride;
     uint32_t* edges;
-    int64_t edges_stride;
+    int64_t edges_stride;  // per-pair edge capacity (words, multiple of 4): a pair with more O2 edges overflows
     int32_t* rowptr;      // [n+1] per pair, stride rp_stride
     int64_t rp_stride;
     int4* piv;
@@ -84,9 +85,9 @@ struct WS {
     uint32_t* light_mask; // [W] bitset of the sparse rows (k_sc2_light's rows)
     uint2* heavy_UP;      // [cap][W] per heavy row a: (U_{H_a} word, exclusive prefix popcount of U_{H_a})
     int64_t heavy_UP_stride;
-    uint8_t* heavy_X;     // [cap][Kcap] uint8 rows of C restricted to H
+    uint8_t* heavy_X;     // [cap][heavy_Kcap] rows of C restricted to H (uint8 0/1, or packed e2m1 when x_fp4)
     int64_t heavy_X_stride;
-    int32_t heavy_Kcap;
+    int32_t heavy_Kcap;   // bytes per X row: 32 W (uint8) or round_up(16 W, 128) (packed e2m1)
     int32_t heavy_cap;    // max |H| (multiple of 256)
     uint16_t* heavy_D;    // [cap][cap] X X^T (+ sparse-column correction)
     int64_t heavy_D_stride;
@@ -95,7 +96,8 @@ struct WS {
     int32_t k1, k2, mode;
     int32_t pair_base;    // index of pair 0 of this view in the batch (TMA coordinates address the whole batch)
     uint16_t* uprefix;    // SC^2 mode only: [n][W] exclusive prefix popcount of U_i per word (stride bits_stride)
-    double2* herr;        // [K1*K2] per hypothesis (Σ sqrtf(s), Σ s) over the pair's correspondences (r20)
+    double2* herr;        // [K1*K2][SCORE_SEGS_MAX] per hypothesis and correspondence segment (Σ sqrtf(s), Σ s)
+                          // (r20); k_finalize adds the segments in order into slot [h][0] (deterministic)
     int32_t x_fp4;        // heavy_X holds packed e2m1 (block-scaled fp4 tensor-core path) instead of uint8
     int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
 };
@@ -131,10 +133,10 @@ inline WS ws_view(const WS& w, int p0, size_t result_bytes) {
     v.light_mask = w.light_mask + p0 * (w.bits_stride / w.row_stride);
     v.heavy_UP = w.heavy_UP + p0 * w.heavy_UP_stride;
     v.heavy_X = w.heavy_X + p0 * w.heavy_X_stride;
-    v.heavy_D = w.heavy_D + p0 * w.heavy_D_stride;
+    if (w.heavy_D) v.heavy_D = w.heavy_D + p0 * w.heavy_D_stride;
     v.pair_base = w.pair_base + p0;
     if (w.uprefix) v.uprefix = w.uprefix + p0 * w.bits_stride;
-    v.herr = w.herr + p0 * w.cl_stride;
+    if (w.herr) v.herr = w.herr + p0 * w.cl_stride * SCORE_SEGS_MAX;
     return v;
 }
 

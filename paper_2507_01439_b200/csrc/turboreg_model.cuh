@@ -439,11 +439,8 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
         const int h = hbase + SCORE_THREADS * u;
         if (!vh[u]) continue;
         if (cnt[u]) atomicAdd(reinterpret_cast<int*>(ws.hyp + (q * ws.cl_stride + h) * 16 + 12), cnt[u]);
-        if constexpr (ERR) {
-            double2* he = ws.herr + q * ws.cl_stride;
-            atomicAdd(&he[h].x, ea[u]);
-            atomicAdd(&he[h].y, es[u]);
-        }
+        if constexpr (ERR)  // this segment's partial sums in their own slot: no float atomics (deterministic)
+            ws.herr[(q * ws.cl_stride + h) * SCORE_SEGS_MAX + seg] = make_double2(ea[u], es[u]);
     }
 }
 
@@ -477,11 +474,26 @@ __global__ void __launch_bounds__(1024) k_finalize(WS ws) {
     // complement of the error's bit pattern (non-negative doubles order like their bits) — S and ijz break
     // ties below, as in the oracle's scan of the canonical list
     const int rank = ws.err_mode >> 1;
-    const double2* he = ws.herr + q * ws.cl_stride;
+    double2* hes = ws.herr + q * ws.cl_stride * SCORE_SEGS_MAX;
+    if ((ws.err_mode & 1) && d.n > 0) {  // MAE/MSE sums: the segments' partials added in segment order
+        for (int s = t; s < K; s += blockDim.x) {
+            double2 a = hes[(int64_t)s * SCORE_SEGS_MAX];
+#pragma unroll
+            for (int g = 1; g < SCORE_SEGS_MAX; ++g) {
+                const double2 b = hes[(int64_t)s * SCORE_SEGS_MAX + g];
+                a.x += b.x;
+                a.y += b.y;
+            }
+            hes[(int64_t)s * SCORE_SEGS_MAX] = a;
+        }
+        __syncthreads();
+    }
+    auto he_of = [&](int s) { return hes[(int64_t)s * SCORE_SEGS_MAX]; };
     auto quad = [&](int s) { return *reinterpret_cast<const int4*>(hyp + (int64_t)s * 16 + 12); };  // count, flag, S
     auto key_of = [&](int s, const int4 h) -> unsigned long long {
         if (rank == 0) return ((unsigned long long)(unsigned)h.x << 17) | (unsigned)h.z;
-        const double e = rank == 1 ? he[s].x : he[s].y;
+        const double2 hv = he_of(s);
+        const double e = rank == 1 ? hv.x : hv.y;
         return ~(unsigned long long)__double_as_longlong(e);
     };
     unsigned long long best1 = 0ull;
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(1024) k_finalize(WS ws) {
         const int bests = (bestt == ~0ull) ? -1 : s_slot;
         int status = d.host_status;
         if (status == 0 && st->nonfinite) status = 4;
+        if (status == 0 && st->edge_overflow) status = 8;  // TURBOREG_ERR_EDGE_CAPACITY
         if (status == 0 && bests < 0) status = 5;
         DevResult r;
         for (int k = 0; k < 9; ++k) r.R[k] = 0.f;
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(1024) k_finalize(WS ws) {
         r.hypotheses_evaluated = (d.n > 0) ? nev : 0;
         r.status = status;
         r.stage_ms[0] = r.stage_ms[1] = r.stage_ms[2] = 0.f;
-        r.num_edges = (d.n > 0) ? st->edges : 0;
+        r.num_edges = (d.n > 0) ? (st->edge_overflow ? (int64_t)(st->deg_sum >> 1) : st->edges) : 0;
         if (status == 0) {
             const float* h = hyp + (int64_t)bests * 16;
             for (int k = 0; k < 9; ++k) r.R[k] = h[k];

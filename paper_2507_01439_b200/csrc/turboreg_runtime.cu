@@ -87,8 +87,21 @@ struct turboreg_ctx {
     void* d_results = nullptr;
     float* d_inputs = nullptr;  // staging for host inputs: 2 × max_batch × max_n × 3 floats
     int* d_counters = nullptr;  // per-call work-queue counters
-    // pinned host staging
-    trk::PairDesc* h_desc = nullptr;
+    // pinned host staging: a ring of NDESC descriptor slots, each reusable once the event recorded after
+    // its H2D copy has completed (an asynchronous call must not see its descriptors overwritten)
+    static constexpr int NDESC = 4;
+    trk::PairDesc* h_desc = nullptr;  // NDESC × max_batch
+    cudaEvent_t ev_desc[NDESC] = {};
+    int desc_slot = 0;
+    // completion of the last call on whatever stream it ran: the next call's stream waits on it before it
+    // touches the shared workspace
+    cudaEvent_t ev_done = nullptr;
+    // per-pair O2 edge capacity (words) and the layout choices the allocation was made for
+    int64_t edge_cap = 0;
+    bool alloc_fp4 = true, alloc_D = false;
+    // point_resolution's own device buffers (grown on demand; independent of max_n)
+    void* pr_buf = nullptr;
+    size_t pr_bytes = 0;
     turboreg_result* h_results = nullptr;
     float* h_inputs = nullptr;
     // bookkeeping of the last call
@@ -167,24 +180,35 @@ void free_ws(turboreg_ctx* c) {
     c->ws_bytes = 0;
 }
 
-// Carve one allocation into the per-pair arrays (sizes by max_n, max_batch, K1*K2).
+// Layout of X: packed e2m1 rows (16 W bytes, rounded to the 128-byte K block) unless the dense block runs
+// as kind::i8 or on the CUDA cores (uint8 rows, 32 W bytes).
+bool want_fp4_layout(const turboreg_ctx* c) { return c->opt_sc2_path != 2 && c->opt_mma_fp4; }
+bool want_D(const turboreg_ctx* c) { return c->opt_sc2_path == 2; }  // D only on the __dp4a cross-check path
+// per-hypothesis error sums only when MAE/MSE are asked for (reading r20)
+bool want_err(const turboreg_params& p) {
+    return (p.flags & (TURBOREG_F_HYP_ERRORS | TURBOREG_F_RANK_MAE | TURBOREG_F_RANK_MSE)) != 0;
+}
+
+// Carve one allocation into the per-pair arrays (sizes by max_n, max_batch, K1*K2, the edge capacity and
+// the X layout).  The new allocation is made before the old one is released: on failure the context keeps
+// its previous workspace (and parameters) intact.
 turboreg_status alloc_ws(turboreg_ctx* c) {
-    free_ws(c);
     const int64_t B = c->max_batch, N = c->max_n, W = c->Wmax;
     const int64_t K1 = c->prm.k1, KC = (int64_t)c->prm.k1 * c->prm.k2;
     const bool base = c->prm.tau_base > 0.f;
+    const bool fp4 = want_fp4_layout(c), withD = want_D(c);
     struct Item { size_t bytes; void** dst; };
-    trk::WS& w = c->ws;
+    trk::WS w = c->ws;
     w.pts_stride = round_up(N, 32);  // even, so the paired arrays (stride / 2) stay 16-byte aligned
     w.bits_stride = N * W;
     w.row_stride = N;
-    w.edges_stride = round_up(std::max<int64_t>(1, N * (N - 1) / 2), 4);  // uint4-aligned per pair
+    w.edges_stride = round_up(std::max<int64_t>(1, c->edge_cap), 4);  // uint4-aligned per pair
     w.piv_stride = K1;
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
     void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
-    const int64_t cap = c->heavy_cap_alloc, Kcap = (int64_t)W * 32;
+    const int64_t cap = c->heavy_cap_alloc, Kcap = fp4 ? round_up((int64_t)W * 16, trk::MMA_BK) : (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
         {sizeof(trk::PairState) * B, &p_st},
@@ -205,11 +229,11 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(int32_t) * N * B, &p_degf},
         {sizeof(int32_t) * N * B, &p_hpos},
         {(size_t)(cap * Kcap * B), &p_X},
-        {sizeof(uint16_t) * (size_t)(cap * cap * B), &p_D},
+        {withD ? sizeof(uint16_t) * (size_t)(cap * cap * B) : 0, &p_D},
         {sizeof(int32_t) * (size_t)(cap * B), &p_hl},
         {sizeof(uint32_t) * (size_t)(W * B), &p_hm},
         {sizeof(uint32_t) * (size_t)(W * B), &p_lm},
-        {sizeof(double2) * (size_t)(KC * B), &p_herr},
+        {want_err(c->prm) ? sizeof(double2) * (size_t)(KC * trk::SCORE_SEGS_MAX * B) : 0, &p_herr},
         {sizeof(uint2) * (size_t)(cap * W * B), &p_up},
         {sizeof(int) * 16, &p_ctr},
         {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
@@ -230,8 +254,11 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         *it.dst = cur;
         cur += round_up((int64_t)it.bytes, 256);
     }
+    free_ws(c);  // the old workspace (if any) goes only now that the new one exists
     c->d_base = basep;
     c->ws_bytes = total;
+    c->alloc_fp4 = fp4;
+    c->alloc_D = withD;
     c->d_desc = static_cast<trk::PairDesc*>(p_desc);
     w.desc = c->d_desc;
     w.st = static_cast<trk::PairState*>(p_st);
@@ -256,14 +283,14 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_X = static_cast<uint8_t*>(p_X);
     w.heavy_X_stride = cap * Kcap;
     w.heavy_Kcap = (int32_t)Kcap;
-    w.heavy_D = static_cast<uint16_t*>(p_D);
+    w.heavy_D = withD ? static_cast<uint16_t*>(p_D) : nullptr;
     w.heavy_D_stride = cap * cap;
     w.heavy_list = static_cast<int32_t*>(p_hl);
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
     w.light_mask = static_cast<uint32_t*>(p_lm);
     w.heavy_UP = static_cast<uint2*>(p_up);
     w.uprefix = static_cast<uint16_t*>(p_upre);
-    w.herr = static_cast<double2*>(p_herr);
+    w.herr = want_err(c->prm) ? static_cast<double2*>(p_herr) : nullptr;
     w.heavy_UP_stride = cap * W;
     c->d_counters = static_cast<int*>(p_ctr);
     w.lists = static_cast<uint16_t*>(p_lists);
@@ -273,8 +300,11 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.rowptr = static_cast<int32_t*>(p_rp);
     w.rp_stride = N + 1;
     w.dense_list = static_cast<int32_t*>(p_dl);
-    // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle
+    c->ws = w;
+    // TMA descriptor over X as a 3-D uint8 tensor [batch][cap][Kcap], 128×128 boxes, 128B swizzle (the
+    // uint8 map when X holds uint8 rows, the e2m1 map when it holds packed rows)
     c->tmX_ok = false;
+    c->tmX4_ok = false;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) ==
@@ -284,14 +314,10 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         const cuuint64_t strides[2] = {(cuuint64_t)Kcap, (cuuint64_t)(Kcap * cap)};
         const cuuint32_t box[3] = {trk::MMA_BK, trk::MMA_BM, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = encode(&c->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p_X, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        c->tmX_ok = (r == CUDA_SUCCESS);
-        const cuuint64_t dims4[3] = {(cuuint64_t)round_up(Kcap / 2, trk::MMA_BK), (cuuint64_t)cap, (cuuint64_t)B};
-        r = encode(&c->tmX4, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p_X, dims4, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        c->tmX4_ok = (r == CUDA_SUCCESS);
+        const CUresult r = encode(fp4 ? &c->tmX4 : &c->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p_X, dims, strides, box,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        (fp4 ? c->tmX4_ok : c->tmX_ok) = (r == CUDA_SUCCESS);
     }
     cudaGetLastError();
     return TURBOREG_OK;
@@ -302,8 +328,9 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.heavy_cap = c->opt_heavy_cap > 0 ? std::min(c->opt_heavy_cap, c->heavy_cap_alloc) : c->heavy_cap_alloc;
     c->ws.heavy_min_rows = c->opt_heavy_min_rows;
     c->ws.heavy_min_deg = c->opt_heavy_min_deg;
-    c->ws.sc2_path = (c->opt_sc2_path == 0 && !c->tmX_ok) ? 1 : c->opt_sc2_path;
-    c->ws.x_fp4 = (c->ws.sc2_path == 0 && c->opt_mma_fp4 && c->tmX4_ok) ? 1 : 0;
+    // the tensor-core block needs the tensor map of the layout X was allocated in; without it, popcount only
+    c->ws.sc2_path = (c->opt_sc2_path == 0 && !(c->alloc_fp4 ? c->tmX4_ok : c->tmX_ok)) ? 1 : c->opt_sc2_path;
+    c->ws.x_fp4 = (c->ws.sc2_path == 0 && c->alloc_fp4) ? 1 : 0;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -324,6 +351,21 @@ bool is_device_ptr(const void* p) {
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
+
+// Next free descriptor slot of the pinned ring: waits until the H2D copy that last read it has run, so an
+// asynchronous call's descriptors are never overwritten before the device has them.
+trk::PairDesc* next_desc(turboreg_ctx* c, int* slot) {
+    const int k = c->desc_slot;
+    c->desc_slot = (k + 1) % turboreg_ctx::NDESC;
+    cudaEventSynchronize(c->ev_desc[k]);
+    *slot = k;
+    return c->h_desc + (size_t)k * c->max_batch;
+}
+
+// Every call starts by making its stream wait for the previous call's completion (the workspace is shared,
+// whatever stream either call ran on) and ends by recording its own.
+cudaError_t begin_call(turboreg_ctx* c, cudaStream_t s) { return cudaStreamWaitEvent(s, c->ev_done, 0); }
+cudaError_t end_call(turboreg_ctx* c, cudaStream_t s) { return cudaEventRecord(c->ev_done, s); }
 
 // --------------------------------------------------------------------------------- launch sequencing
 struct Launcher {
@@ -531,7 +573,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     if (mode == RUN_FULL) {
         const int64_t KC = (int64_t)c->prm.k1 * c->prm.k2;
-        if (ws.err_mode & 1) CK(cudaMemsetAsync(ws.herr, 0, sizeof(double2) * KC * batch, s));
+        if (ws.err_mode & 1)
+            CK(cudaMemsetAsync(ws.herr, 0, sizeof(double2) * KC * trk::SCORE_SEGS_MAX * batch, s));
         CK(L.run(KID_KABSCH, [&] { trk::k_kabsch<<<dim3((unsigned)((KC + 127) / 128), B), 128, 0, s>>>(ws); }));
         CK(L.run(KID_SCORE, [&] {
             const int npk = c->opt_score_pairs;  // packed hypothesis pairs per thread
@@ -609,15 +652,18 @@ const char* turboreg_status_string(turboreg_status s) {
         case TURBOREG_ERR_NO_HYPOTHESIS: return "no hypothesis";
         case TURBOREG_ERR_CUDA: return "CUDA error";
         case TURBOREG_ERR_OUT_OF_MEMORY: return "out of device memory";
+        case TURBOREG_ERR_EDGE_CAPACITY: return "edge capacity exceeded (more graph edges than max_edges)";
     }
     return "unknown status";
 }
 
-turboreg_status turboreg_create(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
-                                turboreg_ctx** out) {
-    if (!out || !params_valid(params) || max_n < 3 || max_n > 32768 || max_batch < 1 || max_batch > 65535)
+turboreg_status turboreg_create_ex(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
+                                   int64_t max_edges, turboreg_ctx** out) {
+    if (!out || !params_valid(params) || max_n < 3 || max_n > 32768 || max_batch < 1 || max_batch > 65535 ||
+        max_edges < 0)
         return TURBOREG_ERR_INVALID_ARGUMENT;
     *out = nullptr;
+    const int64_t full_edges = (int64_t)max_n * (max_n - 1) / 2;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         cudaGetLastError();
@@ -631,6 +677,7 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     c->max_batch = max_batch;
     c->Wmax = words_per_row(max_n);
     c->heavy_cap_alloc = (int32_t)std::max<int64_t>(256, std::min<int64_t>(round_up(max_n, 256), HEAVY_CAP_MAX));
+    c->edge_cap = (max_edges == 0 || max_edges > full_edges) ? full_edges : max_edges;
     turboreg_status st = TURBOREG_OK;
     // A blocking stream: it orders itself with the legacy default stream, so inputs produced there (e.g. by
     // torch's default stream) are complete before our kernels read them.
@@ -639,15 +686,18 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
         cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess) {
         st = TURBOREG_ERR_CUDA;
     }
     for (auto& e : c->ev_chunk)
         if (st == TURBOREG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) st = TURBOREG_ERR_CUDA;
+    for (auto& e : c->ev_desc)
+        if (st == TURBOREG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) st = TURBOREG_ERR_CUDA;
     if (st == TURBOREG_OK) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (st == TURBOREG_OK) st = alloc_ws(c);
     if (st == TURBOREG_OK) {
-        if (cudaMallocHost(&c->h_desc, sizeof(trk::PairDesc) * max_batch) != cudaSuccess ||
+        if (cudaMallocHost(&c->h_desc, sizeof(trk::PairDesc) * max_batch * turboreg_ctx::NDESC) != cudaSuccess ||
             cudaMallocHost(&c->h_results, sizeof(turboreg_result) * max_batch) != cudaSuccess)
             st = TURBOREG_ERR_OUT_OF_MEMORY;
     }
@@ -695,9 +745,15 @@ turboreg_status turboreg_create(const turboreg_params* params, int device, int32
     return TURBOREG_OK;
 }
 
+turboreg_status turboreg_create(const turboreg_params* params, int device, int32_t max_n, int32_t max_batch,
+                                turboreg_ctx** out) {
+    return turboreg_create_ex(params, device, max_n, max_batch, 0, out);
+}
+
 turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t value) {
     if (!c || !name) return TURBOREG_ERR_INVALID_ARGUMENT;
     const std::string k(name);
+    const int32_t old_sc2 = c->opt_sc2_path, old_fp4 = c->opt_mma_fp4;
     if (k == "sc2_path") {
         if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_sc2_path = (int32_t)value;
@@ -734,6 +790,18 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else {
         return TURBOREG_ERR_INVALID_ARGUMENT;
     }
+    if (want_fp4_layout(c) != c->alloc_fp4 || want_D(c) != c->alloc_D) {  // X / D layout changes: reallocate
+        CK(cudaSetDevice(c->device));
+        CK(cudaEventSynchronize(c->ev_done));
+        drop_graphs(c);
+        const turboreg_status st = alloc_ws(c);
+        if (st != TURBOREG_OK) {  // keep the old workspace and the options it was laid out for
+            c->opt_sc2_path = old_sc2;
+            c->opt_mma_fp4 = old_fp4;
+            set_ws_params(c);
+            return st;
+        }
+    }
     set_ws_params(c);
     return TURBOREG_OK;
 }
@@ -742,22 +810,28 @@ turboreg_status turboreg_set_params(turboreg_ctx* c, const turboreg_params* p) {
     if (!c || !params_valid(p)) return TURBOREG_ERR_INVALID_ARGUMENT;
     const bool realloc = (int64_t)p->k1 * p->k2 != (int64_t)c->prm.k1 * c->prm.k2 || p->k1 != c->prm.k1 ||
                          p->graph_mode != c->prm.graph_mode ||
-                         ((p->tau_base > 0.f) != (c->prm.tau_base > 0.f));
+                         ((p->tau_base > 0.f) != (c->prm.tau_base > 0.f)) || want_err(*p) != want_err(c->prm);
+    CK(cudaSetDevice(c->device));
+    const turboreg_params old = c->prm;
     c->prm = *p;
-    set_ws_params(c);
     if (realloc) {
-        cudaStreamSynchronize(c->own_stream);
-        cudaDeviceSynchronize();
-        turboreg_status st = alloc_ws(c);
-        if (st != TURBOREG_OK) return st;
-        set_ws_params(c);
+        CK(cudaEventSynchronize(c->ev_done));  // every earlier call (any stream) is done with the old workspace
+        drop_graphs(c);
+        const turboreg_status st = alloc_ws(c);
+        if (st != TURBOREG_OK) {  // the old workspace is intact: keep the parameters it was sized for
+            c->prm = old;
+            set_ws_params(c);
+            return st;
+        }
     }
+    set_ws_params(c);
     return TURBOREG_OK;
 }
 
 void turboreg_destroy(turboreg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->ev_done) cudaEventSynchronize(c->ev_done);  // the last call (any stream) is done with the workspace
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     free_ws(c);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -769,8 +843,12 @@ void turboreg_destroy(turboreg_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     for (auto e : c->ev_chunk)
         if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_desc)
+        if (e) cudaEventDestroy(e);
+    if (c->pr_buf) cudaFree(c->pr_buf);
     delete c;
 }
 
@@ -780,6 +858,7 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
         return TURBOREG_ERR_INVALID_ARGUMENT;
     for (int32_t p = 0; p < batch; ++p)
         if (offsets[p] < 0 || n[p] < 0) return TURBOREG_ERR_INVALID_ARGUMENT;
+    if (!c->d_base) return TURBOREG_ERR_OUT_OF_MEMORY;
     CK(cudaSetDevice(c->device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
     const bool dev_in = is_device_ptr(src) && is_device_ptr(dst);
@@ -826,8 +905,11 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
     int32_t maxn_batch = 3;
     int32_t maxn_chunk[NCHUNK] = {3, 3, 3, 3};
     c->last_n.assign(n, n + batch);
+    int dslot = 0;
+    trk::PairDesc* hd = next_desc(c, &dslot);
+    CK(begin_call(c, s));
     for (int32_t p = 0; p < batch; ++p) {
-        trk::PairDesc& d = c->h_desc[p];
+        trk::PairDesc& d = hd[p];
         d.src = dsrc + 3 * dev_off[p];
         d.dst = ddst + 3 * dev_off[p];
         d.host_status = 0;
@@ -840,7 +922,8 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
         for (int k = 0; k < nchunk; ++k)
             if (p >= bnd[k] && p < bnd[k + 1] && d.n > maxn_chunk[k]) maxn_chunk[k] = d.n;
     }
-    CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc) * batch, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->d_desc, hd, sizeof(trk::PairDesc) * batch, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->ev_desc[dslot], s));
     c->last_batch = batch;
     cudaStream_t cs = nchunk > 1 ? c->copy_stream : s;
     if (nchunk > 1) {  // the staging area is free once everything queued before on s is done
@@ -874,12 +957,14 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
     const bool want_stage = c->prm.flags & TURBOREG_F_STAGE_TIMING;
     if (dev_out) {
         CK(cudaMemcpyAsync(out, c->d_results, sizeof(turboreg_result) * batch, cudaMemcpyDeviceToDevice, s));
+        CK(end_call(c, s));
         if (want_stage && !c->profiling) {
             CK(cudaStreamSynchronize(s));
             harvest_events(c, nullptr);
         }
     } else {
         CK(cudaMemcpyAsync(c->h_results, c->d_results, sizeof(turboreg_result) * batch, cudaMemcpyDeviceToHost, s));
+        CK(end_call(c, s));
         CK(cudaStreamSynchronize(s));
         float stage[3] = {0, 0, 0};
         if (want_stage && !c->profiling) harvest_events(c, stage);
@@ -903,19 +988,31 @@ turboreg_status turboreg_register(turboreg_ctx* c, const float* src, const float
 }
 
 turboreg_status turboreg_point_resolution(turboreg_ctx* c, const float* xyz, int32_t n, float* out_pr) {
-    if (!c || !xyz || !out_pr || n < 2) return TURBOREG_ERR_INVALID_ARGUMENT;
-    if (n > c->max_n) return TURBOREG_ERR_TOO_MANY_POINTS;
+    if (!c || !xyz || !out_pr || n < 2 || n > TURBOREG_MAX_CLOUD_POINTS) return TURBOREG_ERR_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
     cudaStream_t s = c->own_stream;
-    const float* pts = xyz;
-    if (!is_device_ptr(xyz)) {  // stage through the context's input area
-        CK(cudaMemcpyAsync(c->d_inputs, xyz, sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, s));
-        pts = c->d_inputs;
+    // its own buffers, grown on demand (a cloud is not bounded by max_n): [flag, result, pad] int32 x 4,
+    // nn2[n] int32, then the staged points (host input) float32 [n][3]
+    const size_t need = 16 + sizeof(int) * (size_t)n + sizeof(float) * 3 * (size_t)n;
+    CK(cudaEventSynchronize(c->ev_done));  // an earlier asynchronous call may still read pr_buf's memory
+    if (need > c->pr_bytes) {
+        void* nb = nullptr;
+        CK(cudaMalloc(&nb, need));
+        if (c->pr_buf) cudaFree(c->pr_buf);
+        c->pr_buf = nb;
+        c->pr_bytes = need;
     }
-    int* nn2 = reinterpret_cast<int*>(c->d_inputs + (size_t)3 * c->max_n * c->max_batch);  // staging, 2nd half
-    int* flag = c->d_counters;
-    float* res = reinterpret_cast<float*>(c->d_counters + 1);
-    CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 2, s));
+    CK(begin_call(c, s));
+    int* flag = static_cast<int*>(c->pr_buf);
+    float* res = reinterpret_cast<float*>(flag + 1);
+    int* nn2 = flag + 4;
+    const float* pts = xyz;
+    if (!is_device_ptr(xyz)) {  // stage the host cloud
+        float* staged = reinterpret_cast<float*>(nn2 + n);
+        CK(cudaMemcpyAsync(staged, xyz, sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, s));
+        pts = staged;
+    }
+    CK(cudaMemsetAsync(flag, 0, sizeof(int) * 2, s));
     trk::k_fill_inf<<<(n + 255) / 256, 256, 0, s>>>(nn2, n);
     // candidate splits so the grid covers ~4 blocks per SM (each split at least one shared-memory tile)
     const int pb = (n + 255) / 256;
@@ -926,7 +1023,8 @@ turboreg_status turboreg_point_resolution(turboreg_ctx* c, const float* xyz, int
     trk::k_select_kth<<<1, 1024, 0, s>>>(nn2, n, (n - 1) / 2, res);
     CK(cudaGetLastError());
     int h[2];
-    CK(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(end_call(c, s));
     CK(cudaStreamSynchronize(s));
     c->launches += 3;
     if (h[0]) return TURBOREG_ERR_NONFINITE_INPUT;
@@ -1036,17 +1134,19 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             if (!dst) return TURBOREG_OK;
             if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
             if (!(w.err_mode & 1)) return TURBOREG_ERR_INVALID_ARGUMENT;
-            std::vector<double2> e((size_t)w.cl_stride);
+            std::vector<double2> e((size_t)w.cl_stride * trk::SCORE_SEGS_MAX);
             std::vector<float> h((size_t)w.cl_stride * 16);
-            CK(cudaMemcpy(e.data(), w.herr + pair * w.cl_stride, sizeof(double2) * e.size(), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(e.data(), w.herr + pair * w.cl_stride * trk::SCORE_SEGS_MAX, sizeof(double2) * e.size(),
+                          cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(h.data(), w.hyp + pair * w.cl_stride * 16, sizeof(float) * h.size(), cudaMemcpyDeviceToHost));
             const double nn = (double)c->last_n[pair];
             double* out = static_cast<double*>(dst);
-            for (size_t s = 0; s < e.size(); ++s) {
+            for (size_t s = 0; s < (size_t)w.cl_stride; ++s) {
                 int32_t flag;
                 std::memcpy(&flag, &h[16 * s + 13], 4);
-                out[2 * s] = flag == 0 ? e[s].x / nn : std::nan("");
-                out[2 * s + 1] = flag == 0 ? e[s].y / nn : std::nan("");
+                const double2 v = e[s * trk::SCORE_SEGS_MAX];  // slot 0 holds the ordered sum (k_finalize)
+                out[2 * s] = flag == 0 ? v.x / nn : std::nan("");
+                out[2 * s + 1] = flag == 0 ? v.y / nn : std::nan("");
             }
             return TURBOREG_OK;
         }
@@ -1079,19 +1179,24 @@ turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bit
             rows[(size_t)r * W + k] = v;
         }
     cudaStream_t s = c->own_stream;
+    int dslot = 0;
+    trk::PairDesc* hd = next_desc(c, &dslot);
+    CK(begin_call(c, s));
     CK(cudaMemcpyAsync(c->ws.bits, rows.data(), sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice, s));
-    trk::PairDesc& d = c->h_desc[0];
+    trk::PairDesc& d = hd[0];
     d.src = nullptr;
     d.dst = nullptr;
     d.n = n;
     d.W = W;
     d.host_status = 0;
     d.pad = 0;
-    CK(cudaMemcpyAsync(c->d_desc, c->h_desc, sizeof(trk::PairDesc), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->d_desc, hd, sizeof(trk::PairDesc), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->ev_desc[dslot], s));
     c->last_batch = 1;
     c->last_n.assign(1, n);
     turboreg_status st = run_pipeline(c, 1, n, s, RUN_FROM_ADJ);
     if (st != TURBOREG_OK) return st;
+    CK(end_call(c, s));
     CK(cudaStreamSynchronize(s));
     if (!c->profiling) harvest_events(c, nullptr);
     return TURBOREG_OK;

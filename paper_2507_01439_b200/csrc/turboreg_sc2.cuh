@@ -306,6 +306,12 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
     int32_t* Dn = ws.dense_list + p * ws.row_stride;
     int32_t* rp = ws.rowptr + p * ws.rp_stride;
     uint32_t* lmask = ws.light_mask + p * (ws.bits_stride / ws.row_stride);
+    if (ws.st[p].edge_overflow) {  // no room for this pair's edges: every row empty, nothing assembled
+        for (int i = t; i <= n; i += 1024) rp[i] = 0;
+        for (int w = t; w < d.W; w += 1024) lmask[w] = 0u;
+        if (t == 0) { ws.st[p].n_light = 0; ws.st[p].n_dense = 0; ws.st[p].edges = 0; }
+        return;
+    }
     if (t == 0) s_cf = s_cu = 0;
     __syncthreads();
     for (int r0 = 0; r0 < n; r0 += 1024 * RPT) {
@@ -770,8 +776,11 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
             if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
         }
     }
-    const bool use = ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
-    if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; }
+    // E = Σ deg / 2 beyond the context's edge capacity: the pair is skipped (no tensor-core block, no
+    // edges; k_rowclass empties its rows; k_finalize reports status 8 with the true E)
+    const bool ovf = (long long)(st->deg_sum >> 1) > ws.edges_stride;
+    const bool use = !ovf && ws.sc2_path != 1 && cnt >= ws.heavy_min_rows && cnt <= ws.heavy_cap;
+    if (t == 0) { s_carry = 0; st->heavy_h = use ? cnt : 0; st->heavy_thr = thr; st->edge_overflow = ovf ? 1 : 0; }
     int32_t* hl = ws.heavy_list + p * ws.heavy_cap;
     uint32_t* hmask = ws.heavy_mask + p * (ws.bits_stride / ws.row_stride);
     // ordered compaction of the register-held rows: block scan of the per-thread counts

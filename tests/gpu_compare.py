@@ -57,6 +57,12 @@ def compare_pair(tr, pair, src, dst, tau, k1, k2, thr, result=None, check_graph=
     rp = list(map(tuple, ref["pivots"].tolist()))
     gp = list(map(tuple, g["pivots"].tolist()))
     assert sorted(gp) == sorted(rp), f"pivots differ: {len(gp)} vs {len(rp)}"
+    if rp:  # the order too, whenever the candidates at or above the cut weight fit the 8192-key sort
+        alpha = min(w for _, _, w in rp)
+        ncand = int((np.triu(ref["G"], 1) >= max(alpha, 1)).sum())
+        if ncand <= 8192:
+            assert gp == rp, "pivot order differs from (w desc, i asc, j asc)"
+        stats["pivot_candidates"] = ncand
     # (i) cliques: the same set of (i, j, z, S)
     rc = sorted(map(tuple, ref["cliques"].tolist()))
     gc_order = np.lexsort(g["cliques"][:, ::-1].T)

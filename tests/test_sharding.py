@@ -68,3 +68,21 @@ def test_gather_results_gloo(world, P):
     want = fake_results(0, P).tobytes()
     for rank, blob in got:
         assert blob == want, rank
+
+
+def test_bench_spawns_ranks_and_gathers_gloo():
+    """`bench.py --gpus 2` with no torchrun environment re-launches itself as 2 ranks; the shard / gather /
+    max-over-ranks plumbing of the 1623-pair sweep runs on gloo and rank 0 sees every pair once, in order."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest-gloo"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert lines[0] == {"selftest": "gloo", "n_gpus": 2, "world": 2, "pairs": 1623, "scaling": "strong",
+                        "max_over_ranks": 2.0, "ok": True}
