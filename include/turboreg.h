@@ -65,6 +65,8 @@ typedef enum {
 #define TURBOREG_F_RANK_MAE 0x8u      /* select T* by minimum MAE instead of maximum inlier number
                                          (ties: S desc, then (i,j,z) asc); implies HYP_ERRORS           */
 #define TURBOREG_F_RANK_MSE 0x10u     /* likewise by minimum MSE; not together with RANK_MAE             */
+#define TURBOREG_F_ROW_SUMS 0x20u     /* also compute the per-row SC^2 sums r_i = Σ_j Ĝ_ij (= 2·t_i, App. B
+                                         P:755-761) after the SC^2 assembly (TURBOREG_I_ROWSUM)          */
 
 typedef struct {
     float tau;              /* τ of Eq. 1, metres, > 0: the stringent TurboClique threshold (Def. 1); drives
@@ -168,6 +170,29 @@ turboreg_status turboreg_register_batch(turboreg_ctx* ctx, const float* src_xyz,
                                         const int64_t* offsets, const int32_t* n, int32_t batch,
                                         turboreg_result* out, void* stream);
 
+/* One hypothesis of the ranked list (SPEC RegistrationResult.ranked_hypotheses). */
+typedef struct {
+    int32_t clique[3];     /* TurboClique i < j < z                                                        */
+    int32_t clique_weight; /* S^(ij)(z) (Eq. 6)                                                            */
+    float R[9];            /* its Kabsch fit, row-major                                            */
+    float t[3];
+    int32_t inlier_count;  /* g(T)                                                             */
+    int32_t slot;          /* its slot in the clique list (TURBOREG_I_CLIQUES)                              */
+    double mae, mse;       /* over all N correspondences (reading r20); NaN unless the context accumulates
+                              errors (TURBOREG_F_HYP_ERRORS or a RANK flag)                                 */
+} turboreg_hypothesis;
+
+/* The valid (non-degenerate) hypotheses of pair `pair` of the LAST register call, ranked by `metric`
+ * (App. F.1: 0 = inlier number IN descending, 1 = MAE ascending, 2 = MSE ascending; ties S desc,
+ * then (i,j,z) asc — the argmax order of readings r14/r20, so entry 0 under the context's own ranking is
+ * the returned T*).  Writes the first min(top_k, #valid) entries to the HOST array `out` and that number to
+ * *count.  The ranking runs on the GPU (a bitonic network over the K1·K2 slots, off the hot path) after the
+ * context's last call has finished.  Errors: null ctx/count, top_k < 0, out NULL with top_k > 0, pair not
+ * in the last call or not registered, metric outside 0..2, metric 1/2 without error accumulation, or
+ * K1·K2 > 2^22 → INVALID_ARGUMENT. */
+turboreg_status turboreg_ranked_hypotheses(turboreg_ctx* ctx, int32_t pair, int32_t metric, int32_t top_k,
+                                           turboreg_hypothesis* out, int32_t* count);
+
 /* Release the context and all its device memory, after its last call has finished.  NULL is ignored. */
 void turboreg_destroy(turboreg_ctx* ctx);
 
@@ -191,7 +216,8 @@ const char* turboreg_status_string(turboreg_status s);
  *   TURBOREG_I_EDGES     uint32 [n+1 + E] the compact O2 rows: rowptr[0..n], then E words (j << 16) | Ĝ_ij,
  *                        row i's upper edges (j > i) in increasing j at rowptr[i]
  *   TURBOREG_I_STATE     int64  [16] per-pair scalars: n, W, edges, positive edges, alpha, c_gt, need,
- *                        num_pivots, nonfinite, ...                                                   */
+ *                        num_pivots, nonfinite, ...
+ *   TURBOREG_I_ROWSUM    int32  [n] r_i = Σ_j Ĝ_ij (needs TURBOREG_F_ROW_SUMS, else INVALID_ARGUMENT)   */
 #define TURBOREG_I_BITS 1
 #define TURBOREG_I_BITS_BASE 2
 #define TURBOREG_I_SC2 3
@@ -201,6 +227,7 @@ const char* turboreg_status_string(turboreg_status s);
 #define TURBOREG_I_STATE 7
 #define TURBOREG_I_ERRORS 8
 #define TURBOREG_I_EDGES 9
+#define TURBOREG_I_ROWSUM 10
 turboreg_status turboreg_get_intermediates(turboreg_ctx* ctx, int32_t pair, int32_t what, void* dst, size_t bytes,
                                            size_t* needed);
 

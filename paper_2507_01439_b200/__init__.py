@@ -5,6 +5,7 @@ only the thin Python binding (argument marshalling).  There is no CPU fallback: 
 fails loudly when the shared library is missing.
 """
 from ._binding import (  # noqa: F401
+    HYPOTHESIS_DTYPE,
     RESULT_DTYPE,
     Params,
     Result,
@@ -15,4 +16,4 @@ from ._binding import (  # noqa: F401
     library_path,
 )
 
-__all__ = ["TurboReg", "Params", "Result", "Status", "TurboRegError", "RESULT_DTYPE", "library", "library_path"]
+__all__ = ["TurboReg", "HYPOTHESIS_DTYPE", "Params", "Result", "Status", "TurboRegError", "RESULT_DTYPE", "library", "library_path"]

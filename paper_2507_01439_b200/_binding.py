@@ -41,8 +41,10 @@ F_KERNEL_TIMING = 0x2
 F_HYP_ERRORS = 0x4
 F_RANK_MAE = 0x8
 F_RANK_MSE = 0x10
+F_ROW_SUMS = 0x20
 
-I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS, I_EDGES = 1, 2, 3, 4, 5, 6, 7, 8, 9
+I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS, I_EDGES, I_ROWSUM = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
+METRICS = {"in": 0, "mae": 1, "mse": 2}
 
 
 class Params(ctypes.Structure):
@@ -85,6 +87,15 @@ RESULT_DTYPE = np.dtype(
 )
 assert ctypes.sizeof(Result) == RESULT_DTYPE.itemsize == 104
 
+HYPOTHESIS_DTYPE = np.dtype(  # turboreg_hypothesis
+    {
+        "names": ["clique", "clique_weight", "R", "t", "inlier_count", "slot", "mae", "mse"],
+        "formats": [("<i4", (3,)), "<i4", ("<f4", (9,)), ("<f4", (3,)), "<i4", "<i4", "<f8", "<f8"],
+        "offsets": [0, 12, 16, 52, 64, 68, 72, 80],
+        "itemsize": 88,
+    }
+)
+
 _lib = None
 
 
@@ -114,6 +125,7 @@ def library():
     lib.turboreg_status_string.restype = ctypes.c_char_p
     lib.turboreg_get_intermediates.argtypes = [P, i32, i32, P, u64, ctypes.POINTER(u64)]
     lib.turboreg_pgs_from_adjacency.argtypes = [P, P, i32, i32]
+    lib.turboreg_ranked_hypotheses.argtypes = [P, i32, i32, i32, P, ctypes.POINTER(i32)]
     lib.turboreg_profile_begin.argtypes = [P]
     lib.turboreg_profile_end.argtypes = [P, P, P, P, i32, ctypes.POINTER(i32)]
     lib.turboreg_set_option.argtypes = [P, ctypes.c_char_p, i64]
@@ -124,7 +136,8 @@ def library():
     lib.turboreg_workspace_bytes.restype = u64
     for name in ("turboreg_create", "turboreg_create_ex", "turboreg_set_params", "turboreg_register", "turboreg_register_batch",
                  "turboreg_get_intermediates", "turboreg_pgs_from_adjacency", "turboreg_profile_begin",
-                 "turboreg_profile_end", "turboreg_point_resolution", "turboreg_ransac"):
+                 "turboreg_profile_end", "turboreg_point_resolution", "turboreg_ransac",
+                 "turboreg_ranked_hypotheses"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -174,13 +187,14 @@ class TurboReg:
 
     def __init__(self, tau, k1=1000, k2=2, inlier_threshold=0.1, *, tau_base=0.0, graph_mode=0,
                  max_n=5000, max_batch=1, device=0, stage_timing=False, kernel_timing=False, hyp_errors=False,
-                 rank_metric="in", max_edges=0, max_density=None):
+                 rank_metric="in", max_edges=0, max_density=None, row_sums=False):
         """``max_edges``: per-pair O2 edge capacity (0 = complete graph, never overflows); ``max_density``
         (fraction of the max_n(max_n-1)/2 possible edges) is the same bound as a ratio.  Pairs with more
         edges report status EDGE_CAPACITY (include/turboreg.h, turboreg_create_ex)."""
         self._lib = library()
         flags = (F_STAGE_TIMING if stage_timing else 0) | (F_KERNEL_TIMING if kernel_timing else 0)
         flags |= (F_HYP_ERRORS if hyp_errors else 0) | {"in": 0, "mae": F_RANK_MAE, "mse": F_RANK_MSE}[rank_metric]
+        flags |= F_ROW_SUMS if row_sums else 0
         self.params = Params(float(tau), float(tau_base), int(k1), int(k2), float(inlier_threshold),
                              int(graph_mode), flags)
         if max_density is not None:
@@ -309,6 +323,18 @@ class TurboReg:
         _check(st, "register_batch")
         return out
 
+    def ranked_hypotheses(self, pair=0, metric="in", top_k=None):
+        """The valid hypotheses of `pair` of the last call ranked by `metric` ("in" descending, "mae" / "mse"
+        ascending; ties S desc, (i,j,z) asc) as a HYPOTHESIS_DTYPE array of at most `top_k` entries (all when
+        None).  MAE/MSE ranking needs a context created with hyp_errors=True or an error rank_metric."""
+        k = int(self.params.k1) * int(self.params.k2) if top_k is None else int(top_k)
+        out = np.zeros(max(k, 1), HYPOTHESIS_DTYPE)
+        cnt = ctypes.c_int32()
+        _check(self._lib.turboreg_ranked_hypotheses(self._h, int(pair), METRICS[metric], k,
+                                                    out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt)),
+               "ranked_hypotheses")
+        return out[: cnt.value]
+
     # ------------------------------------------------------------------------------------------ test views
     def intermediate(self, pair, what):
         need = ctypes.c_size_t()
@@ -333,6 +359,8 @@ class TurboReg:
             return buf.view(np.float32).reshape(-1, 16)
         if what == I_ERRORS:
             return buf.view(np.float64).reshape(-1, 2)
+        if what == I_ROWSUM:
+            return buf.view(np.int32)
         if what == I_EDGES:
             v = buf.view(np.uint32)
             n = int(self.intermediate(pair, I_STATE)["n"])

@@ -9,11 +9,14 @@
 //                                 rowptr[i]: (j << 16) | Ĝ_ij   ("rank-indexed" O2 weights, Def. 2)
 //   rowptr     int32[n+1]         exclusive scan of the upper degrees
 //   deg        int32[n]           upper degree of row i
-//   piv        int4[K1]           (i, j, Ĝ_ij, 0) in lexicographic order
+//   piv        int4[K1]           (i, j, Ĝ_ij, 0) in (Ĝ desc, i asc, j asc) order (lexicographic when more
+//                                 than PIV_CAP edges reach the cut weight)
 //   cliq       int4[K1*K2]        (i, j, z, S) per slot pivot*K2 + r; empty (-1,-1,-1,0)
 //   hyp        float[K1*K2][16]   R[9], t[3], count, flag, S, 0
-// Float32 arithmetic that decides an integer (Eq. 1 edges, inlier tests) uses explicit _rn intrinsics
-// in exactly the oracle's expression tree (readings r1, r13) so no contraction can change a bit.
+// Float32 arithmetic that decides an integer is bit-identical to the oracle's: the inlier test uses explicit
+// _rn intrinsics in the reading-r13 FMA tree; Eq. 1 edges come from a certified square-root-free filter whose
+// decisions provably equal the oracle's float32 tree, with that exact tree (r1) evaluated for
+// every test the filter cannot certify.
 // =====================================================================================================
 #pragma once
 // Stage headers (each includes the previous one, so definitions keep their order):
@@ -23,4 +26,5 @@
 //   turboreg_select.cuh  a4 pivots
 //   turboreg_pgs.cuh     a5 PGS, SC^2-mode canonical list
 //   turboreg_model.cuh   a6 Kabsch, a7 scoring, a8 argmax
-#include "turboreg_model.cuh"
+//   turboreg_rank.cuh    optional outputs: per-row SC^2 sums r_i, the ranked hypothesis list
+#include "turboreg_rank.cuh"

@@ -1,0 +1,128 @@
+// Optional outputs beside the hot path: per-row SC^2 sums r_i (App. B) and the ranked hypothesis list
+// (App. F.1; SPEC RegistrationResult.ranked_hypotheses).  Part of turboreg_kernels.cuh.
+#pragma once
+#include "turboreg_model.cuh"
+
+namespace trk {
+
+// ------------------------------------------------------------------------------------------ r_i
+// r_i = Σ_j Ĝ_ij over the full symmetric Ĝ (Eq. 2), which App. B identifies with 2·t_i, t_i the
+// number of triangles through node i.  The O2 rows hold each edge once (i < j), so an edge adds its weight
+// to both endpoints: one warp per row sums its upper edges (coalesced) into r_i and adds each weight to
+// r_j.  Integer atomics: the result is exact and order-independent.
+__global__ void __launch_bounds__(256) k_rowsum(WS ws, int32_t* rsum, int64_t rstride) {
+    const int p = blockIdx.y;
+    const int n = ws.desc[p].n;
+    if (n == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t* rowptr = ws.rowptr + p * ws.rp_stride;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    int32_t* r = rsum + p * rstride;
+    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += gridDim.x * 8) {
+        const int e0 = rowptr[i], e1 = rowptr[i + 1];
+        int own = 0;
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const uint32_t v = __ldg(edges + e);
+            const int w = (int)(v & 0xffffu);
+            own += w;
+            if (w) atomicAdd(r + (v >> 16), w);
+        }
+        own = (int)__reduce_add_sync(FULL, (unsigned)own);
+        if (lane == 0 && own) atomicAdd(r + i, own);
+    }
+}
+
+// ------------------------------------------------------------------------------------------ ranking
+// The valid hypotheses of one pair ranked by a metric (App. F.1: IN descending, MAE / MSE
+// ascending; ties S desc, then (i,j,z) asc — the argmax order of readings r14 / r20, so rank 0 is T*).
+// Off the hot path: a bitonic network over slot indices in global memory, one launch per stage, with a
+// comparator that reads each slot's precomputed key.
+struct RankKey {
+    unsigned long long primary;  // IN: 2^32-1-count; MAE/MSE: the error's bits (non-negative double); invalid: ~0
+    unsigned long long ijz;      // i << 30 | j << 15 | z
+    int32_t nS;                  // -S
+    int32_t slot;
+};
+
+__device__ __forceinline__ bool rank_less(const RankKey& a, const RankKey& b) {
+    if (a.primary != b.primary) return a.primary < b.primary;
+    if (a.nS != b.nS) return a.nS < b.nS;
+    return a.ijz < b.ijz;
+}
+
+__global__ void k_rank_prep(WS ws, int pair, int metric, RankKey* keys, int32_t* idx, int m2) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m2) return;
+    const int K = ws.k1 * ws.k2;
+    RankKey k{~0ull, ~0ull, 0, s};
+    if (s < K) {
+        const int4 h = *reinterpret_cast<const int4*>(ws.hyp + (pair * ws.cl_stride + s) * 16 + 12);  // count, flag, S
+        const int4 c = ws.cliq[pair * ws.cl_stride + s];
+        if (h.y == 0 && c.x >= 0) {
+            if (metric == 0) {
+                k.primary = 0xffffffffull - (unsigned)h.x;
+            } else {
+                const double2 e = ws.herr[(pair * ws.cl_stride + s) * SCORE_SEGS_MAX];  // ordered sum (k_finalize)
+                k.primary = (unsigned long long)__double_as_longlong(metric == 1 ? e.x : e.y);
+            }
+            k.nS = -h.z;
+            k.ijz = ((unsigned long long)c.x << 30) | ((unsigned long long)c.y << 15) | (unsigned long long)c.z;
+        }
+    }
+    keys[s] = k;
+    idx[s] = s;
+}
+
+__global__ void k_rank_step(const RankKey* keys, int32_t* idx, int m2, int size, int stride) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m2 / 2) return;
+    const int lo = 2 * k - (k & (stride - 1));
+    const int hi = lo + stride;
+    const bool up = (lo & size) == 0;
+    const int a = idx[lo], b = idx[hi];
+    if (rank_less(keys[b], keys[a]) == up) { idx[lo] = b; idx[hi] = a; }
+}
+
+struct DevHypothesis {  // mirrors turboreg_hypothesis
+    int32_t clique[3];
+    int32_t clique_weight;
+    float R[9];
+    float t[3];
+    int32_t inlier_count;
+    int32_t slot;
+    double mae, mse;
+};
+
+__global__ void k_rank_emit(WS ws, int pair, const RankKey* keys, const int32_t* idx, int top, int n,
+                            DevHypothesis* out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= top) return;
+    const int s = idx[r];
+    DevHypothesis o;
+    const float* h = ws.hyp + (pair * ws.cl_stride + s) * 16;
+    const int4 c = ws.cliq[pair * ws.cl_stride + s];
+    o.clique[0] = c.x; o.clique[1] = c.y; o.clique[2] = c.z;
+    o.clique_weight = c.w;
+    for (int k = 0; k < 9; ++k) o.R[k] = h[k];
+    for (int k = 0; k < 3; ++k) o.t[k] = h[9 + k];
+    o.inlier_count = __float_as_int(h[12]);
+    o.slot = s;
+    if (ws.herr) {
+        const double2 e = ws.herr[(pair * ws.cl_stride + s) * SCORE_SEGS_MAX];
+        o.mae = e.x / n;
+        o.mse = e.y / n;
+    } else {
+        o.mae = o.mse = __longlong_as_double(0x7ff8000000000000ll);  // NaN: errors not accumulated
+    }
+    out[r] = o;
+}
+
+// number of valid entries (primary != ~0) among the first m2 sorted indices
+__global__ void k_rank_count(const RankKey* keys, const int32_t* idx, int m2, int* count) {
+    int c = 0;
+    for (int k = threadIdx.x; k < m2; k += blockDim.x) c += keys[idx[k]].primary != ~0ull;
+    c = (int)__reduce_add_sync(FULL, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+}  // namespace trk

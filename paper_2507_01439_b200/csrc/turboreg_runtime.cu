@@ -21,6 +21,7 @@
 #include "turboreg_sc2_mma.cuh"
 
 static_assert(sizeof(trk::DevResult) == sizeof(turboreg_result), "result layout");
+static_assert(sizeof(trk::DevHypothesis) == sizeof(turboreg_hypothesis), "hypothesis layout");
 
 namespace {
 
@@ -49,14 +50,15 @@ enum KernelId {
     KID_SCORE,
     KID_FINALIZE,
     KID_RANSAC,
+    KID_ROWSUM,
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
                                        "k_expand",   "k_sc2_mma",      "k_emit_hh",     "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
-                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize",    "k_ransac_sample"};
+                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize",    "k_ransac_sample", "k_rowsum"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 1};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 1, 0};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -99,9 +101,12 @@ struct turboreg_ctx {
     // per-pair O2 edge capacity (words) and the layout choices the allocation was made for
     int64_t edge_cap = 0;
     bool alloc_fp4 = true, alloc_D = false;
-    // point_resolution's own device buffers (grown on demand; independent of max_n)
+    // point_resolution's and the ranking's own device buffers (grown on demand; independent of max_n)
     void* pr_buf = nullptr;
     size_t pr_bytes = 0;
+    void* rank_buf = nullptr;
+    size_t rank_bytes = 0;
+    int32_t* d_rowsum = nullptr;  // [max_batch][max_n] r_i (TURBOREG_F_ROW_SUMS)
     turboreg_result* h_results = nullptr;
     float* h_inputs = nullptr;
     // bookkeeping of the last call
@@ -162,7 +167,7 @@ bool params_valid(const turboreg_params* p) {
     if (p->graph_mode != 0 && p->graph_mode != 1) return false;
     if (p->graph_mode == 1 && (int64_t)p->k1 * p->k2 > trk::CANON_CAP) return false;  // canonical sort in smem
     if (p->flags & ~(TURBOREG_F_STAGE_TIMING | TURBOREG_F_KERNEL_TIMING | TURBOREG_F_HYP_ERRORS | TURBOREG_F_RANK_MAE |
-                     TURBOREG_F_RANK_MSE))
+                     TURBOREG_F_RANK_MSE | TURBOREG_F_ROW_SUMS))
         return false;
     if ((p->flags & TURBOREG_F_RANK_MAE) && (p->flags & TURBOREG_F_RANK_MSE)) return false;
     return true;
@@ -207,7 +212,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp; void* p_rs;
     const int64_t cap = c->heavy_cap_alloc, Kcap = fp4 ? round_up((int64_t)W * 16, trk::MMA_BK) : (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -241,6 +246,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(int32_t) * (size_t)(N * B), &p_dl},
         {sizeof(unsigned long long) * (size_t)(trk::PIV_CAP * B), &p_cand},
         {sizeof(int32_t) * (size_t)((N + 1) * B), &p_rp},
+        {sizeof(int32_t) * (size_t)(N * B), &p_rs},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     if (c->prm.graph_mode == 1) items.push_back({sizeof(uint16_t) * N * W * B, &p_upre});
@@ -293,6 +299,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.herr = want_err(c->prm) ? static_cast<double2*>(p_herr) : nullptr;
     w.heavy_UP_stride = cap * W;
     c->d_counters = static_cast<int*>(p_ctr);
+    c->d_rowsum = static_cast<int32_t*>(p_rs);
     w.lists = static_cast<uint16_t*>(p_lists);
     w.lists_stride = N * trk::LIST_MAX;
     w.light_list = static_cast<int32_t*>(p_ll);
@@ -537,6 +544,13 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             CK(cudaEventRecord(c->ev_join, sl));
             CK(cudaStreamWaitEvent(s, c->ev_join, 0));
         }
+    }
+    if (c->prm.flags & TURBOREG_F_ROW_SUMS) {  // r_i = Σ_j Ĝ_ij (App. B), beside the path
+        int32_t* rs = c->d_rowsum + (int64_t)p0 * c->max_n;
+        CK(cudaMemsetAsync(rs, 0, sizeof(int32_t) * (size_t)c->max_n * batch, s));
+        CK(L.run(KID_ROWSUM, [&] {
+            trk::k_rowsum<<<dim3((unsigned)((maxn_batch + 63) / 64), B), 256, 0, s>>>(ws, rs, c->max_n);
+        }));
     }
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
     const int sel_bpp = std::max(trk::SEL_BLOCKS_PER_PAIR, std::min((4 * c->num_sms + batch - 1) / batch, 256));
@@ -849,6 +863,7 @@ void turboreg_destroy(turboreg_ctx* c) {
     for (auto e : c->ev_desc)
         if (e) cudaEventDestroy(e);
     if (c->pr_buf) cudaFree(c->pr_buf);
+    if (c->rank_buf) cudaFree(c->rank_buf);
     delete c;
 }
 
@@ -1150,6 +1165,15 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
             }
             return TURBOREG_OK;
         }
+        case TURBOREG_I_ROWSUM: {
+            if (!(c->prm.flags & TURBOREG_F_ROW_SUMS)) return TURBOREG_ERR_INVALID_ARGUMENT;
+            need = sizeof(int32_t) * (size_t)n;
+            if (needed) *needed = need;
+            if (!dst) return TURBOREG_OK;
+            if (bytes < need) return TURBOREG_ERR_INVALID_ARGUMENT;
+            CK(cudaMemcpy(dst, c->d_rowsum + (int64_t)pair * c->max_n, need, cudaMemcpyDeviceToHost));
+            return TURBOREG_OK;
+        }
         case TURBOREG_I_STATE: {
             need = sizeof(int64_t) * 16;
             if (needed) *needed = need;
@@ -1164,6 +1188,60 @@ turboreg_status turboreg_get_intermediates(turboreg_ctx* c, int32_t pair, int32_
         }
         default: return TURBOREG_ERR_INVALID_ARGUMENT;
     }
+}
+
+turboreg_status turboreg_ranked_hypotheses(turboreg_ctx* c, int32_t pair, int32_t metric, int32_t top_k,
+                                           turboreg_hypothesis* out, int32_t* count) {
+    if (!c || !count || top_k < 0 || (top_k > 0 && !out) || metric < 0 || metric > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+    if (pair < 0 || pair >= c->last_batch) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const int n = c->last_n[pair];
+    if (n < 3 || n > c->max_n) return TURBOREG_ERR_INVALID_ARGUMENT;
+    if (metric > 0 && !c->ws.herr) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const int64_t K = c->ws.cl_stride;
+    if (K > ((int64_t)1 << 22)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    int m2 = 2;
+    while (m2 < K) m2 <<= 1;
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventSynchronize(c->ev_done));
+    const size_t need = sizeof(trk::RankKey) * m2 + sizeof(int32_t) * m2 + 16 +
+                        sizeof(trk::DevHypothesis) * (size_t)std::min<int64_t>(std::max(top_k, 1), K);
+    if (need > c->rank_bytes) {
+        void* nb = nullptr;
+        CK(cudaMalloc(&nb, need));
+        if (c->rank_buf) cudaFree(c->rank_buf);
+        c->rank_buf = nb;
+        c->rank_bytes = need;
+    }
+    cudaStream_t s = c->own_stream;
+    CK(begin_call(c, s));
+    trk::RankKey* keys = static_cast<trk::RankKey*>(c->rank_buf);
+    int32_t* idx = reinterpret_cast<int32_t*>(keys + m2);
+    int* d_cnt = idx + m2;
+    trk::DevHypothesis* d_out = reinterpret_cast<trk::DevHypothesis*>(reinterpret_cast<char*>(c->rank_buf) +
+                                                                      sizeof(trk::RankKey) * m2 + sizeof(int32_t) * m2 + 16);
+    CK(cudaMemsetAsync(d_cnt, 0, sizeof(int), s));
+    trk::k_rank_prep<<<(m2 + 255) / 256, 256, 0, s>>>(c->ws, pair, metric, keys, idx, m2);
+    CK(cudaGetLastError());
+    for (int size = 2; size <= m2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            trk::k_rank_step<<<(m2 / 2 + 255) / 256, 256, 0, s>>>(keys, idx, m2, size, stride);
+            CK(cudaGetLastError());
+        }
+    trk::k_rank_count<<<1, 1024, 0, s>>>(keys, idx, m2, d_cnt);
+    CK(cudaGetLastError());
+    int valid = 0;
+    CK(cudaMemcpyAsync(&valid, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int top = std::min(top_k, valid);
+    if (top > 0) {
+        trk::k_rank_emit<<<(top + 127) / 128, 128, 0, s>>>(c->ws, pair, keys, idx, top, n, d_out);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, d_out, sizeof(turboreg_hypothesis) * top, cudaMemcpyDeviceToHost, s));
+    }
+    CK(end_call(c, s));
+    CK(cudaStreamSynchronize(s));
+    *count = top;
+    return TURBOREG_OK;
 }
 
 turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bits, int32_t n, int32_t stride_words) {

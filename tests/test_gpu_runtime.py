@@ -232,3 +232,68 @@ def test_binding_rejects_bad_extents(TR):
     with pytest.raises(ValueError):
         tr.register_batch(torch.from_numpy(inst["src"]).cuda(), torch.from_numpy(inst["dst"]).cuda(), [0], [500],
                           out=torch.zeros(50, dtype=torch.uint8, device="cuda"))
+
+
+@pytest.mark.parametrize("key,n", [("A", None), ("B", 5000), ("D", 2000)])
+def test_row_sums_equal_twice_triangle_counts(TR, key, n):
+    """r_i = Σ_j Ĝ_ij (north star: "per-row SC² sums"): equal to the oracle's Ĝ row sums, and to 2·t_i with
+    t_i the triangles through i (App. B), computed here as diag(C³)/2 with numpy on the GPU's own C
+    (a library matmul, independent of oracle/)."""
+    from paper_2507_01439_b200._binding import I_ROWSUM
+
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=21, n=n)
+    nn = inst["src"].shape[0]
+    tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn, row_sums=True)
+    r = tr.register(inst["src"], inst["dst"])
+    rs = tr.intermediate(0, I_ROWSUM)
+    ref = oracle.estimate(inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, trace=True)
+    assert (rs == ref["G"].sum(axis=1)).all()
+    C = tr.bits(0).astype(np.float64)
+    two_t = np.einsum("ij,ji->i", C @ C, C)  # diag(C^3) = 2 t_i
+    assert (rs == two_t.astype(np.int64)).all()
+    plain = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn)
+    assert plain.register(inst["src"], inst["dst"])["clique"] == r["clique"]
+    with pytest.raises(Exception):
+        plain.intermediate(0, I_ROWSUM)
+
+
+def _oracle_ranking(ref, metric):
+    ok = ref["hyp_degenerate"] == 0
+    cl = ref["cliques"][ok]
+    cnt = ref["hyp_count"][ok].astype(np.int64)
+    err = {"in": -cnt, "mae": ref["hyp_mae"][ok], "mse": ref["hyp_mse"][ok]}[metric]
+    order = np.lexsort((cl[:, 2], cl[:, 1], cl[:, 0], -cl[:, 3], err))
+    return cl[order], err[order]
+
+
+@pytest.mark.parametrize("metric", ["in", "mae", "mse"])
+@pytest.mark.parametrize("key,n,graph_mode", [("A", None, 0), ("B", 5000, 0), ("C", 3000, 1)])
+def test_ranked_hypotheses_match_oracle(TR, metric, key, n, graph_mode):
+    """Ranked hypothesis list (App. F.1): the oracle's per-hypothesis IN / MAE / MSE
+    sorted by (metric, S desc, (i,j,z) asc); entry 0 under the context's own metric is the returned T*."""
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=23, n=n)
+    nn = inst["src"].shape[0]
+    tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=nn, hyp_errors=True, graph_mode=graph_mode,
+            rank_metric=metric)
+    res = tr.register(inst["src"], inst["dst"])
+    got = tr.ranked_hypotheses(0, metric)
+    ref = oracle.estimate(inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, trace=True,
+                          graph_mode=graph_mode)
+    want_cl, want_key = _oracle_ranking(ref, metric)
+    assert len(got) == len(want_cl) == res["hypotheses_evaluated"]
+    gcl = np.concatenate([got["clique"], got["clique_weight"][:, None]], axis=1)
+    if metric == "in":
+        assert (gcl == want_cl).all()
+        assert (got["inlier_count"] == -want_key).all()
+    else:  # float64 sums in another order: equal within 1e-12, so only near-equal keys may swap
+        gkey = got[metric]
+        assert np.all(np.abs(np.sort(gkey) - np.sort(want_key)) <= 1e-12 * np.abs(want_key))
+        assert np.all(np.diff(gkey) >= 0)
+        same = np.all(gcl == want_cl, axis=1)
+        for k in np.nonzero(~same)[0]:  # a swap is only allowed among keys equal to 1e-12
+            assert abs(gkey[k] - want_key[k]) <= 1e-12 * abs(want_key[k])
+    assert tuple(got[0]["clique"]) == tuple(res["clique"])
+    top = tr.ranked_hypotheses(0, metric, top_k=5)
+    assert top.tobytes() == got[:5].tobytes()
