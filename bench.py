@@ -475,7 +475,7 @@ def run_cuda(args, rank, world, local_rank):
     else:
         all_ok = int((res["status"] == 0).sum())
 
-    context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 else None
+    context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 and not args.no_context else None
     if rank != 0:
         return
     pk = peaks()
@@ -651,6 +651,7 @@ def main():
     ap.add_argument("--pairs", type=int, default=0, help="weak scaling: this many pairs per GPU instead of --sweep")
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-context", action="store_true", help="skip the single-pair / RANSAC context numbers")
     ap.add_argument("--selftest-gloo", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.gpus < 1 or args.steps < 1 or args.warmup < 0:

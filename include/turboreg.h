@@ -193,6 +193,39 @@ typedef struct {
 turboreg_status turboreg_ranked_hypotheses(turboreg_ctx* ctx, int32_t pair, int32_t metric, int32_t top_k,
                                            turboreg_hypothesis* out, int32_t* count);
 
+/* ----------------------------------------------------------------- NEXT(1): one pair split over ranks
+ * Pivot-level parallelism across GPUs for large N ("Pivot-level Parallelism"; SPEC S:268-269;
+ * SURVEY §8(e)).  Each of `world` ranks (one context per GPU, same parameters) runs the three phases below
+ * on the same pair; the caller exchanges device buffers between them (all-reduce SUM, all-gather), e.g. with
+ * NCCL — paper_2507_01439_b200/split.py does it over torch.distributed.  Work split: compat block-row pairs,
+ * tensor-core tiles, dense-row items, sparse-row groups and pivots are each partitioned into contiguous
+ * rank ranges; every bit word of C and every O2 edge word is written by exactly one rank into a zeroed
+ * buffer, so a SUM all-reduce rebuilds the full arrays on every rank; pivot selection then runs on identical
+ * data everywhere (no candidate exchange needed).  Results are bit-identical to turboreg_register.
+ * Requirements: graph_mode 0, inlier-number ranking, no ROW_SUMS, sc2_path != 2 (else INVALID_ARGUMENT).
+ *   1. turboreg_split_begin: ingest + this rank's compat tiles into a zeroed bit matrix.
+ *        exchange: all-reduce SUM of buffer TURBOREG_SPLIT_BITS (int32 words, n·W of them).
+ *   2. turboreg_split_sc2: degrees / heavy split / row classes on the full C, this rank's share of the SC^2
+ *        assembly into a zeroed edge array; *num_edges = E (the call synchronises).
+ *        exchange: all-reduce SUM of the first E words of buffer TURBOREG_SPLIT_EDGES.
+ *   3. turboreg_split_search: pivots (identical on every rank), PGS on this rank's pivot slice, Kabsch and
+ *        scoring of its TurboCliques, its local argmax into buffer TURBOREG_SPLIT_RESULT (one record).
+ *        exchange: all-gather of the `world` records into a device array (rank order).
+ *   4. turboreg_split_merge: T* = the argmax over the gathered records (key of reading r14) on the GPU,
+ *        counts summed; `out` host (blocking) or device.
+ * src/dst: HOST or DEVICE n×3 float32; phases 1, 3, 4 are asynchronous on `stream` (NULL = context stream).
+ * Per-pair statuses 2/3 are returned by turboreg_split_begin; 4/5/8 appear in the merged record. */
+#define TURBOREG_SPLIT_BITS 0
+#define TURBOREG_SPLIT_EDGES 1
+#define TURBOREG_SPLIT_RESULT 2
+turboreg_status turboreg_split_begin(turboreg_ctx* ctx, const float* src_xyz, const float* dst_xyz, int32_t n,
+                                     int32_t rank, int32_t world, void* cuda_stream);
+turboreg_status turboreg_split_buffer(turboreg_ctx* ctx, int32_t which, void** dev_ptr, size_t* bytes);
+turboreg_status turboreg_split_sc2(turboreg_ctx* ctx, int64_t* num_edges, void* cuda_stream);
+turboreg_status turboreg_split_search(turboreg_ctx* ctx, void* cuda_stream);
+turboreg_status turboreg_split_merge(turboreg_ctx* ctx, const void* parts, int32_t world, turboreg_result* out,
+                                     void* cuda_stream);
+
 /* Release the context and all its device memory, after its last call has finished.  NULL is ignored. */
 void turboreg_destroy(turboreg_ctx* ctx);
 

@@ -43,6 +43,8 @@ F_RANK_MAE = 0x8
 F_RANK_MSE = 0x10
 F_ROW_SUMS = 0x20
 
+SPLIT_BITS, SPLIT_EDGES, SPLIT_RESULT = 0, 1, 2
+
 I_BITS, I_BITS_BASE, I_SC2, I_PIVOTS, I_CLIQUES, I_HYPS, I_STATE, I_ERRORS, I_EDGES, I_ROWSUM = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 METRICS = {"in": 0, "mae": 1, "mse": 2}
 
@@ -126,6 +128,11 @@ def library():
     lib.turboreg_get_intermediates.argtypes = [P, i32, i32, P, u64, ctypes.POINTER(u64)]
     lib.turboreg_pgs_from_adjacency.argtypes = [P, P, i32, i32]
     lib.turboreg_ranked_hypotheses.argtypes = [P, i32, i32, i32, P, ctypes.POINTER(i32)]
+    lib.turboreg_split_begin.argtypes = [P, P, P, i32, i32, i32, P]
+    lib.turboreg_split_buffer.argtypes = [P, i32, ctypes.POINTER(P), ctypes.POINTER(u64)]
+    lib.turboreg_split_sc2.argtypes = [P, ctypes.POINTER(i64), P]
+    lib.turboreg_split_search.argtypes = [P, P]
+    lib.turboreg_split_merge.argtypes = [P, P, i32, P, P]
     lib.turboreg_profile_begin.argtypes = [P]
     lib.turboreg_profile_end.argtypes = [P, P, P, P, i32, ctypes.POINTER(i32)]
     lib.turboreg_set_option.argtypes = [P, ctypes.c_char_p, i64]
@@ -137,7 +144,8 @@ def library():
     for name in ("turboreg_create", "turboreg_create_ex", "turboreg_set_params", "turboreg_register", "turboreg_register_batch",
                  "turboreg_get_intermediates", "turboreg_pgs_from_adjacency", "turboreg_profile_begin",
                  "turboreg_profile_end", "turboreg_point_resolution", "turboreg_ransac",
-                 "turboreg_ranked_hypotheses"):
+                 "turboreg_ranked_hypotheses", "turboreg_split_begin", "turboreg_split_buffer",
+                 "turboreg_split_sc2", "turboreg_split_search", "turboreg_split_merge"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -334,6 +342,71 @@ class TurboReg:
                                                     out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt)),
                "ranked_hypotheses")
         return out[: cnt.value]
+
+    # ------------------------------------------------------------------------------------------ NEXT(1) split
+    # One pair over several ranks (include/turboreg.h "NEXT(1)"); split.register_split drives the phases and the
+    # exchanges over torch.distributed.  `stream`: a torch.cuda.Stream or raw handle (None = torch's current).
+    @staticmethod
+    def _stream_ptr(stream):
+        if stream is None:
+            import torch
+
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+
+    def split_begin(self, src, dst, rank, world, stream=None):
+        """Phase 1; returns the pair status (0, or 2/3 when n is out of range: nothing else to do)."""
+        n = _points(src, "src")
+        if _points(dst, "dst") != n:
+            raise ValueError("src and dst must have the same number of rows")
+        ps, ks = _ptr(src, np.float32)
+        pd, kd = _ptr(dst, np.float32)
+        st = self._lib.turboreg_split_begin(self._h, ps, pd, n, int(rank), int(world), self._stream_ptr(stream))
+        if st not in (0, 2, 3):
+            raise TurboRegError(st, "split_begin")
+        self._split_keep = (ks, kd)
+        return int(st)
+
+    def split_tensor(self, which, count=None):
+        """Zero-copy torch view (int32 words; uint8 for SPLIT_RESULT) of a workspace buffer to exchange."""
+        import torch
+
+        ptr, nb = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(self._lib.turboreg_split_buffer(self._h, int(which), ctypes.byref(ptr), ctypes.byref(nb)),
+               "split_buffer")
+        if which == SPLIT_RESULT:
+            typestr, n = "|u1", nb.value
+        else:
+            typestr, n = "<i4", nb.value // 4 if count is None else int(count)
+            if n * 4 > nb.value:
+                raise ValueError("count exceeds the buffer")
+
+        class _Dev:
+            pass
+
+        d = _Dev()
+        d.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr.value or 0, False),
+                                      "version": 3, "strides": None, "stream": None}
+        return torch.as_tensor(d, device=torch.device("cuda", self.device))
+
+    def split_sc2(self, stream=None):
+        """Phase 2 (after the bits all-reduce); returns E, the number of edge words to all-reduce."""
+        e = ctypes.c_int64()
+        _check(self._lib.turboreg_split_sc2(self._h, ctypes.byref(e), self._stream_ptr(stream)), "split_sc2")
+        return int(e.value)
+
+    def split_search(self, stream=None):
+        """Phase 3 (after the edges all-reduce): this rank's record in split_tensor(SPLIT_RESULT)."""
+        _check(self._lib.turboreg_split_search(self._h, self._stream_ptr(stream)), "split_search")
+
+    def split_merge(self, parts, world, stream=None):
+        """Phase 4: T* over the `world` gathered records (a CUDA uint8 tensor of world*104 bytes)."""
+        if not _is_torch_cuda(parts) or _nbytes(parts) < int(world) * RESULT_DTYPE.itemsize:
+            raise ValueError("parts must be a CUDA tensor of world result records")
+        res = Result()
+        _check(self._lib.turboreg_split_merge(self._h, ctypes.c_void_p(parts.data_ptr()), int(world),
+                                              ctypes.byref(res), self._stream_ptr(stream)), "split_merge")
+        return result_to_dict(res)
 
     # ------------------------------------------------------------------------------------------ test views
     def intermediate(self, pair, what):

@@ -39,6 +39,7 @@ struct PairState {
     int32_t ncand;               // pivot candidates (weight >= α) collected
     int32_t cand_overflow;       // ncand > PIV_CAP: the ordered count/scan/emit path selects instead
     int32_t edge_overflow;       // E > the context's per-pair edge capacity: pair skipped (status 8)
+    int32_t pad2[4];
     uint32_t bbox[12];     // order keys of max src xyz, -min src xyz, max dst xyz, -min dst xyz (k_ingest)
     int32_t hist_hi[256];  // histogram of Ĝ_ij >> 7 over positive O2 edges
     int32_t hist_lo[128];  // histogram of Ĝ_ij & 127 within bin b1
@@ -100,7 +101,17 @@ struct WS {
                           // (r20); k_finalize adds the segments in order into slot [h][0] (deterministic)
     int32_t x_fp4;        // heavy_X holds packed e2m1 (block-scaled fp4 tensor-core path) instead of uint8
     int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
+    // NEXT(1), one pair split over split_world ranks (1 = not split): this rank's share of every split work
+    // list (compat block-row pairs from compat_b0, tensor-core tiles, dense-row items, sparse-row groups,
+    // pivots) is the contiguous range split_range(count) below
+    int32_t split_rank, split_world, compat_b0;
 };
+
+// [lo, hi) of `count` work units owned by this rank: the contiguous partition of sharding.shard_range.
+__device__ __forceinline__ void split_range(const WS& ws, int count, int* lo, int* hi) {
+    *lo = (int)((long long)ws.split_rank * count / ws.split_world);
+    *hi = (int)((long long)(ws.split_rank + 1) * count / ws.split_world);
+}
 
 // The workspace restricted to pairs [p0, p0 + count): every per-pair array advanced by p0 strides.
 inline WS ws_view(const WS& w, int p0, size_t result_bytes) {

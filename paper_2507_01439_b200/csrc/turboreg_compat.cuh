@@ -24,7 +24,8 @@ __device__ __forceinline__ float compat_kappa(const PairState* st, float t2) {
         const double ed = (double)float_from_order_key(st->bbox[6 + c]) + (double)float_from_order_key(st->bbox[9 + c]);
         smax += es * es + ed * ed;
     }
-    return __double2float_ru((double)t2 + ldexp(smax * (1.0 + 0x1p-20), -21));
+    const float k = __double2float_ru((double)t2 + ldexp(smax * (1.0 + 0x1p-20), -21));
+    return k >= 0x1p-100f ? k : __int_as_float(0x7f800000);  // absurdly small τ: κ = +inf, every test exact
 }
 
 // Repack the caller's N×3 float32 rows into float4 (x, y, z, 0) and flag non-finite input.
@@ -236,7 +237,10 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
     const f2_t mone = f2_pack(-1.0f, -1.0f);
     const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f);
     const f2_t s_hi2 = f2_pack(s_hi, s_hi);
-    const f2_t kap2 = f2_pack(kap, kap);
+    // −2^-19 (|D| + κ) in one rounding: fma(|D|, −2^-19, −2^-19 κ) = −2^-19 fl(|D| + κ) exactly (power-of-two
+    // scaling; κ ≥ 2^-100 keeps it normal, see compat_kappa), so b below is bit-identical to
+    // fma(fl(|D| + κ), −2^-19 S, |q|) of DESIGN §6.1 with one operation fewer
+    const f2_t nkap19 = f2_pack(-0x1p-19f * kap, -0x1p-19f * kap);
     // per test, in bit 31:  cc: S > s_hi (q decides);  b: |q| < Tq (q unsure);  q: q < 0.
     // decided = ~b & cc (bit 31);  edge = sign(q);  sacc keeps bit 31 while all decided.
     uint32_t colw[NT], sacc = 0xffffffffu;
@@ -259,7 +263,7 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
             // |q| − Tq with one rounding: the sign is exactly that of |q| − fl(|D| + κ)·S·2^-19
-            const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
+            const f2_t b = f2_fma(f2_fma(absD, nc19, nkap19), S, q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
             const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
             // edge bit = sign(q): only read when every test of the lane is decided (else the lane redoes all)
@@ -313,7 +317,10 @@ __device__ __forceinline__ void compat_tiles(const WS& ws, int p, int n, int W, 
 // Row-pair packing: the f32x2 lanes hold two row points (2k, 2k+1) of tile row I (negated, from shared
 // memory, one LDS.128 + one LDS.64 per coordinate triple), each lane's NC column points are scalar
 // broadcast operands held in registers.  Same per-test arithmetic as compat_tiles.
-template <int NC, int UNR>
+// DIAG: tile k = 0 is the diagonal tile (J == I).  Its self tests (row r = lane) have S = 0, which the
+// filter cannot certify (S <= τ²(1 + 2^-16)); they are excluded from the decided mask (C_ii = 0 is masked
+// off below anyway), so a diagonal item no longer sends every lane through the exact tree.
+template <int NC, int UNR, bool DIAG = false>
 __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int W, int T, int I, int J,
                                                 const float4* s_rs, const float4* s_rd, const float4* s_pxy,
                                                 const float2* s_pz, const float4* s_qxy, const float2* s_qz,
@@ -341,10 +348,14 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
     const f2_t mone = f2_pack(-1.0f, -1.0f);
     const float s_hi = __fmul_rn(t2, 1.0f + 0x1p-16f);
     const f2_t s_hi2 = f2_pack(s_hi, s_hi);
-    const f2_t kap2 = f2_pack(kap, kap);
+    // −2^-19 (|D| + κ) in one rounding: fma(|D|, −2^-19, −2^-19 κ) = −2^-19 fl(|D| + κ) exactly (power-of-two
+    // scaling; κ ≥ 2^-100 keeps it normal, see compat_kappa), so b below is bit-identical to
+    // fma(fl(|D| + κ), −2^-19 S, |q|) of DESIGN §6.1 with one operation fewer
+    const f2_t nkap19 = f2_pack(-0x1p-19f * kap, -0x1p-19f * kap);
     uint32_t colw[NC], sacc = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < NC; ++k) colw[k] = 0u;
+    const uint32_t selfw = DIAG ? (1u << lane) : 0u;  // the lane's own row (DIAG)
 #pragma unroll UNR
     for (int kk = 0; kk < 16; ++kk) {
         const float4 P = s_pxy[kk];
@@ -366,9 +377,13 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
             const f2_t q = f2_fma(D, D, f2_fma(S, m2t2x2, t4x2));
             const f2_t absD = D & 0x7fffffff7fffffffull;
             // |q| − Tq with one rounding: the sign is exactly that of |q| − fl(|D| + κ)·S·2^-19
-            const f2_t b = f2_fma(f2_add(absD, kap2), f2_mul(S, nc19), q & 0x7fffffff7fffffffull);
+            const f2_t b = f2_fma(f2_fma(absD, nc19, nkap19), S, q & 0x7fffffff7fffffffull);
             const f2_t cc = f2_fma(S, mone, s_hi2);
-            const uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
+            uint32_t k0 = f2_lo(cc), k1 = f2_hi(cc);
+            if (DIAG && k == 0) {  // rows 2kk, 2kk+1 of the diagonal tile: the self test is not a test
+                k0 |= (selfw << (31 - 2 * kk)) & 0x80000000u;
+                k1 |= (selfw << (30 - 2 * kk)) & 0x80000000u;
+            }
             // edge bit = sign(q): only read when every test of the lane is decided (else the lane redoes all)
             colw[k] = __funnelshift_l(f2_lo(q), colw[k], 1);
             colw[k] = __funnelshift_l(f2_hi(q), colw[k], 1);
@@ -432,7 +447,7 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
     const int T = (n + 31) >> 5;
     // `split` blocks share a block-row pair (small batches: enough blocks to fill the GPU); block part sp
     // takes every split-th item of the pair's work list
-    const int b = blockIdx.x / split, sp = blockIdx.x % split;
+    const int b = ws.compat_b0 + blockIdx.x / split, sp = blockIdx.x % split;
     if (2 * b >= T) return;
     const int warp = threadIdx.x >> 5;
     const float4* s4 = ws.src4 + p * ws.pts_stride;
@@ -479,12 +494,19 @@ __global__ void __launch_bounds__(256, MINB) k_compat(WS ws, int split) {
         const float kap = s_kap;
         if constexpr (NP < 0) {
             constexpr int NC = -NP;
-            const int P0 = (T - I0 + NC - 1) / NC, P1 = (I1 != I0) ? (T - I1 + NC - 1) / NC : 0;
+            // per block-row: item 0 is the diagonal tile alone (its self tests are excluded from the filter's
+            // decided mask, DIAG), then the tiles right of it NC at a time
+            const int P0 = 1 + (T - I0 - 1 + NC - 1) / NC, P1 = (I1 != I0) ? 1 + (T - I1 - 1 + NC - 1) / NC : 0;
             for (int t = warp + 8 * sp; t < P0 + P1; t += 8 * split) {
                 const bool second = t >= P0;
-                const int I = second ? I1 : I0, J = I + NC * (second ? t - P0 : t), o = second ? 32 : 0, h = second;
-                compat_tiles_rp<NC, UNR>(ws, p, n, W, T, I, J, s_rs + o, s_rd + o, s_pxy[h], s_pz[h], s_qxy[h],
-                                         s_qz[h], kap);
+                const int u = second ? t - P0 : t;
+                const int I = second ? I1 : I0, o = second ? 32 : 0, h = second;
+                if (u == 0)
+                    compat_tiles_rp<1, UNR, true>(ws, p, n, W, T, I, I, s_rs + o, s_rd + o, s_pxy[h], s_pz[h],
+                                                  s_qxy[h], s_qz[h], kap);
+                else
+                    compat_tiles_rp<NC, UNR>(ws, p, n, W, T, I, I + 1 + NC * (u - 1), s_rs + o, s_rd + o, s_pxy[h],
+                                             s_pz[h], s_qxy[h], s_qz[h], kap);
             }
             return;
         }

@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
                      : "memory");
     };
     if (threadIdx.x == 0) issue(0);
-    const uint32_t thr2b = __float_as_uint(__fmul_rn(ws.thr, ws.thr));
+    const uint32_t thr1b = __float_as_uint(__fmul_rn(ws.thr, ws.thr)) + 1u;
     f2_t Rp[NP][9], tp[NP][3];
 #pragma unroll
     for (int m = 0; m < NP; ++m) {
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
         for (int k = 0; k < 3; ++k) tp[m][k] = f2_pack(Rh[2 * m][9 + k], Rh[2 * m + 1][9 + k]);
     }
     const f2_t mone = f2_pack(-1.0f, -1.0f);
-    int cnt[NH];
+    uint32_t cnt[NH];
     double ea[NH], es[NH];  // ERR: Σ sqrtf(s), Σ s per hypothesis (r20)
 #pragma unroll
     for (int u = 0; u < NH; ++u) { cnt[u] = 0; ea[u] = es[u] = 0.0; }
@@ -420,9 +420,11 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
                 const f2_t e1 = f2_fma(f2_pack(y.y, y.y), mone, p1);
                 const f2_t e2 = f2_fma(f2_pack(y.z, y.z), mone, p2);
                 const f2_t sq = f2_fma(e2, e2, f2_fma(e1, e1, f2_mul(e0, e0)));
-                // s >= 0, so integer order of the bit patterns is float order
-                cnt[2 * m] += f2_lo(sq) <= thr2b;
-                cnt[2 * m + 1] += f2_hi(sq) <= thr2b;
+                // s >= 0 (or +inf), so integer order of the bit patterns is float order: s <= thr2 ⇔ the
+                // 31-bit difference s − (thr2 + 1) is negative; its sign bit is added (IADD3 + LEA.HI, no
+                // predicate)
+                cnt[2 * m] += (f2_lo(sq) - thr1b) >> 31;
+                cnt[2 * m + 1] += (f2_hi(sq) - thr1b) >> 31;
                 if constexpr (ERR) {
                     const float s0 = __uint_as_float(f2_lo(sq)), s1 = __uint_as_float(f2_hi(sq));
                     ea[2 * m] += (double)__fsqrt_rn(s0);

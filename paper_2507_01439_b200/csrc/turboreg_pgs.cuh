@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws
     // the pivot slot is read before |P| is known (both loads in flight; slots >= |P| are never used)
     const int4 pvt = ws.piv[q * ws.piv_stride + pv];
     const int P = ws.st[q].npiv;
-    if (pv >= P) {
+    int pv_lo, pv_hi;  // this rank's pivots (all of them unless the pair is split): others leave empty slots
+    split_range(ws, P, &pv_lo, &pv_hi);
+    if (pv >= P || pv < pv_lo || pv >= pv_hi) {
         for (int r = lane; r < K2; r += 32) out[r] = make_int4(-1, -1, -1, 0);
         return;
     }

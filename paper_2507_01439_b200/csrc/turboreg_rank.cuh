@@ -125,4 +125,36 @@ __global__ void k_rank_count(const RankKey* keys, const int32_t* idx, int m2, in
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// ------------------------------------------------------------------------------------------ NEXT(1) merge
+// A pair split over `world` ranks: each rank's record holds the argmax over its own pivots' TurboCliques
+// (k_finalize).  T* is the maximum of those by the same key (count desc, S desc, (i,j,z) asc, reading r14);
+// clique and hypothesis counts add up; |P|, E and the per-pair status are the same on every rank.
+__global__ void k_split_merge(const DevResult* parts, int world, DevResult* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int best = -1, ncl = 0, nev = 0;
+    for (int r = 0; r < world; ++r) {
+        const DevResult& a = parts[r];
+        ncl += a.num_cliques;
+        nev += a.hypotheses_evaluated;
+        if (a.status != 0) continue;
+        if (best < 0) { best = r; continue; }
+        const DevResult& b = parts[best];
+        const unsigned long long ka = ((unsigned long long)(unsigned)a.inlier_count << 17) | (unsigned)a.clique_weight;
+        const unsigned long long kb = ((unsigned long long)(unsigned)b.inlier_count << 17) | (unsigned)b.clique_weight;
+        const unsigned long long ta = ((unsigned long long)a.clique[0] << 30) | ((unsigned long long)a.clique[1] << 15) | a.clique[2];
+        const unsigned long long tb = ((unsigned long long)b.clique[0] << 30) | ((unsigned long long)b.clique[1] << 15) | b.clique[2];
+        if (ka > kb || (ka == kb && ta < tb)) best = r;
+    }
+    DevResult o = parts[best >= 0 ? best : 0];
+    if (best < 0) {  // no rank has a hypothesis: the shared status (2/3/4/8), else NO_HYPOTHESIS
+        int st = 5;
+        for (int r = 0; r < world; ++r)
+            if (parts[r].status != 5 && parts[r].status != 0) st = parts[r].status;
+        o.status = st;
+    }
+    o.num_cliques = ncl;
+    o.hypotheses_evaluated = nev;
+    *out = o;
+}
+
 }  // namespace trk

@@ -51,14 +51,16 @@ enum KernelId {
     KID_FINALIZE,
     KID_RANSAC,
     KID_ROWSUM,
+    KID_ZERO_EDGES,
+    KID_MERGE,
     KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_ingest",   "k_compat",       "k_degree",      "k_heavy",       "k_rowclass",
                                        "k_expand",   "k_sc2_mma",      "k_emit_hh",     "k_sc2",         "k_sc2_light",   "k_hist_hi",     "k_hist_lo",     "k_alpha",       "k_collect",     "k_pivot_sort",
                                        "k_select_count", "k_select_scan", "k_select_emit", "k_pgs",
-                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize",    "k_ransac_sample", "k_rowsum"};
+                                       "k_canon",    "k_kabsch",   "k_score",        "k_finalize",    "k_ransac_sample", "k_rowsum", "k_zero_edges", "k_split_merge"};
 // stage of each kernel for turboreg_result.stage_ms: 0 graph (O2Graph construction), 1 PGS, 2 model
-const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 1, 0};
+const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 1, 0, 0, 2};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
@@ -107,6 +109,7 @@ struct turboreg_ctx {
     void* rank_buf = nullptr;
     size_t rank_bytes = 0;
     int32_t* d_rowsum = nullptr;  // [max_batch][max_n] r_i (TURBOREG_F_ROW_SUMS)
+    int32_t split_rank = 0, split_world = 1;  // NEXT(1): this context's share of a split pair (1 = no split)
     turboreg_result* h_results = nullptr;
     float* h_inputs = nullptr;
     // bookkeeping of the last call
@@ -344,6 +347,9 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.k1 = c->prm.k1;
     c->ws.k2 = c->prm.k2;
     c->ws.mode = c->prm.graph_mode;
+    c->ws.split_rank = 0;
+    c->ws.split_world = 1;
+    c->ws.compat_b0 = 0;
     {
         const int rank = (c->prm.flags & TURBOREG_F_RANK_MAE) ? 1 : (c->prm.flags & TURBOREG_F_RANK_MSE) ? 2 : 0;
         c->ws.err_mode = ((rank || (c->prm.flags & TURBOREG_F_HYP_ERRORS)) ? 1 : 0) | (rank << 1);
@@ -415,18 +421,22 @@ void harvest_events(turboreg_ctx* c, float* stage_ms) {
 
 enum RunMode { RUN_FULL = 0, RUN_FROM_ADJ = 1, RUN_RANSAC = 2 };
 
-// phase: PH_ALL = the whole path; PH_HEAD = state reset + ingest + compat (per pipelined sub-batch);
-// PH_TAIL = everything after compat.
-enum Phase { PH_ALL = 0, PH_HEAD = 1, PH_TAIL = 2 };
+// phase (bit set): PH_HEAD = state reset + ingest + compat (per pipelined sub-batch); PH_GRAPH = degrees, row
+// classes and the SC^2 assembly; PH_SEARCH = pivots, PGS, Kabsch, scoring, argmax.  PH_TAIL = everything after
+// compat.  A split pair (NEXT(1)) runs the three separately, with an exchange between them.
+enum Phase { PH_HEAD = 1, PH_GRAPH = 2, PH_SEARCH = 4, PH_TAIL = 6, PH_ALL = 7 };
 
 turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, cudaStream_t s, RunMode mode,
                            int32_t p0 = 0, int phase = PH_ALL) {
     trk::WS ws = p0 ? trk::ws_view(c->ws, p0, sizeof(turboreg_result)) : c->ws;
+    ws.split_rank = c->split_rank;
+    ws.split_world = c->split_world;
+    const bool splitp = c->split_world > 1;
     const bool timed = c->profiling || (c->prm.flags & TURBOREG_F_STAGE_TIMING);
     Launcher L{c, s, timed};
     const int Wb = words_per_row(std::max(maxn_batch, 1));
     const unsigned B = (unsigned)batch;
-    if (phase != PH_TAIL) {
+    if (phase & PH_HEAD) {
         CK(cudaMemsetAsync(ws.st, 0, sizeof(trk::PairState) * batch, s));
         CK(cudaMemsetAsync(c->d_counters, 0, sizeof(int) * 16, s));
     }
@@ -454,15 +464,23 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         CK(L.run(KID_FINALIZE, [&] { trk::k_finalize<<<B, 1024, 0, s>>>(wr); }));
         return TURBOREG_OK;
     }
-    if (mode == RUN_FULL && phase != PH_TAIL) {
+    if (mode == RUN_FULL && (phase & PH_HEAD)) {
         CK(L.run(KID_INGEST, [&] {
             trk::k_ingest<<<dim3((maxn_batch + 255) / 256, B), 256, 0, s>>>(ws);
         }));
         const int T = (maxn_batch + 31) / 32;
-        // small batches: several blocks share a block-row pair so the grid still covers ~2 waves
-        const int bpp = (T + 1) / 2;
-        const int split = std::max(1, std::min(16, (5 * c->num_sms + bpp * batch - 1) / (bpp * batch)));
-        CK(L.run(KID_COMPAT, [&] {
+        // small batches: several blocks share a block-row pair so the grid still covers ~2 waves; a split pair
+        // computes only this rank's block-row pairs, into a zeroed bit matrix (the ranks' matrices are summed)
+        int bpp = (T + 1) / 2;
+        if (splitp) {
+            const int b0 = (int)((int64_t)c->split_rank * bpp / c->split_world);
+            const int b1 = (int)((int64_t)(c->split_rank + 1) * bpp / c->split_world);
+            ws.compat_b0 = b0;
+            bpp = std::max(b1 - b0, 0);
+            CK(cudaMemsetAsync(ws.bits, 0, sizeof(uint32_t) * (size_t)ws.bits_stride * batch, s));
+        }
+        const int split = std::max(1, std::min(16, (5 * c->num_sms + std::max(bpp, 1) * batch - 1) / (std::max(bpp, 1) * batch)));
+        if (bpp > 0) CK(L.run(KID_COMPAT, [&] {
             const dim3 g((unsigned)(bpp * split), B);
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws, split);
             else if (c->opt_compat_variant == 1) trk::k_compat<false, 5, 16, 1><<<g, 256, 0, s>>>(ws, split);
@@ -470,11 +488,13 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else trk::k_compat<false, 5, 16, -2><<<g, 256, 0, s>>>(ws, split);
         }));
     }
-    if (phase == PH_HEAD) return TURBOREG_OK;
+    if (!(phase & PH_TAIL)) return TURBOREG_OK;
+    if (phase & PH_GRAPH) {
     const dim3 grow((maxn_batch + trk::DEG_ROWS_PER_BLOCK - 1) / trk::DEG_ROWS_PER_BLOCK, B);
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_ROWCLASS, [&] { trk::k_rowclass<<<B, 1024, 0, s>>>(ws); }));
+    if (splitp) CK(L.run(KID_ZERO_EDGES, [&] { trk::k_zero_edges<<<dim3(2 * c->num_sms, B), 256, 0, s>>>(ws); }));
     if (ws.sc2_path != 1) {
         CK(L.run(KID_EXPAND, [&] {
             const dim3 ge((unsigned)(ws.heavy_X_stride / ws.heavy_Kcap / 8), B);
@@ -552,6 +572,8 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             trk::k_rowsum<<<dim3((unsigned)((maxn_batch + 63) / 64), B), 256, 0, s>>>(ws, rs, c->max_n);
         }));
     }
+    }  // PH_GRAPH
+    if (!(phase & PH_SEARCH)) return TURBOREG_OK;
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
     const int sel_bpp = std::max(trk::SEL_BLOCKS_PER_PAIR, std::min((4 * c->num_sms + batch - 1) / batch, 256));
     const dim3 gflat((unsigned)sel_bpp, B);
@@ -690,7 +712,10 @@ turboreg_status turboreg_create_ex(const turboreg_params* params, int device, in
     c->max_n = max_n;
     c->max_batch = max_batch;
     c->Wmax = words_per_row(max_n);
-    c->heavy_cap_alloc = (int32_t)std::max<int64_t>(256, std::min<int64_t>(round_up(max_n, 256), HEAVY_CAP_MAX));
+    // the tensor-core block holds up to 2048 heavy rows for max_n <= 8192 (config-E pairs: |H| ≈ 1250), and up
+    // to half the rows beyond (large N: an inlier block of thousands of rows)
+    const int64_t hcap = max_n <= 8192 ? HEAVY_CAP_MAX : round_up((max_n + 1) / 2, 256);
+    c->heavy_cap_alloc = (int32_t)std::max<int64_t>(256, std::min<int64_t>(round_up(max_n, 256), hcap));
     c->edge_cap = (max_edges == 0 || max_edges > full_edges) ? full_edges : max_edges;
     turboreg_status st = TURBOREG_OK;
     // A blocking stream: it orders itself with the legacy default stream, so inputs produced there (e.g. by
@@ -875,6 +900,8 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
         if (offsets[p] < 0 || n[p] < 0) return TURBOREG_ERR_INVALID_ARGUMENT;
     if (!c->d_base) return TURBOREG_ERR_OUT_OF_MEMORY;
     CK(cudaSetDevice(c->device));
+    c->split_rank = 0;
+    c->split_world = 1;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
     const bool dev_in = is_device_ptr(src) && is_device_ptr(dst);
     const bool dev_out = is_device_ptr(out);
@@ -1244,6 +1271,110 @@ turboreg_status turboreg_ranked_hypotheses(turboreg_ctx* c, int32_t pair, int32_
     return TURBOREG_OK;
 }
 
+// ------------------------------------------------------------------------------------------ NEXT(1)
+turboreg_status turboreg_split_begin(turboreg_ctx* c, const float* src, const float* dst, int32_t n, int32_t rank,
+                                     int32_t world, void* stream) {
+    if (!c || !src || !dst || world < 1 || world > 4096 || rank < 0 || rank >= world) return TURBOREG_ERR_INVALID_ARGUMENT;
+    // the split covers the paper's path: O2 mode, inlier-number ranking, the tensor-core or popcount SC^2 block
+    if (c->prm.graph_mode != 0 || c->opt_sc2_path == 2 ||
+        (c->prm.flags & (TURBOREG_F_HYP_ERRORS | TURBOREG_F_RANK_MAE | TURBOREG_F_RANK_MSE | TURBOREG_F_ROW_SUMS)))
+        return TURBOREG_ERR_INVALID_ARGUMENT;
+    if (n < 3) return TURBOREG_ERR_TOO_FEW_POINTS;
+    if (n > c->max_n) return TURBOREG_ERR_TOO_MANY_POINTS;
+    if (!c->d_base) return TURBOREG_ERR_OUT_OF_MEMORY;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    if (is_device_ptr(src) != is_device_ptr(dst)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    int dslot = 0;
+    trk::PairDesc* hd = next_desc(c, &dslot);
+    CK(begin_call(c, s));
+    const float* ds = src;
+    const float* dd = dst;
+    if (!is_device_ptr(src)) {  // stage host inputs in the context's input area
+        float* in = c->d_inputs;
+        CK(cudaMemcpyAsync(in, src, sizeof(float) * 3 * (size_t)n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(in + 3 * (size_t)c->max_n * c->max_batch, dst, sizeof(float) * 3 * (size_t)n,
+                           cudaMemcpyHostToDevice, s));
+        ds = in;
+        dd = in + 3 * (size_t)c->max_n * c->max_batch;
+    }
+    hd[0] = trk::PairDesc{ds, dd, n, words_per_row(n), 0, 0};
+    CK(cudaMemcpyAsync(c->d_desc, hd, sizeof(trk::PairDesc), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->ev_desc[dslot], s));
+    c->split_rank = rank;
+    c->split_world = world;
+    c->last_batch = 1;
+    c->last_n.assign(1, n);
+    const turboreg_status st = launch_all(c, 1, n, s, RUN_FULL, 0, PH_HEAD);
+    if (st != TURBOREG_OK) return st;
+    CK(end_call(c, s));
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_split_buffer(turboreg_ctx* c, int32_t which, void** dev_ptr, size_t* bytes) {
+    if (!c || !dev_ptr || !bytes || c->last_batch < 1 || c->last_n.empty()) return TURBOREG_ERR_INVALID_ARGUMENT;
+    const int n = c->last_n[0];
+    if (n < 3 || n > c->max_n) return TURBOREG_ERR_INVALID_ARGUMENT;
+    switch (which) {
+        case TURBOREG_SPLIT_BITS: *dev_ptr = c->ws.bits; *bytes = sizeof(uint32_t) * (size_t)n * words_per_row(n); break;
+        case TURBOREG_SPLIT_EDGES: *dev_ptr = c->ws.edges; *bytes = sizeof(uint32_t) * (size_t)c->ws.edges_stride; break;
+        case TURBOREG_SPLIT_RESULT: *dev_ptr = c->d_results; *bytes = sizeof(turboreg_result); break;
+        default: return TURBOREG_ERR_INVALID_ARGUMENT;
+    }
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_split_sc2(turboreg_ctx* c, int64_t* num_edges, void* stream) {
+    if (!c || !num_edges || c->split_world < 1 || c->last_n.empty()) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    CK(begin_call(c, s));
+    const turboreg_status st = launch_all(c, 1, c->last_n[0], s, RUN_FULL, 0, PH_GRAPH);
+    if (st != TURBOREG_OK) return st;
+    int32_t E = 0;
+    CK(cudaMemcpyAsync(&E, &c->ws.st[0].edges, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(end_call(c, s));
+    CK(cudaStreamSynchronize(s));
+    *num_edges = E;
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_split_search(turboreg_ctx* c, void* stream) {
+    if (!c || c->last_n.empty()) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    CK(begin_call(c, s));
+    const turboreg_status st = launch_all(c, 1, c->last_n[0], s, RUN_FULL, 0, PH_SEARCH);
+    if (st != TURBOREG_OK) return st;
+    CK(end_call(c, s));
+    return TURBOREG_OK;
+}
+
+turboreg_status turboreg_split_merge(turboreg_ctx* c, const void* parts, int32_t world, turboreg_result* out,
+                                     void* stream) {
+    if (!c || !parts || !out || world < 1 || !is_device_ptr(parts)) return TURBOREG_ERR_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    CK(begin_call(c, s));
+    trk::k_split_merge<<<1, 32, 0, s>>>(static_cast<const trk::DevResult*>(parts), world,
+                                        static_cast<trk::DevResult*>(c->d_results));
+    CK(cudaGetLastError());
+    c->launches++;
+    c->k_launches[KID_MERGE]++;
+    c->split_rank = 0;
+    c->split_world = 1;
+    if (is_device_ptr(out)) {
+        CK(cudaMemcpyAsync(out, c->d_results, sizeof(turboreg_result), cudaMemcpyDeviceToDevice, s));
+        CK(end_call(c, s));
+    } else {
+        CK(cudaMemcpyAsync(c->h_results, c->d_results, sizeof(turboreg_result), cudaMemcpyDeviceToHost, s));
+        CK(end_call(c, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(out, c->h_results, sizeof(turboreg_result));
+    }
+    return TURBOREG_OK;
+}
+
 turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bits, int32_t n, int32_t stride_words) {
     if (!c || !bits || n < 3 || n > c->max_n || stride_words < (n + 31) / 32) return TURBOREG_ERR_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
@@ -1257,6 +1388,8 @@ turboreg_status turboreg_pgs_from_adjacency(turboreg_ctx* c, const uint32_t* bit
             rows[(size_t)r * W + k] = v;
         }
     cudaStream_t s = c->own_stream;
+    c->split_rank = 0;
+    c->split_world = 1;
     int dslot = 0;
     trk::PairDesc* hd = next_desc(c, &dslot);
     CK(begin_call(c, s));

@@ -6,14 +6,12 @@
 namespace trk {
 
 // ------------------------------------------------------------------------------------------ a3 SC^2
-// Eq. 2 for every O2 edge (i < j), assembled in row i's rank order.  One warp per row i;
-// U_i's words are enumerated lane-parallel (lane = word, rank = warp prefix of popcounts), one edge per
-// lane per round:
-//   * both endpoints heavy → Ĝ_ij was computed on the tensor cores: gather D[hpos i][hpos j];
-//   * otherwise (the sparse remainder) → popcount(row_i AND row_j): row_i in registers (lane-strided),
-//     G light edges at a time so G·WPL row_j loads are in flight, REDUX per edge.
-// The result (j << 16 | Ĝ_ij) goes to edges[rowptr(i) + rank]; positive weights feed a 256-bin histogram
-// of Ĝ >> 7 (the high digit of the pivot radix select, Eq. 4).
+// Eq. 2 for every O2 edge (i < j), written as (j << 16 | Ĝ_ij) to edges[rowptr(i) + rank of j
+// in U_i] (compact, rank-indexed rows).  Three passes write disjoint sets of edges:
+//   * both endpoints heavy → the tensor-core epilogue (k_sc2_mma; k_emit_hh on the cross-check path);
+//   * one endpoint dense (heavy, or degree > LIST_MAX) → k_sc2 below, from the dense row's side;
+//   * both sparse → k_sc2_light.
+// The pivot passes (turboreg_select.cuh) then histogram the positive weights for the radix select (Eq. 4).
 constexpr int SC2_WARPS = 8;
 constexpr int DEG_ROWS_PER_BLOCK = 64;  // k_degree: rows per 8-warp block
 constexpr int SEL_WARPS = 8;
@@ -178,7 +176,9 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
     // work item = (dense row, group of cpi 32-word chunks of its row): rows with many dense neighbours
     // are spread over several warps
     const int ngrp = (nchunks + cpi - 1) / cpi;
-    for (int item = blockIdx.x * SC2_WARPS + warp; item < nd * ngrp; item += nw) {
+    int it_lo, it_hi;  // this rank's items (all of them unless the pair is split over ranks)
+    split_range(ws, nd * ngrp, &it_lo, &it_hi);
+    for (int item = it_lo + blockIdx.x * SC2_WARPS + warp; item < it_hi; item += nw) {
         const int kq = item / ngrp, c_lo = (item - kq * ngrp) * cpi, c_hi = min(nchunks, c_lo + cpi);
         const int i = ws.dense_list[p * ws.row_stride + kq];
         const uint32_t* ri = bits + (int64_t)i * W;
@@ -368,6 +368,16 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
     }
 }
 
+// NEXT(1) split mode: every rank assembles only its share of the edges, so the pair's E edge words are
+// cleared first (the ranks' arrays are then summed: each word is written by exactly one rank).
+__global__ void __launch_bounds__(256) k_zero_edges(WS ws) {
+    const int p = blockIdx.y;
+    if (ws.desc[p].n == 0) return;
+    const int E = ws.st[p].edges;
+    uint32_t* e = ws.edges + p * ws.edges_stride;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < E; k += gridDim.x * blockDim.x) e[k] = 0u;
+}
+
 // SC^2 edges of the sparse rows, packed for full lanes: a warp takes LG sparse rows (bitmaps and lists
 // staged in shared memory), enumerates all their upper edges, and pushes them into two queues — j sparse
 // (|L_j ∩ N(i)| against row i's bitmap) and j dense (|L_i ∩ N(j)| against row j's words) — each flushed
@@ -414,8 +424,11 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int W = d.W;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nl = ws.st[p].n_light;
-    const int g0 = (blockIdx.x * 8 + warp) * LG;
-    if (g0 >= nl) return;
+    int gr_lo, gr_hi;  // this rank's groups of LG sparse rows (all of them unless the pair is split)
+    split_range(ws, (nl + LG - 1) / LG, &gr_lo, &gr_hi);
+    const int gi = gr_lo + blockIdx.x * 8 + warp;
+    if (gi >= gr_hi) return;
+    const int g0 = gi * LG;
     const int nr = min(LG, nl - g0);
     uint32_t* bm = s_dyn + warp * light_warp_words<WPL, LG>();
     uint16_t* ls = reinterpret_cast<uint16_t*>(bm + LG * 32 * WPL);

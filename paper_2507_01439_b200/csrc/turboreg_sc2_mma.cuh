@@ -2,16 +2,19 @@
 // SC^2 on the dense block: Ĝ = C ⊙ (C·C) (Eq. 2) restricted to the "heavy" rows H (the
 // high-degree rows — on registration workloads the inliers, whose mutual compatibility is dense).
 // C·C over H is a dense binary contraction, so it runs on the 5th-gen tensor cores:
-//   X = C[H, :] as uint8 0/1 (K-major, [h][K]),  D = X · X^T  (exact: int32 accumulate, K <= 32768)
-// with tcgen05.mma kind::i8 (M=128, N=256, K=32 per instruction), operands staged by TMA
+//   X = C[H, :] (K-major, [h][K]),  D = X · X^T  (exact: every product is 0 or 1, every count < 2^24)
+// by default as packed e2m1 (bit → 1.0 / 0.0) with tcgen05.mma kind::mxf4.block_scale (M=128, N=240,
+// K=64 per instruction, unit UE8M0 block scales in TMEM, fp32 accumulate); option mma_fp4 = 0 runs uint8
+// 0/1 operands with kind::i8 (M=128, N=256, K=32, int32 accumulate).  Operands are staged by TMA
 // (cp.async.bulk.tensor, 128B swizzle) through a 4-stage mbarrier pipeline.
-// Persistent: one CTA per SM walks the (pair, tile) list of the whole batch; the accumulator is double
-// buffered in TMEM (2 × 256 columns) so the epilogue of tile t overlaps the MMAs of tile t+1.
-// The epilogue (4 warps, tcgen05.ld 32x32b, thread = output row a) does not store D: it keeps the entries
+// Persistent: one CTA per SM walks the (pair, tile) list of the whole batch (or one rank's tile range of a
+// split pair); the accumulator is double buffered in TMEM (2 × 256 columns) so the epilogue of tile t
+// overlaps the MMAs of tile t+1.  The epilogue (16 warps, 4 per TMEM lane quarter, tcgen05.ld 32x32b)
+// does not store D: it transposes 32×32 chunks through shared memory (lane = column), keeps the entries
 // that are O2 edges — b > a and C[H_a][H_b] = 1, tested on row H_a's upper words — and writes each
 // straight to its slot in the compact edge list, rowptr(H_a) + rank of H_b in U_{H_a} (prefix counts
 // per word from k_expand).  Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread
-// MMA issuer, warps 2..17 = epilogue (4 per TMEM lane quarter).  Which rows are heavy only changes speed.
+// MMA issuer, warps 2..17 = epilogue.  Which rows are heavy only changes speed.
 // =====================================================================================================
 #pragma once
 #include <cuda.h>
@@ -213,6 +216,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(gen_tptr);
+    // global tile range of this launch: every tile, or this rank's share of a split pair (batch 1, table)
+    int g_lo = 0, g_hi = 0x7fffffff;
+    if (ws.split_world > 1 && table) split_range(ws, s_tpre[batch], &g_lo, &g_hi);
     if constexpr (FP4) {  // block scales: UE8M0 127 (= 1.0) in every byte of columns 496..511
         if (warp >= 2 && warp < 6) {
             const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 496u;
@@ -236,7 +242,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             TableCursor tc{s_tpre, s_th, TN};
             int it = 0;
             int p, rb, cb, h;
-            for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
+            for (int g = g_lo + blockIdx.x;
+                 g < g_hi && (table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h));
                  g += gridDim.x) {
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
@@ -259,7 +266,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             TableCursor tc{s_tpre, s_th, TN};
             int it = 0, lt = 0;
             int p, rb, cb, h;
-            for (int g = blockIdx.x; table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h);
+            for (int g = g_lo + blockIdx.x;
+                 g < g_hi && (table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h));
                  g += gridDim.x, ++lt) {
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 const int acc = lt & 1;
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         cur.TN = TN;
         TableCursor tc{s_tpre, s_th, TN};
         auto locate = [&](int gq, int* pp, int* rbp, int* cbp, int* hp) {
-            return table ? tc.locate(batch, gq, pp, rbp, cbp, hp) : cur.locate(ws, batch, gq, pp, rbp, cbp, hp);
+            return gq < g_hi && (table ? tc.locate(batch, gq, pp, rbp, cbp, hp) : cur.locate(ws, batch, gq, pp, rbp, cbp, hp));
         };
         // per-warp tile metadata in registers (no block barrier between tiles): the heavy ids of this warp's
         // columns (lane = column of chunks sub and sub + MMA_EPI_SUB) and its rows' edge-list bases (lane =
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             return (k < TN && cbq * TN + k < hq) ? __ldg(hlq + cbq * TN + k) : -1;
         };
         int p, rb, cb, h;
-        int g = blockIdx.x;
+        int g = g_lo + blockIdx.x;
         bool have = locate(g, &p, &rb, &cb, &h);
         int jb0 = -1, jb1 = -1;
         if (have) {

@@ -31,6 +31,17 @@ want = {
     "sm__ops_path_tensor_src_int8.sum": "tensor_int8_ops",
     "sm__ops_path_tensor_src_int8.sum.per_second": "tensor_int8_ops_per_s",
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active": "mem_tensor_active_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_inst_pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_inst_pct",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_inst_pct",
+    "sm__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "smsp__inst_executed.sum": "inst_executed",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active": "shared_pipe_pct",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
 }
 idx = {k: hdr.index(k) for k in want if k in hdr}
 ki = hdr.index("Kernel Name")
@@ -71,7 +82,10 @@ with open(out + ".txt", "w") as f:
         f.write(f"{k:22s} dur {v.get('duration', 0):9.1f} us  dram {v['dram_bytes']/1e6:9.2f} MB  "
                 f"sm {v.get('sm_throughput_pct', 0):5.1f}%  tensor {v.get('tensor_pipe_pct', 0):5.1f}%  "
                 f"occ {v.get('occupancy_pct', 0):5.1f}%  ipc {v.get('ipc', 0):4.2f}  regs {v.get('registers', 0):.0f}"
-                + (f"  int8 {v['tensor_int8_ops']/1e9:.1f} Gop" if v.get("tensor_int8_ops") else "") + "\n")
+                + (f"  int8 {v['tensor_int8_ops']/1e9:.1f} Gop" if v.get("tensor_int8_ops") else "")
+                + f"  issue {v.get('issue_active_pct', 0):5.1f}%  fma {v.get('fma_pipe_pct', 0):5.1f}%"
+                + f"  alu {v.get('alu_pipe_pct', 0):5.1f}%  l2hit {v.get('l2_hit_pct', 0):5.1f}%"
+                + f"  dram {v.get('dram_pct', 0):5.1f}%  inst {v.get('inst_executed', 0)/1e6:.1f}M\n")
 print(open(out + ".txt").read())
 
 if len(sys.argv) > 3:

@@ -1,14 +1,17 @@
 #!/bin/bash
-# Round evidence for profiles/<round>/ (run on the GPU box from the repo root; outputs in gpurun_out/):
-#   bench line, ncu launch list of the bench command, ncu --set full of the top kernels.
+# Round evidence for profiles/<round>/ (run on the GPU box from the repo root; outputs in gpurun_out/<round>/):
+#   bench line, ncu launch list of the bench command, ncu --set full of every kernel >= ~1 % of the step.
 # Each ncu pass runs only after the same command has exited 0 without ncu.
 set -e
-mkdir -p gpurun_out
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_ll.log 2>&1
-python tools/perf_probe.py --pairs 203 --cfg E > gpurun_out/perf.json
+R=${1:-r02}
+O=gpurun_out/$R
+mkdir -p $O
+python bench.py > $O/bench.json 2> $O/bench.err
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-context"
+$CMD > $O/plain_ll.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_ll.log 2>&1
+CMD2="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-context"
+$CMD2 > $O/plain_full.log 2>&1 && \
 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_compat|k_sc2_mma|k_score|k_sc2|k_pgs|k_degree|k_expand|k_hist|k_collect" -c 10 \
-    -o gpurun_out/prof_full -f python tools/perf_probe.py --pairs 203 --cfg E > gpurun_out/ncu_full.log 2>&1
+    -k regex:"k_compat|k_sc2|k_score|k_pgs|k_degree|k_expand|k_hist|k_collect" -c 11 \
+    -o $O/prof_full -f $CMD2 > $O/ncu_full.log 2>&1
