@@ -82,6 +82,7 @@ struct WS {
     int32_t* light_list;  // [n] sparse non-heavy rows, index order
     int32_t* dense_list;  // [n] all other rows, index order
     int64_t lists_stride;
+    int32_t list_max;     // sparse-row degree bound and list row stride of this launch (64, or 256 if W > 256)
     uint32_t* heavy_mask; // [W] bitset of H
     uint32_t* light_mask; // [W] bitset of the sparse rows (k_sc2_light's rows)
     uint2* heavy_UP;      // [cap][W] per heavy row a: (U_{H_a} word, exclusive prefix popcount of U_{H_a})

@@ -64,6 +64,9 @@ const int kKernelStage[KID_COUNT] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int words_per_row(int n) { return (int)round_up((n + 31) / 32, 4); }
+// sparse-row list length for rows of W words: the SC^2 kernels' WPL = ceil(W/32) templates above 8 use the
+// long lists (trk::list_max_of)
+inline int list_cap(int64_t W) { return (W + 31) / 32 > 8 ? trk::LIST_MAX_BIG : trk::LIST_MAX; }
 constexpr int HEAVY_CAP_MAX = 2048;
 constexpr int NCHUNK = 4;  // sub-batches of a pipelined host-input call
 
@@ -244,7 +247,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {want_err(c->prm) ? sizeof(double2) * (size_t)(KC * trk::SCORE_SEGS_MAX * B) : 0, &p_herr},
         {sizeof(uint2) * (size_t)(cap * W * B), &p_up},
         {sizeof(int) * 16, &p_ctr},
-        {sizeof(uint16_t) * (size_t)(N * trk::LIST_MAX * B), &p_lists},
+        {sizeof(uint16_t) * (size_t)(N * list_cap(W) * B), &p_lists},
         {sizeof(int32_t) * (size_t)(N * B), &p_ll},
         {sizeof(int32_t) * (size_t)(N * B), &p_dl},
         {sizeof(unsigned long long) * (size_t)(trk::PIV_CAP * B), &p_cand},
@@ -304,7 +307,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     c->d_counters = static_cast<int*>(p_ctr);
     c->d_rowsum = static_cast<int32_t*>(p_rs);
     w.lists = static_cast<uint16_t*>(p_lists);
-    w.lists_stride = N * trk::LIST_MAX;
+    w.lists_stride = N * list_cap(W);
     w.light_list = static_cast<int32_t*>(p_ll);
     w.cand = static_cast<unsigned long long*>(p_cand);
     w.rowptr = static_cast<int32_t*>(p_rp);
@@ -489,6 +492,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         }));
     }
     if (!(phase & PH_TAIL)) return TURBOREG_OK;
+    ws.list_max = list_cap(Wb);
     if (phase & PH_GRAPH) {
     const dim3 grow((maxn_batch + trk::DEG_ROWS_PER_BLOCK - 1) / trk::DEG_ROWS_PER_BLOCK, B);
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));

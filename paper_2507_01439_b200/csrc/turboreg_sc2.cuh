@@ -9,29 +9,27 @@ namespace trk {
 // Eq. 2 for every O2 edge (i < j), written as (j << 16 | Ĝ_ij) to edges[rowptr(i) + rank of j
 // in U_i] (compact, rank-indexed rows).  Three passes write disjoint sets of edges:
 //   * both endpoints heavy → the tensor-core epilogue (k_sc2_mma; k_emit_hh on the cross-check path);
-//   * one endpoint dense (heavy, or degree > LIST_MAX) → k_sc2 below, from the dense row's side;
+//   * one endpoint dense (heavy, or degree > list_max) → k_sc2 below, from the dense row's side;
 //   * both sparse → k_sc2_light.
 // The pivot passes (turboreg_select.cuh) then histogram the positive weights for the radix select (Eq. 4).
 constexpr int SC2_WARPS = 8;
 constexpr int DEG_ROWS_PER_BLOCK = 64;  // k_degree: rows per 8-warp block
 constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 128;
-constexpr int LIST_MAX = 64;  // rows with degree <= LIST_MAX keep a sorted uint16 neighbour list
-constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
-// Row i as a byte map (one byte per column) trades the per-row expansion (~40 instructions per word) for
-// cheaper list lookups; with a few dozen sparse neighbours per dense row it does not pay, so it is off.
-constexpr bool SC2_BYTEMAP = false;
+constexpr int LIST_MAX = 64;       // rows with degree <= list_max keep a sorted uint16 neighbour list: 64, or
+constexpr int LIST_MAX_BIG = 256;  // 256 for rows of more than 256 words (N > 8192, where outliers' degrees grow)
 template <int WPL>
-constexpr int sc2_warp_words() {  // U_i, rank prefix, row i, queue (+ row i as a byte map if enabled)
-    return 96 * WPL + 32 * WPL + ((SC2_BYTEMAP && WPL <= 8) ? 32 * WPL * 32 / 4 : 0);
-}
+constexpr int list_max_of() { return WPL >= 16 ? LIST_MAX_BIG : LIST_MAX; }
+constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
+template <int WPL>
+constexpr int sc2_warp_words() { return 96 * WPL + 32 * WPL; }  // U_i, rank prefix, row i, queue
 template <int WPL>
 constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
 
-// Dense rows (not sparse: heavy, or degree > LIST_MAX), one warp per row i, SC2_BLOCKS_PER_PAIR blocks of
+// Dense rows (not sparse: heavy, or degree > list_max), one warp per row i, SC2_BLOCKS_PER_PAIR blocks of
 // warps striding over the pair's dense rows.  Row i's edges come from three sources:
 //   (1) i, j both heavy: written by the tensor-core epilogue (k_sc2_mma) or k_emit_hh, not here;
-//   (2) j sparse (degree <= LIST_MAX, sorted neighbour list L_j), on EITHER side of i:
+//   (2) j sparse (degree <= list_max, sorted neighbour list L_j), on EITHER side of i:
 //       Ĝ_ij = |L_j ∩ N(i)|, one edge per lane, list entries tested against row i's bitmap in shared
 //       memory.  For j > i the result goes to row i's slot; for j < i to row j's slot, whose rank
 //       (entries of L_j below i, minus those up to j) falls out of the same pass over L_j;
@@ -41,106 +39,87 @@ constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
 constexpr int SC2_BLOCKS_PER_PAIR = 64;  // 512 warps stride over a pair's dense rows
 constexpr int SC2_CLAIM = 4;
 
-// |L ∩ N(i)| for a sorted list L of <= LIST_MAX uint16 entries (16-byte aligned, zero padded) against row
-// i's bitmap in shared memory.  Entries past len are zeros, so a chunk is processed whole and the pad's
-// bit 0 tests are subtracted once (row i's own bit 0 is read once).
+// |L ∩ N(i)| for a sorted list L of <= LM uint16 entries (16-byte aligned, zero padded) against row i's
+// bitmap in shared memory.  Entries past len are zeros, so a chunk is processed whole and the pad's bit 0
+// tests are subtracted once (row i's own bit 0 is read once).  64 entries (8 chunks) are loaded before any
+// is tested.
+template <int LM>
 __device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len, const uint32_t* sr) {
     const int nch = (len + 7) >> 3;
-    uint4 v[LIST_MAX / 8];
-#pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c)
-        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
     uint32_t cnt = 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < nch; c0 += 8) {
+        uint4 v[8];
 #pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c) {
-        if (c < nch) {
-            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+        for (int c = 0; c < 8; ++c)
+            v[c] = (c0 + c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c0 + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t k0 = wv[e] & 0xffffu, k1 = wv[e] >> 16;
-                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+        for (int c = 0; c < 8; ++c) {
+            if (c0 + c < nch) {
+                const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t k0 = wv[e] & 0xffffu, k1 = wv[e] >> 16;
+                    cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+                }
             }
         }
+        if (LM <= 64) break;
     }
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
-
 
 // As list_bitmap_count, for an edge (j, i) with j < i stored in row j: also returns the rank of i among
 // the entries of L_j above j (= #{x in L_j : j < x < i}).
+template <int LM>
 __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, int len, const uint32_t* sr, int i,
                                                            int j, int* rank) {
     const int nch = (len + 7) >> 3;
-    uint4 v[LIST_MAX / 8];
-#pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c)
-        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
     uint32_t cnt = 0;
     int r = 0;
     const unsigned span = (unsigned)(i - j - 1);
+#pragma unroll 1
+    for (int c0 = 0; c0 < nch; c0 += 8) {
+        uint4 v[8];
 #pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c) {
-        if (c < nch) {
-            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+        for (int c = 0; c < 8; ++c)
+            v[c] = (c0 + c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c0 + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
-                cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
-                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
-                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
+        for (int c = 0; c < 8; ++c) {
+            if (c0 + c < nch) {
+                const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                    cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
+                    // j < k < i as one unsigned range test; pads are 0 <= j: never counted
+                    r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
+                }
             }
         }
+        if (LM <= 64) break;
     }
     *rank = r;
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
-// As list_bitmap_count_rank, against row i as a byte map (one byte per column, 0/1) in shared memory:
-// one byte load per list entry instead of word load + shift + mask.
-__device__ __forceinline__ uint32_t list_bytemap_count_rank(const uint16_t* L, int len, const uint8_t* sb, int i, int j,
-                                                            int* rank) {
-    const int nch = (len + 7) >> 3;
-    uint4 v[LIST_MAX / 8];
-#pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c)
-        v[c] = (c < nch) ? __ldg(reinterpret_cast<const uint4*>(L) + c) : make_uint4(0, 0, 0, 0);
-    uint32_t cnt = 0;
-    int r = 0;
-    const unsigned span = (unsigned)(i - j - 1);
-#pragma unroll
-    for (int c = 0; c < LIST_MAX / 8; ++c) {
-        if (c < nch) {
-            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
-                cnt += (uint32_t)sb[k0] + (uint32_t)sb[k1];
-                // j < k < i as one unsigned range test; pads are 0 <= j: never counted
-                r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
-            }
-        }
-    }
-    *rank = r;
-    return cnt - (uint32_t)(nch * 8 - len) * (uint32_t)sb[0];
-}
-
-// Edge between dense row i (bitmap sr — or byte map sb when non-null —, U_i words su, rank prefix sp in
-// shared memory) and sparse row j, on either side of i: one code path for both sides (no divergence).
+// Edge between dense row i (bitmap sr, U_i words su, rank prefix sp in shared memory) and sparse row j, on
+// either side of i: one code path for both sides (no divergence).
+template <int LM>
 __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
                                                 const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
-                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr,
-                                                const uint8_t* sb, int i, int j) {
-    const uint16_t* L = lists + (int64_t)j * LIST_MAX;
+                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr, int i,
+                                                int j) {
+    const uint16_t* L = lists + (int64_t)j * LM;
     int rank;
-    const uint32_t c = sb ? list_bytemap_count_rank(L, deg_full[j], sb, i, j, &rank)
-                          : list_bitmap_count_rank(L, deg_full[j], sr, i, j, &rank);
+    const uint32_t c = list_bitmap_count_rank<LM>(L, deg_full[j], sr, i, j, &rank);
     const int wj = j >> 5;
     uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u)) : edges + rowptr[j] + rank;
     *dst = ((uint32_t)((j > i) ? j : i) << 16) | c;
 }
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
+__global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 : 4)) k_sc2(WS ws, int cpi) {
     constexpr int G = 4;
     constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
@@ -152,7 +131,6 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
     int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
     uint32_t* sr = su + 64 * WPL;
     uint32_t* sq = su + 96 * WPL;
-    uint8_t* sbm = (SC2_BYTEMAP && WPL <= 8) ? reinterpret_cast<uint8_t*>(su + 128 * WPL) : nullptr;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -199,17 +177,6 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
                 const int cnt = __popc(u);
                 const int incl = warp_incl_scan(cnt);
                 sr[w] = reg[k];
-                if (sbm) {  // bits of word w -> bytes 32w .. 32w+31 (two 16-byte stores)
-                    uint32_t b[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const uint32_t nib = (reg[k] >> (4 * q)) & 0xfu;
-                        b[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-                    }
-                    uint4* d = reinterpret_cast<uint4*>(sbm + 32 * w);
-                    d[0] = make_uint4(b[0], b[1], b[2], b[3]);
-                    d[1] = make_uint4(b[4], b[5], b[6], b[7]);
-                }
                 su[w] = u;
                 sp[w] = carry + incl - cnt;
                 carry += __shfl_sync(FULL, incl, 31);
@@ -239,7 +206,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
                 nq += __popc(sb);
                 if (nq > QCAP - 32) {
                     __syncwarp();
-                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
+                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
                     __syncwarp();
                     nq = 0;
                 }
@@ -282,7 +249,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, 4) k_sc2(WS ws, int cpi) {
             }
         }
         __syncwarp();
-        for (int t = lane; t < nq; t += 32) sc2_sparse_edge(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, sbm, i, (int)sq[t]);
+        for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
         __syncwarp();
     }
 }
@@ -320,7 +287,7 @@ __global__ void __launch_bounds__(1024) k_rowclass(WS ws) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int i = ib + k;
-            fl[k] = (i < n && hpos[i] < 0 && deg[i] <= LIST_MAX) ? 1 : 0;
+            fl[k] = (i < n && hpos[i] < 0 && deg[i] <= ws.list_max) ? 1 : 0;
             ud[k] = i < n ? udeg[i] : 0;
             fs += fl[k];
             us += ud[k];
@@ -393,7 +360,7 @@ template <int WPL>
 constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
 template <int WPL, int LG = light_rows<WPL>()>
 constexpr int light_warp_words() {
-    return LG * 32 * WPL + LG * (LIST_MAX / 2) + 64 + 64 + 4 * LG;
+    return LG * 32 * WPL + LG * (list_max_of<WPL>() / 2) + 64 + 64 + 4 * LG;
 }
 template <int WPL, int LG = light_rows<WPL>()>
 constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL, LG>() * 4; }
@@ -405,10 +372,11 @@ __device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t*
     const uint16_t* lists = ws.lists + p * ws.lists_stride;
     const int32_t* deg_full = ws.deg_full + p * ws.row_stride;
     if (lane < cnt) {
+        constexpr int LM = list_max_of<WPL>();
         const uint32_t e = q[lane];
-        const int j = (int)(e & 0xffffu), t = (int)((e >> 16) & 63), r = (int)(e >> 22);
+        const int j = (int)(e & 0xffffu), t = (int)((e >> 16) & 255), r = (int)(e >> 24);
         const int i = meta[4 * r], lo = meta[4 * r + 2];
-        const uint32_t c = list_bitmap_count(lists + (int64_t)j * LIST_MAX, deg_full[j], bm + r * 32 * WPL);
+        const uint32_t c = list_bitmap_count<LM>(lists + (int64_t)j * LM, deg_full[j], bm + r * 32 * WPL);
         ws.edges[p * ws.edges_stride + ws.rowptr[p * ws.rp_stride + i] + (t - lo)] = ((uint32_t)j << 16) | c;
     }
 }
@@ -430,9 +398,10 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     if (gi >= gr_hi) return;
     const int g0 = gi * LG;
     const int nr = min(LG, nl - g0);
+    constexpr int LM = list_max_of<WPL>();
     uint32_t* bm = s_dyn + warp * light_warp_words<WPL, LG>();
     uint16_t* ls = reinterpret_cast<uint16_t*>(bm + LG * 32 * WPL);
-    uint32_t* qL = bm + LG * 32 * WPL + LG * (LIST_MAX / 2);
+    uint32_t* qL = bm + LG * 32 * WPL + LG * (LM / 2);
     uint32_t* qD = qL + 64;
     int32_t* meta = reinterpret_cast<int32_t*>(qD + 64);
     const uint32_t* bits = ws.bits + p * ws.bits_stride;
@@ -455,10 +424,10 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
         const int r = idx / W4, c = idx - r * W4;
         cp_async16(bm + r * 32 * WPL + 4 * c, bits + (int64_t)meta[4 * r] * W + 4 * c);
     }
-    for (int idx = lane; idx < nr * (LIST_MAX / 8); idx += 32) {
-        const int r = idx / (LIST_MAX / 8), c = idx - r * (LIST_MAX / 8);
-        uint16_t* dst = ls + r * LIST_MAX + 8 * c;
-        if (c * 8 < meta[4 * r + 1]) cp_async16(dst, lists + (int64_t)meta[4 * r] * LIST_MAX + 8 * c);
+    for (int idx = lane; idx < nr * (LM / 8); idx += 32) {
+        const int r = idx / (LM / 8), c = idx - r * (LM / 8);
+        uint16_t* dst = ls + r * LM + 8 * c;
+        if (c * 8 < meta[4 * r + 1]) cp_async16(dst, lists + (int64_t)meta[4 * r] * LM + 8 * c);
         else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -487,8 +456,8 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
             const int lo = meta[4 * r + 2];
             const int pr = meta[4 * r + 3];
             const int t = lo + (e - pr);
-            const int j = ls[r * LIST_MAX + t];
-            packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 22);
+            const int j = ls[r * LM + t];
+            packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 24);
             isL = (__ldg(lmask + (j >> 5)) >> (j & 31)) & 1u;  // sparse j; dense j is k_sc2's edge
         }
         const unsigned bL = __ballot_sync(FULL, isL);
@@ -564,10 +533,10 @@ __global__ void __launch_bounds__(256) k_hist_hi(WS ws) {
 
 // ------------------------------------------------------------------------------------------ a3 heavy split
 // Full degrees (popcount of each bit row), their sum and maximum, and the sorted uint16 neighbour list of
-// every row with degree <= LIST_MAX (zero-padded to a 16-byte chunk); one warp per row.
+// every row with degree <= list_max (zero-padded to a 16-byte chunk); one warp per row.
 // Degrees and the sorted lists of sparse rows.  Lane l owns 8 consecutive words [g + 8l, g + 8l + 8) of a
 // 256-word group (two 16-byte loads), so lane order is column order and one warp scan of the per-lane
-// counts places every lane's entries; only rows with degree <= LIST_MAX extract their set bits.
+// counts places every lane's entries; only rows with degree <= list_max extract their set bits.
 __device__ __forceinline__ void deg_load8(const uint32_t* ri, int w0, int W, uint32_t (&v)[8]) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -602,8 +571,8 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
     const int row0 = blockIdx.x * DEG_ROWS_PER_BLOCK, row1 = min(row0 + DEG_ROWS_PER_BLOCK, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
     auto finish_row = [&](int i, int deg, int ucnt) {  // ucnt: the row's total |U_i|
-        uint16_t* L = lists + (int64_t)i * LIST_MAX;
-        if (deg <= LIST_MAX)
+        uint16_t* L = lists + (int64_t)i * ws.list_max;
+        if (deg <= ws.list_max)
             for (int t = deg + lane; t < ((deg + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
         if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = deg; ws.deg[p * ws.row_stride + i] = ucnt; }
         mine += deg;
@@ -639,8 +608,8 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
                     for (int k = 0; k < WPL; ++k) below += (k < k0) ? __popc(v[k]) : (k == k0 ? __popc(v[k] & mb) : 0);
                 }
                 const int ucnt = deg - __shfl_sync(FULL, below, li);
-                if (deg <= LIST_MAX) {
-                    uint16_t* L = lists + (int64_t)i * LIST_MAX;
+                if (deg <= ws.list_max) {
+                    uint16_t* L = lists + (int64_t)i * ws.list_max;
                     int pos = incl - cnt;
 #pragma unroll
                     for (int k = 0; k < WPL; ++k) {
@@ -712,7 +681,7 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
                     carry += __shfl_sync(FULL, incl, 31);
                 }
             }
-            if (deg <= LIST_MAX) {
+            if (deg <= ws.list_max) {
                 int carry = 0;
                 for (int g = 0; g < W; g += 256) {
                     uint32_t v[8];
@@ -722,7 +691,7 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) cnt += __popc(v[k]);
                     const int incl = warp_incl_scan(cnt);
-                    deg_extract8(v, w0, carry + incl - cnt, lists + (int64_t)i * LIST_MAX);
+                    deg_extract8(v, w0, carry + incl - cnt, lists + (int64_t)i * ws.list_max);
                     carry += __shfl_sync(FULL, incl, 31);
                 }
             }
@@ -779,11 +748,11 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
         thr = hi;
         cnt = count_ge(thr);
     }
-    // widen H to every non-sparse row (degree > LIST_MAX) when that costs no extra 256-row block of the
+    // widen H to every non-sparse row (degree > list_max) when that costs no extra 256-row block of the
     // tensor-core contraction: those rows' dense-dense edges then come from the tensor cores instead of the
     // latency-bound popcount path
     {
-        const int thr2 = max(ws.heavy_min_deg, LIST_MAX + 1);
+        const int thr2 = max(ws.heavy_min_deg, ws.list_max + 1);
         if (thr2 < thr) {
             const int cnt2 = count_ge(thr2);
             if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
