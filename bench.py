@@ -476,6 +476,7 @@ def run_cuda(args, rank, world, local_rank):
         all_ok = int((res["status"] == 0).sum())
 
     context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 and not args.no_context else None
+    split_ctx = split_pair_context(world, local_rank) if world > 1 and not args.no_context else None
     if rank != 0:
         return
     pk = peaks()
@@ -509,6 +510,8 @@ def run_cuda(args, rank, world, local_rank):
         "wall_s_timed_region": wall,
     }
     line.update(context or {})
+    if split_ctx:
+        line["split_pair_latency_ms"] = split_ctx
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
     print(json.dumps(line), flush=True)
@@ -608,6 +611,38 @@ def single_pair_context(rank, local_rank, stream, src_d, dst_d):
                          "ms_per_pair_host_io": round(1e3 * float(np.median(t_r)), 3)}}
     return {"single_pair_latency_ms_configs": lat_cfg, "single_pair_latency_ms_large_n": lat_big,
             "ransac_equal_budget": ransac}
+
+
+def split_pair_context(world, local_rank, n=32768, reps=3):
+    """NEXT(1) context (not the metric): one 3DMatch-shaped pair of N = 32768 split over all ranks
+    (split.register_split: NCCL all-reduce of C's words and of the edge words, all-gather of the records),
+    wall time of the whole call with a barrier on both sides, max over ranks, median of `reps`."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_01439_b200 import TurboReg
+    from paper_2507_01439_b200.split import register_split
+
+    c = synth.CONFIGS["B"]
+    inst = synth.workload_instance(c, pair=0, n=n)
+    dev = torch.device("cuda", local_rank)
+    src, dst = torch.from_numpy(inst["src"]).to(dev), torch.from_numpy(inst["dst"]).to(dev)
+    tr = TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=n, max_batch=1, device=local_rank, max_density=0.1)
+    ts = []
+    res = None
+    for k in range(reps + 1):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        res = register_split(tr, src, dst)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if k:
+            ts.append(_max_over_ranks(time.perf_counter() - t0, world, dev))
+    tr.close()
+    return {"N": n, "ranks": world, "ms": round(1e3 * float(np.median(ts)), 3), "status": int(res["status"]),
+            "inlier_count": int(res["inlier_count"]),
+            "recovered": bool(synth.rotation_error_deg(np.asarray(res["R"]).reshape(3, 3), inst["R"]) <= 5)}
 
 
 def ncu_traffic(kernel):

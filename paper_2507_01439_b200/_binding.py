@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libturboreg.so")
+# TURBOREG_LIBRARY selects another in-tree build (the tests' checked build, lib/libturboreg_checked.so)
+_LIB_PATH = os.environ.get("TURBOREG_LIBRARY") or os.path.join(_HERE, "lib", "libturboreg.so")
 
 
 class TurboRegError(RuntimeError):

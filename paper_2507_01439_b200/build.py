@@ -10,6 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libturboreg.so")
+LIB_CHECKED = os.path.join(LIBDIR, "libturboreg_checked.so")  # TRK_CHECKS: device-side invariant checks (tests)
 SOURCES = [os.path.join(CSRC, "turboreg_runtime.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")] + [
     os.path.join(ROOT, "include", "turboreg.h")]
@@ -29,26 +30,28 @@ def nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
-    if not force and os.path.exists(LIB):
-        mt = os.path.getmtime(LIB)
+    lib = LIB_CHECKED if checked else LIB
+    if not force and os.path.exists(lib):
+        mt = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= mt for d in DEPS):
-            return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
+            return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DTRK_CHECKS"] if checked else []), "-I", os.path.join(ROOT, "include"), "-o",
+           tmp, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed ({r.returncode}) building {LIB}")
+        raise RuntimeError(f"nvcc failed ({r.returncode}) building {lib}")
     if verbose:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -13,6 +13,7 @@ namespace trk {
 // per-lane register lists (K2 <= KL) merged by K2 warp argmax rounds, or K2 threshold rounds otherwise.
 constexpr int PGS_WARPS = 8;
 constexpr int PGS_KL = 8;
+constexpr int PGS_GATHER = 4;  // candidates whose two weight gathers are issued together
 
 template <typename F>
 __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
@@ -30,17 +31,28 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
         carry_i += __shfl_sync(FULL, si, 31);
         carry_j += __shfl_sync(FULL, sj, 31);
         uint32_t m = ui & uj;
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1u;
-            const uint32_t below = (1u << b) - 1u;
-            const int rk_i = exi + __popc(ui & below);
-            const int rk_j = exj + __popc(uj & below);
-            const int wiz = (int)(__ldg(ei + rk_i) & 0xffffu);
-            const int wjz = (int)(__ldg(ej + rk_j) & 0xffffu);
-            const int z = w * 32 + b;
-            const int S = wij + wiz + wjz;
-            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+        while (m) {  // up to PGS_GATHER candidates at a time: all their weight gathers in flight together
+            int zb[PGS_GATHER];
+            uint32_t gi[PGS_GATHER], gj[PGS_GATHER];
+#pragma unroll
+            for (int u = 0; u < PGS_GATHER; ++u) {
+                zb[u] = -1;
+                if (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1u;
+                    const uint32_t below = (1u << b) - 1u;
+                    zb[u] = b;
+                    gi[u] = __ldg(ei + exi + __popc(ui & below));
+                    gj[u] = __ldg(ej + exj + __popc(uj & below));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PGS_GATHER; ++u) {
+                if (zb[u] < 0) break;
+                const int z = w * 32 + zb[u];
+                const int S = wij + (int)(gi[u] & 0xffffu) + (int)(gj[u] & 0xffffu);
+                f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+            }
         }
     }
 }
@@ -132,7 +144,7 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
 // KL: per-lane top list length (2, 4, PGS_KL; 0 = K2 threshold rounds), fixed per launch so each
 // instantiation only holds the registers its own branch needs (occupancy: the kernel is latency-bound).
 template <int MODE, int KL>
-__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws) {
+__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 5 : 4)) k_pgs(WS ws) {
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
     const int n = d.n;

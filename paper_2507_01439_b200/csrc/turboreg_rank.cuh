@@ -157,4 +157,84 @@ __global__ void k_split_merge(const DevResult* parts, int world, DevResult* out)
     *out = o;
 }
 
+// ------------------------------------------------------------------------------------------ checked build
+// TRK_CHECKS (libturboreg_checked.so, tests only; compute-sanitizer is closed on the GPU pool): structural
+// invariants of the assembled graph and of the TurboCliques, verified on the device after each stage;
+// any violation traps, so the call fails with a CUDA error.
+#ifdef TRK_CHECKS
+__device__ __forceinline__ void trk_fail(const char* what, int p, int a, int b, int c) {
+    printf("TRK_CHECKS: %s (pair %d: %d %d %d)\n", what, p, a, b, c);
+    __trap();
+}
+__device__ __forceinline__ bool bit_of(const uint32_t* row, int j) { return (row[j >> 5] >> (j & 31)) & 1u; }
+// Every O2 edge slot written exactly once with the right neighbour and weight: row i's words are the
+// increasing j > i with C_ij = 1, and Ĝ_ij = popcount(row_i AND row_j) (Eq. 2).  One warp per row.
+__global__ void k_check_edges(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n, W = d.W;
+    if (n == 0 || ws.st[p].edge_overflow) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int32_t* rp = ws.rowptr + p * ws.rp_stride;
+    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += gridDim.x * 8) {
+        const uint32_t* ri = bits + (int64_t)i * W;
+        int prev = i;
+        for (int e = rp[i]; e < rp[i + 1]; ++e) {
+            const uint32_t v = edges[e];
+            const int j = (int)(v >> 16), w = (int)(v & 0xffffu);
+            if (lane == 0 && (j <= prev || j >= n || !bit_of(ri, j))) trk_fail("edge neighbour", p, i, e, j);
+            uint32_t c = 0;
+            const uint32_t* rj = bits + (int64_t)j * W;
+            for (int k = lane; k < W; k += 32) c += __popc(ri[k] & rj[k]);
+            c = __reduce_add_sync(0xffffffffu, c);
+            if (lane == 0 && (int)c != w) trk_fail("edge weight", p, i, j, w);
+            prev = j;
+        }
+        // the count of upper neighbours equals the row's slot count
+        int u = 0;
+        for (int k = lane; k < W; k += 32) u += __popc(upper_mask(ri[k], k, i));
+        u = (int)__reduce_add_sync(0xffffffffu, (unsigned)u);
+        if (lane == 0 && u != rp[i + 1] - rp[i]) trk_fail("row slot count", p, i, u, rp[i + 1] - rp[i]);
+    }
+}
+// Every emitted TurboClique is a 3-clique of C with i < j < z, its pivot's pair, and S = the sum of its three
+// O2 weights (Eq. 6); pivots are positive O2 edges.
+__global__ void k_check_cliques(WS ws) {
+    const int p = blockIdx.y;
+    const PairDesc d = ws.desc[p];
+    const int n = d.n, W = d.W;
+    if (n == 0) return;
+    const uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const uint32_t* edges = ws.edges + p * ws.edges_stride;
+    const int32_t* rp = ws.rowptr + p * ws.rp_stride;
+    auto weight = [&](int a, int b) -> int {  // a < b: binary search of row a's slots
+        int lo = rp[a], hi = rp[a + 1] - 1;
+        while (lo <= hi) {
+            const int m = (lo + hi) >> 1;
+            const int j = (int)(edges[m] >> 16);
+            if (j == b) return (int)(edges[m] & 0xffffu);
+            if (j < b) lo = m + 1; else hi = m - 1;
+        }
+        return -1;
+    };
+    const int K = ws.k1 * ws.k2;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < K; s += gridDim.x * blockDim.x) {
+        const int4 c = ws.cliq[p * ws.cl_stride + s];
+        if (c.x < 0) continue;
+        if (!(c.x < c.y && c.y < c.z && c.z < n)) trk_fail("clique order", p, c.x, c.y, c.z);
+        const uint32_t* ri = bits + (int64_t)c.x * W;
+        const uint32_t* rj = bits + (int64_t)c.y * W;
+        if (!bit_of(ri, c.y) || !bit_of(ri, c.z) || !bit_of(rj, c.z)) trk_fail("clique not a 3-clique", p, c.x, c.y, c.z);
+        if (weight(c.x, c.y) + weight(c.x, c.z) + weight(c.y, c.z) != c.w) trk_fail("clique weight", p, c.x, c.y, c.w);
+    }
+    if (blockIdx.x == 0)
+        for (int k = threadIdx.x; k < ws.st[p].npiv; k += blockDim.x) {
+            const int4 v = ws.piv[p * ws.piv_stride + k];
+            if (!(v.x < v.y) || v.z <= 0 || weight(v.x, v.y) != v.z) trk_fail("pivot", p, v.x, v.y, v.z);
+        }
+}
+#endif
+
 }  // namespace trk

@@ -498,7 +498,12 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_ROWCLASS, [&] { trk::k_rowclass<<<B, 1024, 0, s>>>(ws); }));
-    if (splitp) CK(L.run(KID_ZERO_EDGES, [&] { trk::k_zero_edges<<<dim3(2 * c->num_sms, B), 256, 0, s>>>(ws); }));
+#ifdef TRK_CHECKS
+    const bool zero_edges = true;  // the checked build verifies every slot was written
+#else
+    const bool zero_edges = splitp;
+#endif
+    if (zero_edges) CK(L.run(KID_ZERO_EDGES, [&] { trk::k_zero_edges<<<dim3(2 * c->num_sms, B), 256, 0, s>>>(ws); }));
     if (ws.sc2_path != 1) {
         CK(L.run(KID_EXPAND, [&] {
             const dim3 ge((unsigned)(ws.heavy_X_stride / ws.heavy_Kcap / 8), B);
@@ -576,8 +581,20 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             trk::k_rowsum<<<dim3((unsigned)((maxn_batch + 63) / 64), B), 256, 0, s>>>(ws, rs, c->max_n);
         }));
     }
+#ifdef TRK_CHECKS
+    if (!splitp) {
+        trk::k_check_edges<<<dim3((maxn_batch + 7) / 8, B), 256, 0, s>>>(ws);
+        CK(cudaGetLastError());
+    }
+#endif
     }  // PH_GRAPH
     if (!(phase & PH_SEARCH)) return TURBOREG_OK;
+#ifdef TRK_CHECKS
+    if (splitp) {  // a split pair's edges are complete only after the exchange
+        trk::k_check_edges<<<dim3((maxn_batch + 7) / 8, B), 256, 0, s>>>(ws);
+        CK(cudaGetLastError());
+    }
+#endif
     const dim3 gsel((maxn_batch + trk::SEL_ROWS_PER_BLOCK - 1) / trk::SEL_ROWS_PER_BLOCK, B);
     const int sel_bpp = std::max(trk::SEL_BLOCKS_PER_PAIR, std::min((4 * c->num_sms + batch - 1) / batch, 256));
     const dim3 gflat((unsigned)sel_bpp, B);
@@ -606,6 +623,12 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             else trk::k_pgs<0, 0><<<g, bt, 0, s>>>(ws);
         }
     }));
+#ifdef TRK_CHECKS
+    if (mode != RUN_RANSAC) {
+        trk::k_check_cliques<<<dim3(8, B), 256, 0, s>>>(ws);
+        CK(cudaGetLastError());
+    }
+#endif
     if (c->prm.graph_mode == 1) {  // canonical order + de-duplication of the SC^2-mode clique list (r9)
         int m2 = 1;
         while (m2 < c->prm.k1 * c->prm.k2) m2 <<= 1;
