@@ -375,7 +375,10 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
                      : "memory");
     };
     if (threadIdx.x == 0) issue(0);
-    const uint32_t thr1b = __float_as_uint(__fmul_rn(ws.thr, ws.thr)) + 1u;
+    // thr2 = RN(thr·thr) (reading r13); thrn = the next float above it: s <= thr2 ⇔ s < thrn ⇔ the sign bit of
+    // fl(s − thrn) (a difference of two floats is 0 only when they are equal, so the sign is exact)
+    const float thrn = __uint_as_float(__float_as_uint(__fmul_rn(ws.thr, ws.thr)) + 1u);
+    const f2_t thrn2 = f2_pack(thrn, thrn);
     f2_t Rp[NP][9], tp[NP][3];
 #pragma unroll
     for (int m = 0; m < NP; ++m) {
@@ -420,11 +423,12 @@ __global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS w
                 const f2_t e1 = f2_fma(f2_pack(y.y, y.y), mone, p1);
                 const f2_t e2 = f2_fma(f2_pack(y.z, y.z), mone, p2);
                 const f2_t sq = f2_fma(e2, e2, f2_fma(e1, e1, f2_mul(e0, e0)));
-                // s >= 0 (or +inf), so integer order of the bit patterns is float order: s <= thr2 ⇔ the
-                // 31-bit difference s − (thr2 + 1) is negative; its sign bit is added (IADD3 + LEA.HI, no
-                // predicate)
-                cnt[2 * m] += (f2_lo(sq) - thr1b) >> 31;
-                cnt[2 * m + 1] += (f2_hi(sq) - thr1b) >> 31;
+                // inlier ⇔ s − thrn < 0: one packed subtract for both hypotheses, then the sign bits are added
+                // (LEA.HI) — integer ALU instructions take FP32-pipe issue slots on this part, FADD2 halves them
+                const f2_t dd = f2_sub(sq, thrn2);
+                asm("{ .reg .b32 lo, hi; mov.b64 {lo, hi}, %2; shr.u32 lo, lo, 31; shr.u32 hi, hi, 31; "
+                    "add.u32 %0, %0, lo; add.u32 %1, %1, hi; }"  // one LEA.HI per hypothesis
+                    : "+r"(cnt[2 * m]), "+r"(cnt[2 * m + 1]) : "l"(dd));
                 if constexpr (ERR) {
                     const float s0 = __uint_as_float(f2_lo(sq)), s1 = __uint_as_float(f2_hi(sq));
                     ea[2 * m] += (double)__fsqrt_rn(s0);

@@ -61,3 +61,25 @@ def test_rank_by_error_selects_oracle_winner(TR, metric, key, n, graph_mode):
     got = _errors_by_clique(tr, 0)[tuple(res["clique"])]
     want = ref["mae"] if metric == "mae" else ref["mse"]
     assert abs(got[0 if metric == "mae" else 1] - want) <= 1e-12 * want
+
+
+@pytest.mark.parametrize("key", ["B", "D"])
+def test_hypothesis_errors_baseline_size(TR, key):
+    """MAE / MSE of every hypothesis at N = 5000 (the BASELINE size) within 1e-12 relative of the oracle's
+    sequential float64 sums, and both error rankings select the oracle's winner."""
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=19)
+    ref = oracle.estimate(inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, trace=True)
+    tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=cfg.n, hyp_errors=True)
+    res = tr.register(inst["src"], inst["dst"])
+    assert res["status"] == ref["status"] == 0 and tuple(res["clique"]) == tuple(ref["clique"])
+    got = _errors_by_clique(tr, 0)
+    ok = ref["hyp_degenerate"] == 0
+    for c, mae, mse in zip(ref["cliques"][ok], ref["hyp_mae"][ok], ref["hyp_mse"][ok]):
+        g = got[tuple(c[:3])]
+        assert abs(g[0] - mae) <= 1e-12 * mae and abs(g[1] - mse) <= 1e-12 * mse
+    for metric, rm in (("mae", 1), ("mse", 2)):
+        t2 = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=cfg.n, rank_metric=metric)
+        r2 = t2.register(inst["src"], inst["dst"])
+        ref2 = oracle.estimate(inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, rank_metric=rm)
+        assert tuple(r2["clique"]) == tuple(ref2["clique"]) and r2["inlier_count"] == ref2["inlier_count"]

@@ -64,3 +64,15 @@ def test_sc2_mode_full_budget_every_triangle_once(TR, density):
 def test_sc2_mode_budget_limit_rejected(TR):
     with pytest.raises(Exception):
         TR(0.01, 10000, 2, 0.1, graph_mode=1, max_n=100)
+
+
+@pytest.mark.parametrize("key", ["B", "C", "D"])
+def test_sc2_mode_parity_baseline_size(TR, key):
+    """graph_mode = 1 at the BASELINE size (N = 5000, the config's own K1, K2): every intermediate and the
+    winner against the oracle (SC^2 mode had been parity-tested only up to N = 2000)."""
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=17)
+    tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, graph_mode=1, max_n=cfg.n)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res,
+                 graph_mode=1)
