@@ -13,11 +13,16 @@ namespace trk {
 // per-lane register lists (K2 <= KL) merged by K2 warp argmax rounds, or K2 threshold rounds otherwise.
 constexpr int PGS_WARPS = 8;
 constexpr int PGS_KL = 8;
-constexpr int PGS_GATHER = 4;  // candidates whose two weight gathers are issued together
+constexpr int PGS_QCAP = 128;  // per-warp candidate queue (entries) of the O2 scan
 
+// Candidates of a 32-word chunk are flattened across the warp before their weights are gathered: every lane
+// writes its own candidates (z, rank in U_i, rank in U_j) to the warp's shared-memory queue at its prefix
+// offset, then the lanes take the queue entries round-robin, so the gathers and the top-K2 insertions run
+// on all 32 lanes whatever the distribution of candidates over the words (a chunk with more than PGS_QCAP
+// candidates falls back to each lane walking its own word).
 template <typename F>
 __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
-                                                    const uint32_t* ei, const uint32_t* ej, int wij, F&& f) {
+                                                    const uint32_t* ei, const uint32_t* ej, int wij, uint2* sq, F&& f) {
     const int lane = threadIdx.x & 31;
     int carry_i = 0, carry_j = 0;
     const int nchunks = (W + 31) >> 5;
@@ -31,27 +36,43 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
         carry_i += __shfl_sync(FULL, si, 31);
         carry_j += __shfl_sync(FULL, sj, 31);
         uint32_t m = ui & uj;
-        while (m) {  // up to PGS_GATHER candidates at a time: all their weight gathers in flight together
-            int zb[PGS_GATHER];
-            uint32_t gi[PGS_GATHER], gj[PGS_GATHER];
-#pragma unroll
-            for (int u = 0; u < PGS_GATHER; ++u) {
-                zb[u] = -1;
-                if (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1u;
-                    const uint32_t below = (1u << b) - 1u;
-                    zb[u] = b;
-                    gi[u] = __ldg(ei + exi + __popc(ui & below));
-                    gj[u] = __ldg(ej + exj + __popc(uj & below));
+        const int cm = __popc(m);
+        const int incl = warp_incl_scan(cm);
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) continue;
+        if (total <= PGS_QCAP) {
+            int o = incl - cm;
+            while (m) {  // this lane's candidates into the queue
+                const int b = __ffs(m) - 1;
+                m &= m - 1u;
+                const uint32_t below = (1u << b) - 1u;
+                const uint32_t rk_i = (uint32_t)(exi + __popc(ui & below)), rk_j = (uint32_t)(exj + __popc(uj & below));
+                sq[o++] = make_uint2((uint32_t)(w * 32 + b) | (rk_i << 16), rk_j);
+            }
+            __syncwarp();
+            for (int k = lane; k < total; k += 64) {  // two queue entries per lane in flight
+                const uint2 e0 = sq[k];
+                const bool two = k + 32 < total;
+                const uint2 e1 = two ? sq[k + 32] : e0;
+                const uint32_t a0 = __ldg(ei + (e0.x >> 16)), b0 = __ldg(ej + e0.y);
+                const uint32_t a1 = __ldg(ei + (e1.x >> 16)), b1 = __ldg(ej + e1.y);
+                const int S0 = wij + (int)(a0 & 0xffffu) + (int)(b0 & 0xffffu);
+                f(((unsigned long long)(unsigned)S0 << 32) | (unsigned long long)(0xffffffffu - (e0.x & 0xffffu)));
+                if (two) {
+                    const int S1 = wij + (int)(a1 & 0xffffu) + (int)(b1 & 0xffffu);
+                    f(((unsigned long long)(unsigned)S1 << 32) | (unsigned long long)(0xffffffffu - (e1.x & 0xffffu)));
                 }
             }
-#pragma unroll
-            for (int u = 0; u < PGS_GATHER; ++u) {
-                if (zb[u] < 0) break;
-                const int z = w * 32 + zb[u];
-                const int S = wij + (int)(gi[u] & 0xffffu) + (int)(gj[u] & 0xffffu);
-                f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+            __syncwarp();
+        } else {
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1u;
+                const uint32_t below = (1u << b) - 1u;
+                const int wiz = (int)(__ldg(ei + exi + __popc(ui & below)) & 0xffffu);
+                const int wjz = (int)(__ldg(ej + exj + __popc(uj & below)) & 0xffffu);
+                const int z = w * 32 + b;
+                f(((unsigned long long)(unsigned)(wij + wiz + wjz) << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
             }
         }
     }
@@ -106,7 +127,8 @@ __device__ __forceinline__ int4 sorted_clique(int i, int j, int z, int S) {
 // Per-lane sorted top-KL lists (KL >= K2) merged by K2 warp argmax rounds.
 template <int KL, int MODE>
 __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t* ri, const uint32_t* rj, int W, int i,
-                                             int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out) {
+                                             int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out,
+                                             uint2* sq) {
     const int lane = threadIdx.x & 31;
     unsigned long long top[KL];
 #pragma unroll
@@ -121,7 +143,7 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
         }
     };
     if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, insert);
-    else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, insert);
+    else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, sq, insert);
     int emitted = 0;
     for (int r = 0; r < K2; ++r) {
         const unsigned long long head = top[0];
@@ -144,7 +166,8 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
 // KL: per-lane top list length (2, 4, PGS_KL; 0 = K2 threshold rounds), fixed per launch so each
 // instantiation only holds the registers its own branch needs (occupancy: the kernel is latency-bound).
 template <int MODE, int KL>
-__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 5 : 4)) k_pgs(WS ws) {
+__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws) {
+    __shared__ uint2 s_q[PGS_WARPS][PGS_QCAP];
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];
     const int n = d.n;
@@ -171,9 +194,10 @@ __global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 5 : 4)) k_pgs(WS ws
     const uint32_t* edges = ws.edges + q * ws.edges_stride;
     const uint32_t* ei = edges + ws.rowptr[q * ws.rp_stride + i];
     const uint32_t* ej = edges + ws.rowptr[q * ws.rp_stride + j];
+    uint2* sq = s_q[warp];
     int emitted = 0;
     if constexpr (KL > 0) {
-        emitted = pgs_topk_list<KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out);
+        emitted = pgs_topk_list<KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out, sq);
     } else {
         unsigned long long thr = ~0ull;
         for (int r = 0; r < K2; ++r) {
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 5 : 4)) k_pgs(WS ws
                 if (key < thr && key > mine) mine = key;
             };
             if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
-            else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, take);
+            else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, sq, take);
             const unsigned long long best = warp_max_u64(mine);
             if (best == 0ull) break;
             if (lane == 0) {

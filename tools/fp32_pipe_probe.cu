@@ -43,7 +43,7 @@ __global__ void k(float* out, int iters, float s) {
             if (MODE == 1) v[i] = ffma2(v[i], m, v[(i + 1) & 7]);
             if (MODE == 2) { if (i & 1) f[i] = fmaf(f[i], s, f[(i + 1) & 7]); else v[i] = ffma2(v[i], m, v[(i + 1) & 7]); }
             if (MODE == 3) v[i] = ffma2(v[i], m, a);
-            if (MODE == 4) {  // one operand a scalar broadcast (.F32), as in the compat/score loops
+            if (MODE == 4) {  // an operand pair re-packed from a scalar in the loop (ptxas emits IMAD/MOV)
                 const u64 bs = ((u64)__float_as_uint(f[i]) << 32) | __float_as_uint(f[i]);
                 v[i] = ffma2(v[i], bs, v[(i + 1) & 7]);
             }
@@ -80,7 +80,7 @@ int main() {
     const int iters = 20000;
     const int NM = 10;
     const char* names[NM] = {"FFMA scalar (3-reg)", "FFMA2 (3-reg pairs)", "mix FFMA2 + FFMA", "FFMA2 (const pair)",
-                             "FFMA2 (scalar bcast)", "FADD2 (pairs)", "FMUL2 (pairs)", "FFMA2 + LOP3/SHF 5:2",
+                             "FFMA2 (pair re-packed)", "FADD2 (pairs)", "FMUL2 (pairs)", "FFMA2 + LOP3/SHF 5:2",
                              "FFMA2 + SHF 1:1", "FFMA2 2 chains/thread"};
     const double lanes_per_inst[NM] = {1, 2, 1.5, 2, 2, 2, 2, 2, 2, 2};
     for (int mode = 0; mode < NM; ++mode) {
