@@ -170,51 +170,100 @@ def make_inputs(first, pairs, n=None):
 
 def algorithmic_work(tr, res, pairs):
     """Algorithmic work of the last call, summed over its pairs: compat pair tests, the
-    dense tensor-core block's operations, scoring residual tests, O2 edges."""
+    dense tensor-core block's operations, scoring residual tests, O2 edges, bytes of the memory passes."""
     from paper_2507_01439_b200._binding import I_STATE
 
-    tests = mma_ops = edges = 0
+    tests = mma_ops = edges = deg_bytes = expand_bytes = 0
     for p in range(pairs):
         st = tr.intermediate(p, I_STATE)
         n, W, h = st["n"], st["W"], st["heavy_h"]
         tests += n * (n - 1) // 2
         edges += st["edges"]
+        deg_bytes += 4 * n * W + 8 * n  # every bit row read, degree + upper degree written
         if h:  # upper 128 x TN tiles (k_sc2_mma: cb >= rb*128 // TN), K = 32W
             tn = 240 if MMA_FP4 else 256
             cbs = -(-h // tn)
             tiles = sum(cbs - rb * 128 // tn for rb in range(-(-h // 128)))
             mma_ops += tiles * 2 * 128 * tn * 32 * W
+            hp = max(-(-h // 256) * 256, -(-h // 240) * 240 + 16)
+            expand_bytes += hp * 16 * W + h * (4 * W + 8 * W)  # X rows (e2m1) written, rows read, UP written
     score_tests = int(sum(int(r["hypotheses_evaluated"]) for r in res)) * CFG.n
-    return {"compat_tests": tests, "mma_ops": mma_ops, "score_tests": score_tests, "edges": edges}
+    return {"compat_tests": tests, "mma_ops": mma_ops, "score_tests": score_tests, "edges": edges,
+            "degree_bytes": deg_bytes, "expand_bytes": expand_bytes}
+
+
+# instructions per 64 tests (one warp instruction = 32 lanes x 2 packed tests) that occupy the FP32 pipe:
+# packed FP (FFMA2/FADD2/FMUL2) and 32-bit integer ALU ops, which tools/fp32_pipe_probe.cu shows cost the
+# same pipe time as an FFMA2 on this part (DESIGN.md §6); each takes 2 cycles of a sub-partition's pipe
+ISSUE_MIX = {"k_compat": (19, 8), "k_score": (16, 2)}
 
 
 def rooflines(kern, work, steps, pk, pairs):
-    """Per-kernel roofline entries (achieved algorithmic rate ÷ peak) from CUDA-event kernel times."""
+    """Per-kernel roofline entries (achieved algorithmic rate ÷ peak) from CUDA-event kernel times, for every
+    kernel with a defined bound; ncu-derived fields (traffic, IPC, L2 hit rate) from the committed summary."""
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    fp32_peak = SMS * 128 * sm_max * 1e6 / 1e12  # Tops/s, one fp32 op per lane per clock
+    fp32_peak = SMS * 128 * sm_max * 1e6 / 1e12  # T lane-ops/s, one fp32 op per lane per clock
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0)) / 1000.0  # TB/s
     # dense-block peak from the measured bf16 figure x the guide's nominal ratio: fp4 9/2.25, int8 4.5/2.25
     mma_peak = (4.0 if MMA_FP4 else 2.0) * float(pk.get("bf16_tflops", 1590.0))
     out = {}
 
-    def entry(name, bound, units, peak, unit, per_unit):
+    def entry(name, bound, units, peak, unit, per_unit, tests=None):
         ms, launches = kern.get(name, (0.0, 0))
         if not launches or not ms:
             return
         t = ms / launches / 1000.0
-        ach = units / t / 1e12
+        e = {"bound": bound, "measured_ms_per_launch": t * 1000, "per_unit": per_unit}
+        if units is not None:
+            ach = units / t / 1e12
+            e.update(achieved=ach, peak=peak, unit=unit, frac=ach / peak)
         tr = ncu_traffic(name)
-        out[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                     "measured_ms_per_launch": t * 1000, "per_unit": per_unit,
-                     "traffic": (tr["dram_bytes_per_pair"] * pairs) if tr else None,
-                     "traffic_source": (tr["source"] + " (ncu --set full dram read+write per pair x pairs)") if tr else None}
+        e["traffic"] = (tr["dram_bytes_per_pair"] * pairs) if tr else None
+        e["traffic_source"] = (tr["source"] + " (ncu --set full dram read+write per pair x pairs)") if tr else None
+        nc = ncu_metrics(name)
+        if nc:
+            e["ncu"] = {k: round(v, 3) for k, v in nc.items() if k in ("ipc", "l2_hit_pct", "dram_pct", "fma_pipe_pct",
+                                                                          "alu_pipe_pct", "tensor_pipe_pct", "occupancy_pct")}
+            if units is None:  # issue-bound kernels: warp instructions issued per cycle per SM, of 4
+                e.update(achieved=nc.get("ipc", 0.0), peak=4.0, unit="warp-instr/clk/SM (ncu)",
+                         frac=nc.get("ipc", 0.0) / 4.0)
+        if name in ISSUE_MIX and tests:
+            fp, alu = ISSUE_MIX[name]
+            t_issue = (fp + alu) * 2.0 * tests / 64.0 / (4 * SMS * sm_max * 1e6)
+            e["issue_bound"] = {"fp2_plus_alu_instr_per_64_tests": fp + alu, "bound_ms": t_issue * 1000,
+                                "frac": t_issue / t}
+        out[name] = e
 
-    entry("k_compat", "alu", work["compat_tests"] * 20, fp32_peak, "Tops/s (fp32)",
-          "20 fp32 ops of the Eq. 1 tree per pair test; N(N-1)/2 tests per pair")
+    entry("k_compat", "alu", work["compat_tests"] * 20, fp32_peak, "T lane-ops/s (fp32)",
+          "20 fp32 ops of the Eq. 1 tree per pair test; N(N-1)/2 tests per pair", tests=work["compat_tests"])
+    entry("k_score", "alu", work["score_tests"] * 15, fp32_peak, "T lane-ops/s (fp32)",
+          "15 FMA-pipe ops of the r13 tree per residual test; hypotheses x N tests per pair",
+          tests=work["score_tests"])
     entry("k_sc2_mma", "tensor", work["mma_ops"], mma_peak, "TOPS (fp4 e2m1)" if MMA_FP4 else "TOPS (int8)",
           "2*128*TN*K ops per upper MMA tile of the dense block, K = 32W, TN = %d" % (240 if MMA_FP4 else 256))
-    entry("k_score", "alu", work["score_tests"] * 24, 2 * fp32_peak, "TFLOP/s (fp32, FMA = 2)",
-          "24 flops per residual test (12 FMA-equivalents); hypotheses x N tests per pair")
+    entry("k_degree", "hbm", work["degree_bytes"], hbm_peak, "TB/s", "4W bytes per bit row read + 8 B per row")
+    entry("k_expand", "hbm", work["expand_bytes"], hbm_peak, "TB/s",
+          "16W B per X row (e2m1) + 12W B per heavy row (row read, UP written)")
+    for k in ("k_hist_hi", "k_hist_lo", "k_collect"):
+        entry(k, "hbm", work["edges"] * 4, hbm_peak, "TB/s", "4 B per O2 edge per pass")
+    for k in ("k_sc2", "k_sc2_light", "k_pgs"):
+        entry(k, "issue", None, None, None, "latency/issue-bound list and bitmap intersections (DESIGN.md §6)")
     return out
+
+
+def ncu_metrics(kernel):
+    """ncu --set full metrics of `kernel` from the newest committed profiles/*/ncu_full_summary.json, or None."""
+    import glob
+
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_summary.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        for k, v in d.items():
+            if k.split("<")[0].split("(")[0].replace("void ", "").strip() == kernel:
+                return v
+    return None
 
 
 # ------------------------------------------------------------------------------------------ host cores / oracle
