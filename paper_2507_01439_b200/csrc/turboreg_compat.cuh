@@ -126,6 +126,36 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
     return x;
 }
 
+// The same transpose in 13 instructions: the two byte-level stages are one PRMT each (a per-lane byte
+// selector), the three bit-level stages a funnel rotate by a per-lane amount and one bitwise select
+// (per-lane keep mask) — every stage free of predicated pairs.  The lane constants are built once per work
+// item (Transpose32 below) and shared by its tiles.
+struct Transpose32 {
+    uint32_t sel16, sel8, keep4, keep2, keep1, rot4, rot2, rot1;
+    __device__ __forceinline__ Transpose32() {
+        const int lane = threadIdx.x & 31;
+        sel16 = (lane & 16) ? 0x3276u : 0x5410u;  // hi lanes: (x & 0xffff0000) | (y >> 16); lo: (x & 0xffff) | (y << 16)
+        sel8 = (lane & 8) ? 0x3715u : 0x6240u;
+        keep4 = (lane & 4) ? 0xf0f0f0f0u : 0x0f0f0f0fu;
+        keep2 = (lane & 2) ? 0xccccccccu : 0x33333333u;
+        keep1 = (lane & 1) ? 0xaaaaaaaau : 0x55555555u;
+        rot4 = (lane & 4) ? 28u : 4u;
+        rot2 = (lane & 2) ? 30u : 2u;
+        rot1 = (lane & 1) ? 31u : 1u;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+        x = __byte_perm(x, __shfl_xor_sync(FULL, x, 16), sel16);
+        x = __byte_perm(x, __shfl_xor_sync(FULL, x, 8), sel8);
+        uint32_t y = __shfl_xor_sync(FULL, x, 4);
+        x = (x & keep4) | (__funnelshift_l(y, y, rot4) & ~keep4);
+        y = __shfl_xor_sync(FULL, x, 2);
+        x = (x & keep2) | (__funnelshift_l(y, y, rot2) & ~keep2);
+        y = __shfl_xor_sync(FULL, x, 1);
+        x = (x & keep1) | (__funnelshift_l(y, y, rot1) & ~keep1);
+        return x;
+    }
+};
+
 // One 32×32 tile (I, J >= I) by one warp, with the optional τ_base plane (r19): both planes need the exact
 // tree value of |a − b|, so this path evaluates it directly (lane = column, rows broadcast from shared memory).
 __device__ __forceinline__ void compat_tile_base(const WS& ws, int p, int n, int W, int T, int I, int J,
@@ -411,6 +441,7 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
         }
     }
     uint32_t* bits = ws.bits + p * ws.bits_stride;
+    const Transpose32 tp32;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
         const int c = (J + k) * 32 + lane;
@@ -420,7 +451,7 @@ __device__ __forceinline__ void compat_tiles_rp(const WS& ws, int p, int n, int 
         uint32_t okr = rv ? cvb : 0u;
         if (I == J + k) { okc &= ~(1u << lane); okr &= ~(1u << lane); }
         const uint32_t cw = colw[k] & okc;
-        const uint32_t rw = transpose32(cw) & okr;
+        const uint32_t rw = tp32(cw) & okr;
         if (rv && J + k < T) bits[(int64_t)r0 * W + J + k] = rw;
         if (cv) bits[(int64_t)c * W + I] = cw;
     }

@@ -31,10 +31,11 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
         const uint32_t ui = (w < W) ? upper_mask(ri[w], w, i) : 0u;
         const uint32_t uj = (w < W) ? upper_mask(rj[w], w, j) : 0u;
         const int pi = __popc(ui), pj = __popc(uj);
-        const int si = warp_incl_scan(pi), sj = warp_incl_scan(pj);
-        const int exi = carry_i + si - pi, exj = carry_j + sj - pj;
-        carry_i += __shfl_sync(FULL, si, 31);
-        carry_j += __shfl_sync(FULL, sj, 31);
+        const int sij = warp_incl_scan(pi | (pj << 16));  // both prefix scans in one (each sum <= 1024)
+        const int exi = carry_i + (sij & 0xffff) - pi, exj = carry_j + (sij >> 16) - pj;
+        const int tij = __shfl_sync(FULL, sij, 31);
+        carry_i += tij & 0xffff;
+        carry_j += tij >> 16;
         uint32_t m = ui & uj;
         const int cm = __popc(m);
         const int incl = warp_incl_scan(cm);
