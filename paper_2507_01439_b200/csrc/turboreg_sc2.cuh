@@ -363,7 +363,7 @@ constexpr int light_warp_words() {
     return LG * 32 * WPL + LG * (list_max_of<WPL>() / 2) + 64 + 64 + 4 * LG;
 }
 template <int WPL, int LG = light_rows<WPL>()>
-constexpr int light_smem_bytes() { return 8 * light_warp_words<WPL, LG>() * 4; }
+constexpr int light_smem_bytes() { return (8 * light_warp_words<WPL, LG>() + 32 * WPL) * 4; }  // + sparse-row mask
 
 template <int WPL>
 __device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t* bm, const int32_t* meta,
@@ -394,6 +394,14 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int nl = ws.st[p].n_light;
     int gr_lo, gr_hi;  // this rank's groups of LG sparse rows (all of them unless the pair is split)
     split_range(ws, (nl + LG - 1) / LG, &gr_lo, &gr_hi);
+    if (gr_lo + (int)blockIdx.x * 8 >= gr_hi) return;  // the whole block is idle
+    // the sparse-row mask in shared memory: the enumeration below tests one bit per list entry
+    uint32_t* s_lm = s_dyn + 8 * light_warp_words<WPL, LG>();
+    {
+        const uint32_t* lmg = ws.light_mask + p * (ws.bits_stride / ws.row_stride);
+        for (int w = threadIdx.x; w < W; w += blockDim.x) s_lm[w] = lmg[w];
+        __syncthreads();
+    }
     const int gi = gr_lo + blockIdx.x * 8 + warp;
     if (gi >= gr_hi) return;
     const int g0 = gi * LG;
@@ -442,8 +450,6 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
     const int M = __shfl_sync(FULL, incl, 31);
     if (lane < nr) meta[4 * lane + 3] = my_pref;
     __syncwarp();
-    const int mstride = ws.bits_stride / ws.row_stride;
-    const uint32_t* lmask = ws.light_mask + p * mstride;
     int nL = 0;
     for (int e0 = 0; e0 < M; e0 += 32) {
         const int e = e0 + lane;
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
             const int t = lo + (e - pr);
             const int j = ls[r * LM + t];
             packed = (uint32_t)j | ((uint32_t)t << 16) | ((uint32_t)r << 24);
-            isL = (__ldg(lmask + (j >> 5)) >> (j & 31)) & 1u;  // sparse j; dense j is k_sc2's edge
+            isL = (s_lm[j >> 5] >> (j & 31)) & 1u;  // sparse j; dense j is k_sc2's edge
         }
         const unsigned bL = __ballot_sync(FULL, isL);
         if (isL) qL[nL + __popc(bL & ((1u << lane) - 1u))] = packed;

@@ -66,11 +66,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     }
 }
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2) {
+// X tiles are re-read by every tile of their pair (35 per config-E pair): loaded with an L2 evict_last policy
+// so the pair's operand block stays in L2 while the edge stores stream past it.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2,
+                                            uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
@@ -242,6 +250,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             TableCursor tc{s_tpre, s_th, TN};
             int it = 0;
             int p, rb, cb, h;
+            const uint64_t pol = l2_evict_last_policy();
             for (int g = g_lo + blockIdx.x;
                  g < g_hi && (table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h));
                  g += gridDim.x) {
@@ -253,9 +262,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     const uint32_t a_dst = tiles + s * MMA_STAGE_BYTES;
                     const uint32_t b_dst = a_dst + MMA_A_BYTES;
                     mbar_expect_tx(full0 + 8 * s, MMA_STAGE_BYTES);
-                    tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, ws.pair_base + p);
-                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN, ws.pair_base + p);
-                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN + 128, ws.pair_base + p);
+                    tma_load_3d(a_dst, &tmX, full0 + 8 * s, kb * MMA_BK, rb * MMA_BM, ws.pair_base + p, pol);
+                    tma_load_3d(b_dst, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN, ws.pair_base + p, pol);
+                    tma_load_3d(b_dst + MMA_A_BYTES, &tmX, full0 + 8 * s, kb * MMA_BK, cb * TN + 128, ws.pair_base + p, pol);
                 }
             }
         }
@@ -413,7 +422,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                     for (int r = 0; r < 16; ++r) {
                         const uint32_t x = u[r].x;
                         const uint32_t slot = (uint32_t)(s_eb[ew * 32 + rh + r] + (int)u[r].y) + __popc(x & bm1);
-                        if (rh + r < lim && (x & bit)) edges[slot] = jhi | vt[r * 34 + lane];
+                        if (rh + r < lim && (x & bit)) __stcs(edges + slot, jhi | vt[r * 34 + lane]);
                     }
                 }
                 __syncwarp();

@@ -297,3 +297,38 @@ def test_ranked_hypotheses_match_oracle(TR, metric, key, n, graph_mode):
     assert tuple(got[0]["clique"]) == tuple(res["clique"])
     top = tr.ranked_hypotheses(0, metric, top_k=5)
     assert top.tobytes() == got[:5].tobytes()
+
+
+def test_api_argument_errors(TR):
+    """Argument failures return INVALID_ARGUMENT (raised by the binding) and leave the context usable."""
+    import ctypes
+
+    from paper_2507_01439_b200._binding import Params, Status, TurboRegError, library
+
+    cfg = synth.CONFIGS["A"]
+    inst = synth.workload_instance(cfg, pair=3)
+    lib = library()
+    h = ctypes.c_void_p()
+    prm = Params(cfg.tau, 0.0, cfg.k1, cfg.k2, cfg.inlier_threshold, 0, 0)
+    assert lib.turboreg_create_ex(ctypes.byref(prm), 0, 500, 1, -1, ctypes.byref(h)) == Status.INVALID_ARGUMENT
+    assert lib.turboreg_create_ex(ctypes.byref(prm), 0, 2, 1, 0, ctypes.byref(h)) == Status.INVALID_ARGUMENT
+    bad = Params(cfg.tau, 0.0, cfg.k1, cfg.k2, cfg.inlier_threshold, 0, 0x40)  # unknown flag
+    assert lib.turboreg_create_ex(ctypes.byref(bad), 0, 500, 1, 0, ctypes.byref(h)) == Status.INVALID_ARGUMENT
+    tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=cfg.n)
+    with pytest.raises(TurboRegError):
+        tr.set_option("no_such_option", 1)
+    with pytest.raises(TurboRegError):
+        tr.set_option("heavy_cap", 100)  # not a multiple of 256
+    with pytest.raises(TurboRegError):
+        tr.ranked_hypotheses(0, "in")  # no call yet
+    r = tr.register(inst["src"], inst["dst"])
+    with pytest.raises(TurboRegError):
+        tr.ranked_hypotheses(0, "mae")  # errors not accumulated by this context
+    with pytest.raises(TurboRegError):
+        tr.ranked_hypotheses(1, "in")  # no such pair in the last call
+    with pytest.raises(TurboRegError):
+        tr.split_begin(inst["src"], inst["dst"], 2, 2)  # rank outside [0, world)
+    assert tr.split_begin(inst["src"][:2], inst["dst"][:2], 0, 2) == 2  # too few points: the pair's status
+    r2 = tr.register(inst["src"], inst["dst"])
+    assert tuple(r2["clique"]) == tuple(r["clique"]) and r2["inlier_count"] == r["inlier_count"]
+    assert len(tr.ranked_hypotheses(0, "in", top_k=3)) == 3
