@@ -78,6 +78,7 @@ struct WS {
     int32_t* deg_full;    // [n] full degree
     int32_t* hpos;        // [n] position in H or -1
     int32_t* heavy_list;  // [cap] H in index order
+    int32_t* tile_tab;    // [2·batch + 1]: tensor-core tile-count prefix over the batch's pairs, then |H| per pair
     uint16_t* lists;      // [n][LIST_MAX] sorted neighbour lists of rows with degree <= LIST_MAX
     int32_t* light_list;  // [n] sparse non-heavy rows, index order
     int32_t* dense_list;  // [n] all other rows, index order

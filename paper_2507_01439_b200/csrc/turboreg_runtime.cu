@@ -218,7 +218,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.cl_stride = KC;
     void* p_desc; void* p_st; void* p_src4; void* p_dst4; void* p_bits; void* p_bitsb = nullptr; void* p_deg;
     void* p_gt; void* p_eq; void* p_take; void* p_off; void* p_edges; void* p_piv; void* p_cl; void* p_hyp;
-    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp; void* p_rs;
+    void* p_res; void* p_in; void* p_degf; void* p_hpos; void* p_X; void* p_D; void* p_hl; void* p_hm; void* p_lm; void* p_up; void* p_upre = nullptr; void* p_herr; void* p_ctr; void* p_lists; void* p_ll; void* p_dl; void* p_cand; void* p_rp; void* p_rs; void* p_tt;
     const int64_t cap = c->heavy_cap_alloc, Kcap = fp4 ? round_up((int64_t)W * 16, trk::MMA_BK) : (int64_t)W * 32;
     std::vector<Item> items = {
         {sizeof(trk::PairDesc) * B, &p_desc},
@@ -253,6 +253,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(unsigned long long) * (size_t)(trk::PIV_CAP * B), &p_cand},
         {sizeof(int32_t) * (size_t)((N + 1) * B), &p_rp},
         {sizeof(int32_t) * (size_t)(N * B), &p_rs},
+        {sizeof(int32_t) * (size_t)(2 * B + 1), &p_tt},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     if (c->prm.graph_mode == 1) items.push_back({sizeof(uint16_t) * N * W * B, &p_upre});
@@ -298,6 +299,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_D = withD ? static_cast<uint16_t*>(p_D) : nullptr;
     w.heavy_D_stride = cap * cap;
     w.heavy_list = static_cast<int32_t*>(p_hl);
+    w.tile_tab = static_cast<int32_t*>(p_tt);
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
     w.light_mask = static_cast<uint32_t*>(p_lm);
     w.heavy_UP = static_cast<uint2*>(p_up);
@@ -519,6 +521,10 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
                 trk::k_emit_hh<<<dim3((unsigned)(ws.heavy_cap / 8), B), 256, 0, s>>>(ws);
             }));
         } else {
+            if (batch > trk::MMA_TABLE_PAIRS) {
+                trk::k_tile_table<<<1, 1024, 0, s>>>(ws, batch, ws.x_fp4 ? 240 : trk::MMA_BN);
+                CK(cudaGetLastError());
+            }
             CK(L.run(KID_SC2_MMA, [&] {
                 if (ws.x_fp4) trk::k_sc2_mma<true><<<c->num_sms, trk::MMA_THREADS, trk::MMA_SMEM_BYTES, s>>>(c->tmX4, ws, B);
                 else trk::k_sc2_mma<false><<<c->num_sms, trk::MMA_THREADS, trk::MMA_SMEM_BYTES, s>>>(c->tmX, ws, B);

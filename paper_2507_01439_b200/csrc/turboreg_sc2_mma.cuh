@@ -31,8 +31,7 @@ constexpr int MMA_B_BYTES = MMA_BN * MMA_BK;  // 32 KB
 constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
 constexpr int MMA_EPI_WARPS = 16;  // 4 per TMEM lane quarter; sub-warp k drains 32-column chunks k, k+4
 constexpr int MMA_EPI_SUB = MMA_EPI_WARPS / 4;
-constexpr int MMA_PAIRS_MAX = 4096;  // pair-prefix table in shared memory (larger batches loop over it)
-constexpr int MMA_TABLE_PAIRS = 1024;  // pair table in shared memory (larger batches walk global state)
+constexpr int MMA_TABLE_PAIRS = 1024;  // pair table in shared memory (larger batches: k_tile_table's global one)
 constexpr int MMA_SMEM_BYTES = MMA_STAGES * MMA_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
                                (2 * MMA_TABLE_PAIRS + 1) * 4 /*tile prefix + |H| per pair*/ +
                                MMA_EPI_WARPS * 16 * 34 * 2 /*transpose*/ + MMA_EPI_WARPS * 32 * 4 /*row bases*/;
@@ -120,31 +119,9 @@ __device__ __forceinline__ void mma_tile_coords(int t, int h, int TN, int* rb_ou
     }
     *rb_out = *cb_out = 0;
 }
-// Global tile g of the batch -> (pair, rb, cb): linear walk over pairs with a running prefix (each role
-// walks its own tiles in increasing g, so the cursor only moves forward).
-struct TileCursor {
-    int p = 0, base = 0, cnt = -1, TN = MMA_BN;
-    __device__ bool locate(const WS& ws, int batch, int g, int* pp, int* rb, int* cb, int* h) {
-        for (;;) {
-            if (p >= batch) return false;
-            if (cnt < 0) {
-                const int hh = (ws.desc[p].n == 0) ? 0 : ws.st[p].heavy_h;
-                cnt = hh ? mma_tile_count(hh, TN) : 0;
-            }
-            if (g < base + cnt) break;
-            base += cnt;
-            cnt = -1;
-            ++p;
-        }
-        *pp = p;
-        *h = ws.st[p].heavy_h;
-        mma_tile_coords(g - base, *h, TN, rb, cb);
-        return true;
-    }
-};
-
-// The same walk over a shared-memory table built once per CTA (tile-count prefix and |H| per pair), for
-// batches up to MMA_PAIRS_MAX: no dependent global loads at tile boundaries.
+// Global tile g of the batch -> (pair, rb, cb) from the tile-count prefix and |H| per pair: a shared-memory
+// table built once per CTA for batches up to MMA_TABLE_PAIRS, else k_tile_table's global one (L1-cached);
+// each role walks its tiles in increasing g, so the pair cursor only moves forward.
 struct TableCursor {
     const int32_t* pre;  // [batch + 1] exclusive prefix of the pairs' tile counts
     const int32_t* hh;   // [batch] |H| per pair
@@ -159,6 +136,37 @@ struct TableCursor {
         return true;
     }
 };
+
+// The batch's tile table for batches beyond the shared-memory table (k_sc2_mma reads it through L1): one
+// block, a scan of the pairs' tile counts.
+__global__ void __launch_bounds__(1024) k_tile_table(WS ws, int batch, int TN) {
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < batch; q0 += 1024) {
+        const int q = q0 + t;
+        const int hq = (q < batch && ws.desc[q].n != 0) ? ws.st[q].heavy_h : 0;
+        const int c = hq ? mma_tile_count(hq, TN) : 0;
+        const int x = warp_incl_scan(c);
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const int y = s_w[lane];
+            s_w[lane] = warp_incl_scan(y) - y;
+        }
+        __syncthreads();
+        if (q < batch) {
+            ws.tile_tab[q + 1] = s_carry + s_w[warp] + x;
+            ws.tile_tab[batch + 1 + q] = hq;
+        }
+        __syncthreads();
+        if (t == 1023) s_carry += s_w[31] + x;
+        __syncthreads();
+    }
+    if (t == 0) ws.tile_tab[0] = 0;
+}
 
 __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -183,7 +191,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);     // [warps][32] edge-list bases
     int32_t* s_tpre = s_eb + MMA_EPI_WARPS * 32;                                    // [batch + 1] tile prefix
     int32_t* s_th = s_tpre + MMA_TABLE_PAIRS + 1;                                 // [batch] |H|
-    const bool table = batch <= MMA_TABLE_PAIRS;
+    const bool smem_table = batch <= MMA_TABLE_PAIRS;
+    const int32_t* t_pre = smem_table ? s_tpre : ws.tile_tab;
+    const int32_t* t_h = smem_table ? s_th : ws.tile_tab + batch + 1;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp: provably uniform
 
     if (threadIdx.x == 0) {
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tptr));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (table) {  // tile counts per pair, then their exclusive prefix (warp 0)
+    if (smem_table) {  // tile counts per pair, then their exclusive prefix (warp 0)
         for (int q = threadIdx.x; q < batch; q += blockDim.x) {
             const int hq = (ws.desc[q].n == 0) ? 0 : ws.st[q].heavy_h;
             s_th[q] = hq;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(gen_tptr);
     // global tile range of this launch: every tile, or this rank's share of a split pair (batch 1, table)
     int g_lo = 0, g_hi = 0x7fffffff;
-    if (ws.split_world > 1 && table) split_range(ws, s_tpre[batch], &g_lo, &g_hi);
+    if (ws.split_world > 1) split_range(ws, t_pre[batch], &g_lo, &g_hi);
     if constexpr (FP4) {  // block scales: UE8M0 127 (= 1.0) in every byte of columns 496..511
         if (warp >= 2 && warp < 6) {
             const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 496u;
@@ -245,14 +255,12 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
-            TileCursor cur;
-            cur.TN = TN;
-            TableCursor tc{s_tpre, s_th, TN};
+            TableCursor tc{t_pre, t_h, TN};
             int it = 0;
             int p, rb, cb, h;
             const uint64_t pol = l2_evict_last_policy();
             for (int g = g_lo + blockIdx.x;
-                 g < g_hi && (table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h));
+                 g < g_hi && tc.locate(batch, g, &p, &rb, &cb, &h);
                  g += gridDim.x) {
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
@@ -270,13 +278,11 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         }
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
-            TileCursor cur;
-            cur.TN = TN;
-            TableCursor tc{s_tpre, s_th, TN};
+            TableCursor tc{t_pre, t_h, TN};
             int it = 0, lt = 0;
             int p, rb, cb, h;
             for (int g = g_lo + blockIdx.x;
-                 g < g_hi && (table ? tc.locate(batch, g, &p, &rb, &cb, &h) : cur.locate(ws, batch, g, &p, &rb, &cb, &h));
+                 g < g_hi && tc.locate(batch, g, &p, &rb, &cb, &h);
                  g += gridDim.x, ++lt) {
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 const int acc = lt & 1;
@@ -309,11 +315,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         const int sub = ew >> 2;
         constexpr int NCH = MMA_BN / 32;
         const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
-        TileCursor cur;
-        cur.TN = TN;
-        TableCursor tc{s_tpre, s_th, TN};
+        TableCursor tc{t_pre, t_h, TN};
         auto locate = [&](int gq, int* pp, int* rbp, int* cbp, int* hp) {
-            return gq < g_hi && (table ? tc.locate(batch, gq, pp, rbp, cbp, hp) : cur.locate(ws, batch, gq, pp, rbp, cbp, hp));
+            return gq < g_hi && tc.locate(batch, gq, pp, rbp, cbp, hp);
         };
         // per-warp tile metadata in registers (no block barrier between tiles): the heavy ids of this warp's
         // columns (lane = column of chunks sub and sub + MMA_EPI_SUB) and its rows' edge-list bases (lane =
