@@ -536,7 +536,9 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
         const int sc2_bpp = std::max(trk::SC2_BLOCKS_PER_PAIR,
                                      std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
         const dim3 gp((unsigned)sc2_bpp, B);
-        const int cpi = c->opt_sc2_chunks > 0 ? c->opt_sc2_chunks : (batch >= 32 ? 64 : 1);  // chunks per item
+        // chunks per item: whole rows for batches; 4 chunks (128 words) for large N, where one pair has
+        // thousands of dense rows and a single-chunk item would re-stage its row W/32 times; else one chunk
+        const int cpi = c->opt_sc2_chunks > 0 ? c->opt_sc2_chunks : (batch >= 32 ? 64 : Wb > 512 ? 4 : 1);
         // the sparse-row kernel needs only the row classes and lists: it runs on the side stream while the
         // dense-row kernel runs here (both are latency-bound; timed calls keep one stream for the events)
         const bool fork = c->use_fork && !timed;

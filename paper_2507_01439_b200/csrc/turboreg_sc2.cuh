@@ -22,7 +22,9 @@ template <int WPL>
 constexpr int list_max_of() { return WPL >= 16 ? LIST_MAX_BIG : LIST_MAX; }
 constexpr int MMA_BK_ = 128;  // K granularity of the tensor-core block (= MMA_BK)
 template <int WPL>
-constexpr int sc2_warp_words() { return 96 * WPL + 32 * WPL; }  // U_i, rank prefix, row i, queue
+constexpr int sc2_qcap() { return WPL >= 8 ? 256 : 32 * WPL; }  // sparse-neighbour queue entries per warp
+template <int WPL>
+constexpr int sc2_warp_words() { return 64 * WPL + sc2_qcap<WPL>(); }  // row i, its U_i rank prefix, queue
 template <int WPL>
 constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 * 32 * WPL) * 4; }
 
@@ -103,34 +105,34 @@ __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, in
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
-// Edge between dense row i (bitmap sr, U_i words su, rank prefix sp in shared memory) and sparse row j, on
-// either side of i: one code path for both sides (no divergence).
+// Edge between dense row i (bitmap sr and the exclusive prefix sp of U_i's popcounts per word in shared
+// memory; U_i's words are sr's above i) and sparse row j, on either side of i: one code path for both sides.
 template <int LM>
 __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
                                                 const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
-                                                const uint32_t* su, const int32_t* sp, const uint32_t* sr, int i,
-                                                int j) {
+                                                const int32_t* sp, const uint32_t* sr, int i, int j) {
     const uint16_t* L = lists + (int64_t)j * LM;
     int rank;
     const uint32_t c = list_bitmap_count_rank<LM>(L, deg_full[j], sr, i, j, &rank);
     const int wj = j >> 5;
-    uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u)) : edges + rowptr[j] + rank;
+    uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(upper_mask(sr[wj], wj, i) & ((1u << (j & 31)) - 1u))
+                            : edges + rowptr[j] + rank;
     *dst = ((uint32_t)((j > i) ? j : i) << 16) | c;
 }
 
 template <int WPL>
 __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 : 4)) k_sc2(WS ws, int cpi) {
     constexpr int G = 4;
-    constexpr int QCAP = 32 * WPL;  // sparse-neighbour queue (a round adds at most 32 entries)
+    constexpr int QCAP = sc2_qcap<WPL>();  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // block: heavy mask, sparse mask; per warp: U_i, rank prefix, row i, queue
+    // block: heavy mask, sparse mask; per warp: row i, rank prefix of U_i per word, queue (U_i's words are
+    // row i's above i, recomputed where needed: a smaller footprint keeps large-N rows at 2 blocks per SM)
     uint32_t* hm = s_dyn;
     uint32_t* lm = s_dyn + 32 * WPL;
-    uint32_t* su = s_dyn + 64 * WPL + warp * sc2_warp_words<WPL>();
-    int32_t* sp = reinterpret_cast<int32_t*>(su + 32 * WPL);
-    uint32_t* sr = su + 64 * WPL;
-    uint32_t* sq = su + 96 * WPL;
+    uint32_t* sr = s_dyn + 64 * WPL + warp * sc2_warp_words<WPL>();
+    int32_t* sp = reinterpret_cast<int32_t*>(sr + 32 * WPL);
+    uint32_t* sq = sr + 64 * WPL;
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -177,7 +179,6 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 
                 const int cnt = __popc(u);
                 const int incl = warp_incl_scan(cnt);
                 sr[w] = reg[k];
-                su[w] = u;
                 sp[w] = carry + incl - cnt;
                 carry += __shfl_sync(FULL, incl, 31);
             }
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 
             const int w = c * 32 + lane;
             const uint32_t lmw = (w < W) ? lm[w] : 0u;
             uint32_t ul = ((w < W) ? sr[w] : 0u) & lmw;
-            uint32_t ud = ((w < W) ? su[w] : 0u) & ~lmw;
+            uint32_t ud = ((w < W) ? upper_mask(sr[w], w, i) : 0u) & ~lmw;
             if (hi >= 0 && w < W) ud &= ~hm[w];
             while (__any_sync(FULL, (ul | ud) != 0u)) {
                 int jl = -1, jd = -1;
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 
                 nq += __popc(sb);
                 if (nq > QCAP - 32) {
                     __syncwarp();
-                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
+                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, sp, sr, i, (int)sq[t]);
                     __syncwarp();
                     nq = 0;
                 }
@@ -242,14 +243,15 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 
                         const uint32_t tot = __reduce_add_sync(FULL, part[g]);
                         if (lane == g) {
                             const int j = jj[g], wj = j >> 5;
-                            erow[sp[wj] + __popc(su[wj] & ((1u << (j & 31)) - 1u))] = ((uint32_t)j << 16) | tot;
+                            erow[sp[wj] + __popc(upper_mask(sr[wj], wj, i) & ((1u << (j & 31)) - 1u))] =
+                                ((uint32_t)j << 16) | tot;
                         }
                     }
                 }
             }
         }
         __syncwarp();
-        for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, su, sp, sr, i, (int)sq[t]);
+        for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, sp, sr, i, (int)sq[t]);
         __syncwarp();
     }
 }

@@ -86,3 +86,25 @@ def test_bench_spawns_ranks_and_gathers_gloo():
     assert len(lines) == 1, r.stdout
     assert lines[0] == {"selftest": "gloo", "n_gpus": 2, "world": 2, "pairs": 1623, "scaling": "strong",
                         "max_over_ranks": 2.0, "ok": True}
+
+
+def test_bench_reference_arm_json():
+    """`bench.py --impl reference`: the oracle on the host cores prints one JSON line with the same metric,
+    unit and direction as the CUDA arm, its cpu_baseline (kind, cores, sample) and an e2e record."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    base = json.load(open(os.path.join(root, "BASELINE.json")))
+    assert line["impl"] == "reference" and line["metric"] == base["metric"]
+    assert line["unit"] == "registrations/s" and line["higher_is_better"] is True and line["value"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
