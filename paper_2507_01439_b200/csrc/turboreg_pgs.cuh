@@ -15,17 +15,26 @@ constexpr int PGS_WARPS = 8;
 constexpr int PGS_KL = 8;
 constexpr int PGS_QCAP = 128;  // per-warp candidate queue (entries) of the O2 scan
 
+// Candidate keys (reading r8: S desc, z asc) in 32 bits: S = Ĝ_ij + Ĝ_iz + Ĝ_jz < 3·2^15 takes 17 bits and
+// z < 2^15 (n <= 32768) the low 15, stored as 32767 − z; every candidate key is > 0 (S >= Ĝ_ij >= 1).
+constexpr uint32_t PGS_ZMAX = 32767u;
+// (Ĝ_a + Ĝ_b) << 15 from two edge words (z << 16 | Ĝ): the Ĝ fields shifted to the top add without a carry
+// out (Ĝ_a + Ĝ_b < 2^16) and the z fields fall off.
+__device__ __forceinline__ uint32_t pgs_pair_sum15(uint32_t a, uint32_t b) { return ((a << 16) + (b << 16)) >> 1; }
+
 // Candidates of a 32-word chunk are flattened across the warp before their weights are gathered: every lane
 // writes its own candidates (z, rank in U_i, rank in U_j) to the warp's shared-memory queue at its prefix
 // offset, then the lanes take the queue entries round-robin, so the gathers and the top-K2 insertions run
 // on all 32 lanes whatever the distribution of candidates over the words (a chunk with more than PGS_QCAP
-// candidates falls back to each lane walking its own word).
+// candidates, i.e. one where most words hold several, has each lane walk its own word: highest bit first,
+// one mask ~(−1 << b) giving both the remaining bits and the rank prefixes).
 template <typename F>
 __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const uint32_t* rj, int W, int i, int j,
                                                     const uint32_t* ei, const uint32_t* ej, int wij, uint2* sq, F&& f) {
     const int lane = threadIdx.x & 31;
     int carry_i = 0, carry_j = 0;
     const int nchunks = (W + 31) >> 5;
+    const uint32_t wbase = ((uint32_t)wij << 15) + PGS_ZMAX;
     for (int c = (i + 1) >> 10; c < nchunks; ++c) {  // chunks holding no bit > i contribute nothing
         const int w = c * 32 + lane;
         const uint32_t ui = (w < W) ? upper_mask(ri[w], w, i) : 0u;
@@ -44,9 +53,9 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
         if (total <= PGS_QCAP) {
             int o = incl - cm;
             while (m) {  // this lane's candidates into the queue
-                const int b = __ffs(m) - 1;
-                m &= m - 1u;
-                const uint32_t below = (1u << b) - 1u;
+                const int b = 31 - __clz(m);
+                const uint32_t below = ~(0xffffffffu << b);
+                m &= below;
                 const uint32_t rk_i = (uint32_t)(exi + __popc(ui & below)), rk_j = (uint32_t)(exj + __popc(uj & below));
                 sq[o++] = make_uint2((uint32_t)(w * 32 + b) | (rk_i << 16), rk_j);
             }
@@ -57,23 +66,20 @@ __device__ __forceinline__ void pgs_scan_candidates(const uint32_t* ri, const ui
                 const uint2 e1 = two ? sq[k + 32] : e0;
                 const uint32_t a0 = __ldg(ei + (e0.x >> 16)), b0 = __ldg(ej + e0.y);
                 const uint32_t a1 = __ldg(ei + (e1.x >> 16)), b1 = __ldg(ej + e1.y);
-                const int S0 = wij + (int)(a0 & 0xffffu) + (int)(b0 & 0xffffu);
-                f(((unsigned long long)(unsigned)S0 << 32) | (unsigned long long)(0xffffffffu - (e0.x & 0xffffu)));
-                if (two) {
-                    const int S1 = wij + (int)(a1 & 0xffffu) + (int)(b1 & 0xffffu);
-                    f(((unsigned long long)(unsigned)S1 << 32) | (unsigned long long)(0xffffffffu - (e1.x & 0xffffu)));
-                }
+                f(pgs_pair_sum15(a0, b0) + wbase - (e0.x & 0xffffu));
+                if (two) f(pgs_pair_sum15(a1, b1) + wbase - (e1.x & 0xffffu));
             }
             __syncwarp();
         } else {
+            const uint32_t* pei = ei + exi;
+            const uint32_t* pej = ej + exj;
+            const uint32_t zb = wbase - (uint32_t)(w * 32);
             while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1u;
-                const uint32_t below = (1u << b) - 1u;
-                const int wiz = (int)(__ldg(ei + exi + __popc(ui & below)) & 0xffffu);
-                const int wjz = (int)(__ldg(ej + exj + __popc(uj & below)) & 0xffffu);
-                const int z = w * 32 + b;
-                f(((unsigned long long)(unsigned)(wij + wiz + wjz) << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+                const int b = 31 - __clz(m);
+                const uint32_t below = ~(0xffffffffu << b);
+                m &= below;
+                const uint32_t a = __ldg(pei + __popc(ui & below)), e = __ldg(pej + __popc(uj & below));
+                f(pgs_pair_sum15(a, e) + zb - (uint32_t)b);
             }
         }
     }
@@ -113,8 +119,7 @@ __device__ __forceinline__ void pgs_scan_candidates_sc2(const WS& ws, int q, con
             const int z = w * 32 + b;
             const uint32_t wiz = (z > i) ? (__ldg(ei + exi + __popc(ui & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, i);
             const uint32_t wjz = (z > j) ? (__ldg(ej + exj + __popc(uj & below)) & 0xffffu) : sc2_lower_weight(ws, q, W, z, j);
-            const int S = wij + (int)wiz + (int)wjz;
-            f(((unsigned long long)(unsigned)S << 32) | (unsigned long long)(0xffffffffu - (unsigned)z));
+            f(((uint32_t)(wij + (int)wiz + (int)wjz) << 15) + PGS_ZMAX - (uint32_t)z);
         }
     }
 }
@@ -131,15 +136,17 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
                                              int j, const uint32_t* ei, const uint32_t* ej, int wij, int K2, int4* out,
                                              uint2* sq) {
     const int lane = threadIdx.x & 31;
-    unsigned long long top[KL];
+    uint32_t top[KL];
 #pragma unroll
-    for (int r = 0; r < KL; ++r) top[r] = 0ull;
-    auto insert = [&](unsigned long long key) {
+    for (int r = 0; r < KL; ++r) top[r] = 0u;
+    auto insert = [&](uint32_t key) {
         if (key > top[KL - 1]) {  // sorted insertion, descending
-            unsigned long long k = key;
+            uint32_t k = key;
 #pragma unroll
             for (int r = 0; r < KL; ++r) {
-                if (k > top[r]) { unsigned long long tmp = top[r]; top[r] = k; k = tmp; }
+                const uint32_t hi = max(k, top[r]);
+                k = min(k, top[r]);
+                top[r] = hi;
             }
         }
     };
@@ -147,18 +154,15 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
     else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, sq, insert);
     int emitted = 0;
     for (int r = 0; r < K2; ++r) {
-        const unsigned long long head = top[0];
-        const unsigned long long best = warp_max_u64(head);
-        if (best == 0ull) break;
+        const uint32_t head = top[0];
+        const uint32_t best = __reduce_max_sync(FULL, head);
+        if (best == 0u) break;
         if (head == best) {  // keys are unique (distinct z), exactly one lane pops
 #pragma unroll
             for (int s2 = 0; s2 < KL - 1; ++s2) top[s2] = top[s2 + 1];
-            top[KL - 1] = 0ull;
+            top[KL - 1] = 0u;
         }
-        if (lane == 0) {
-            const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
-            out[r] = sorted_clique(i, j, z, (int)(best >> 32));
-        }
+        if (lane == 0) out[r] = sorted_clique(i, j, (int)(PGS_ZMAX - (best & PGS_ZMAX)), (int)(best >> 15));
         ++emitted;
     }
     return emitted;
@@ -200,20 +204,17 @@ __global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws
     if constexpr (KL > 0) {
         emitted = pgs_topk_list<KL, MODE>(ws, q, ri, rj, W, i, j, ei, ej, wij, K2, out, sq);
     } else {
-        unsigned long long thr = ~0ull;
+        uint32_t thr = 0xffffffffu;
         for (int r = 0; r < K2; ++r) {
-            unsigned long long mine = 0ull;
-            auto take = [&](unsigned long long key) {
-                if (key < thr && key > mine) mine = key;
+            uint32_t mine = 0u;
+            auto take = [&](uint32_t key) {
+                if (key < thr) mine = max(mine, key);
             };
             if constexpr (MODE == 1) pgs_scan_candidates_sc2(ws, q, ri, rj, W, i, j, ei, ej, wij, take);
             else pgs_scan_candidates(ri, rj, W, i, j, ei, ej, wij, sq, take);
-            const unsigned long long best = warp_max_u64(mine);
-            if (best == 0ull) break;
-            if (lane == 0) {
-                const int z = (int)(0xffffffffu - (unsigned)(best & 0xffffffffull));
-                out[r] = sorted_clique(i, j, z, (int)(best >> 32));
-            }
+            const uint32_t best = __reduce_max_sync(FULL, mine);
+            if (best == 0u) break;
+            if (lane == 0) out[r] = sorted_clique(i, j, (int)(PGS_ZMAX - (best & PGS_ZMAX)), (int)(best >> 15));
             thr = best;
             ++emitted;
         }
