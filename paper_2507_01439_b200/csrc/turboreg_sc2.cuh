@@ -71,15 +71,15 @@ __device__ __forceinline__ uint32_t list_bitmap_count(const uint16_t* L, int len
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
-// As list_bitmap_count, for an edge (j, i) with j < i stored in row j: also returns the rank of i among
-// the entries of L_j above j (= #{x in L_j : j < x < i}).
+// As list_bitmap_count, also returning lt = #{x in L : x < i} (pads included) for the edge's slot.  The
+// comparison runs on both uint16 entries of a word at once: with c = 0x8000 + i − 1 in each half, the half
+// c − x lies in [1, 0xfffe] for x, i < 2^15, so no borrow crosses halves and its bit 15 is [x < i].
 template <int LM>
-__device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, int len, const uint32_t* sr, int i,
-                                                           int j, int* rank) {
+__device__ __forceinline__ uint32_t list_bitmap_count_lt(const uint16_t* L, int len, const uint32_t* sr, int i,
+                                                         int* lt) {
     const int nch = (len + 7) >> 3;
-    uint32_t cnt = 0;
-    int r = 0;
-    const unsigned span = (unsigned)(i - j - 1);
+    uint32_t cnt = 0, acc = 0;
+    const uint32_t c1 = 0x8000u + (uint32_t)i - 1u, cpair = c1 | (c1 << 16);
 #pragma unroll 1
     for (int c0 = 0; c0 < nch; c0 += 8) {
         uint4 v[8];
@@ -92,31 +92,39 @@ __device__ __forceinline__ uint32_t list_bitmap_count_rank(const uint16_t* L, in
                 const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int k0 = (int)(wv[e] & 0xffffu), k1 = (int)(wv[e] >> 16);
+                    const uint32_t k0 = wv[e] & 0xffffu, k1 = wv[e] >> 16;
                     cnt += ((sr[k0 >> 5] >> (k0 & 31)) & 1u) + ((sr[k1 >> 5] >> (k1 & 31)) & 1u);
-                    // j < k < i as one unsigned range test; pads are 0 <= j: never counted
-                    r += ((unsigned)(k0 - j - 1) < span) + ((unsigned)(k1 - j - 1) < span);
+                    acc += ((cpair - wv[e]) >> 15) & 0x10001u;
                 }
             }
         }
         if (LM <= 64) break;
     }
-    *rank = r;
+    *lt = (int)((acc & 0xffffu) + (acc >> 16));
     return cnt - (uint32_t)(nch * 8 - len) * (sr[0] & 1u);
 }
 
 // Edge between dense row i (bitmap sr and the exclusive prefix sp of U_i's popcounts per word in shared
 // memory; U_i's words are sr's above i) and sparse row j, on either side of i: one code path for both sides.
+// For j < i the edge lives in row j at rank #{x in L_j : j < x < i} = lt − pads − #{x in L_j : x < j}, the
+// last being deg(j) − |U_j| = deg_full[j] − (rowptr[j + 1] − rowptr[j]).
 template <int LM>
 __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* lists, const int32_t* deg_full,
                                                 const int32_t* rowptr, uint32_t* edges, uint32_t* erow,
                                                 const int32_t* sp, const uint32_t* sr, int i, int j) {
     const uint16_t* L = lists + (int64_t)j * LM;
-    int rank;
-    const uint32_t c = list_bitmap_count_rank<LM>(L, deg_full[j], sr, i, j, &rank);
+    const int len = deg_full[j];
+    int lt;
+    const uint32_t c = list_bitmap_count_lt<LM>(L, len, sr, i, &lt);
     const int wj = j >> 5;
-    uint32_t* dst = (j > i) ? erow + sp[wj] + __popc(upper_mask(sr[wj], wj, i) & ((1u << (j & 31)) - 1u))
-                            : edges + rowptr[j] + rank;
+    uint32_t* dst;
+    if (j > i) {
+        dst = erow + sp[wj] + __popc(upper_mask(sr[wj], wj, i) & ((1u << (j & 31)) - 1u));
+    } else {
+        const int r0 = rowptr[j], r1 = rowptr[j + 1];
+        const int pads = ((len + 7) & ~7) - len;
+        dst = edges + r0 + (lt - pads - (len - (r1 - r0)));
+    }
     *dst = ((uint32_t)((j > i) ? j : i) << 16) | c;
 }
 
@@ -184,32 +192,44 @@ __global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 
             }
         }
         __syncwarp();
-        // (2) sparse neighbours on both sides (queued, one edge per lane) and (3) dense-dense upper
-        // neighbours that are not both heavy (warp-cooperative popcount)
+        // (2) sparse neighbours on both sides, queued (one edge per lane) and (3) dense-dense upper
+        // neighbours that are not both heavy (warp-cooperative popcount).  A chunk's sparse neighbours enter
+        // the queue in one pass: each lane writes its word's bits at its prefix offset (virtual positions
+        // from nq; full windows of QCAP entries are processed as they fill).
         int nq = 0;
         for (int c = c_lo; c < c_hi; ++c) {
             const int w = c * 32 + lane;
             const uint32_t lmw = (w < W) ? lm[w] : 0u;
-            uint32_t ul = ((w < W) ? sr[w] : 0u) & lmw;
-            uint32_t ud = ((w < W) ? upper_mask(sr[w], w, i) : 0u) & ~lmw;
+            const uint32_t srw = (w < W) ? sr[w] : 0u;
+            uint32_t ul = srw & lmw;
+            uint32_t ud = (w < W) ? upper_mask(srw, w, i) & ~lmw : 0u;
             if (hi >= 0 && w < W) ud &= ~hm[w];
-            while (__any_sync(FULL, (ul | ud) != 0u)) {
-                int jl = -1, jd = -1;
-                if (ul) {
-                    jl = w * 32 + __ffs(ul) - 1;
-                    ul &= ul - 1u;
-                } else if (ud) {
+            const int cl = __popc(ul);
+            const int incl = warp_incl_scan(cl);
+            const int vend = nq + __shfl_sync(FULL, incl, 31);
+            int o = nq + incl - cl, qbase = 0;
+            while (vend - qbase > QCAP) {  // rare: the queue fills inside this chunk
+                while (ul && o < qbase + QCAP) {
+                    const int b = 31 - __clz(ul);
+                    ul &= ~(0xffffffffu << b);
+                    sq[o++ - qbase] = (uint32_t)(w * 32 + b);
+                }
+                __syncwarp();
+                for (int t = lane; t < QCAP; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, sp, sr, i, (int)sq[t]);
+                __syncwarp();
+                qbase += QCAP;
+            }
+            while (ul) {
+                const int b = 31 - __clz(ul);
+                ul &= ~(0xffffffffu << b);
+                sq[o++ - qbase] = (uint32_t)(w * 32 + b);
+            }
+            nq = vend - qbase;
+            while (__any_sync(FULL, ud != 0u)) {
+                int jd = -1;
+                if (ud) {
                     jd = w * 32 + __ffs(ud) - 1;
                     ud &= ud - 1u;
-                }
-                const unsigned sb = __ballot_sync(FULL, jl >= 0);
-                if (jl >= 0) sq[nq + __popc(sb & ((1u << lane) - 1u))] = (uint32_t)jl;
-                nq += __popc(sb);
-                if (nq > QCAP - 32) {
-                    __syncwarp();
-                    for (int t = lane; t < nq; t += 32) sc2_sparse_edge<list_max_of<WPL>()>(ws, lists, deg_full, rowptr, edges, erow, sp, sr, i, (int)sq[t]);
-                    __syncwarp();
-                    nq = 0;
                 }
                 unsigned lb = __ballot_sync(FULL, jd >= 0);
                 while (lb) {
