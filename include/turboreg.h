@@ -292,7 +292,9 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *                      scales, fp32 accumulate; exact below 2^24) with 128x240 tiles (default); 0 = kind::i8
  *                      with 128x256 tiles (same results)
  *   "sc2_chunks"       32-word chunks of a dense row per SC^2 work item: 0 = auto (whole rows for batches
- *                      >= 32 pairs, single chunks below), 1..64 fixed
+ *                      >= 32 pairs, 4 chunks for rows above 512 words, single chunks otherwise), 1..64 fixed
+ *   "mma_l2_policy"    L2 policy of the dense block's operand (TMA) loads: 1 = evict_last (default),
+ *                      0 = evict_normal, 2 = evict_first
  *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1
  *   "concurrent_sc2"   1 = the sparse-row SC^2 kernel runs on a second stream alongside the dense-row kernel
  *                      (default; calls with stage/kernel timing stay on one stream); 0 = one stream

@@ -79,6 +79,7 @@ struct WS {
     int32_t* hpos;        // [n] position in H or -1
     int32_t* heavy_list;  // [cap] H in index order
     int32_t* tile_tab;    // [2·batch + 1]: tensor-core tile-count prefix over the batch's pairs, then |H| per pair
+    int32_t* tile_ctr;    // tensor-core tile counter (dynamic tile scheduling), zeroed before every launch
     uint16_t* lists;      // [n][LIST_MAX] sorted neighbour lists of rows with degree <= LIST_MAX
     int32_t* light_list;  // [n] sparse non-heavy rows, index order
     int32_t* dense_list;  // [n] all other rows, index order
@@ -102,6 +103,7 @@ struct WS {
     double2* herr;        // [K1*K2][SCORE_SEGS_MAX] per hypothesis and correspondence segment (Σ sqrtf(s), Σ s)
                           // (r20); k_finalize adds the segments in order into slot [h][0] (deterministic)
     int32_t x_fp4;        // heavy_X holds packed e2m1 (block-scaled fp4 tensor-core path) instead of uint8
+    int32_t mma_l2;       // L2 policy of the X tile loads: 0 evict_normal, 1 evict_last, 2 evict_first
     int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
     // NEXT(1), one pair split over split_world ranks (1 = not split): this rank's share of every split work
     // list (compat block-row pairs from compat_b0, tensor-core tiles, dense-row items, sparse-row groups,

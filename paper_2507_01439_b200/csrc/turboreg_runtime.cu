@@ -143,6 +143,7 @@ struct turboreg_ctx {
     int num_sms = 148;
     int32_t opt_score_pairs = 2;
     int32_t opt_sc2_chunks = 0;  // 0 = auto
+    int32_t opt_mma_l2 = 1;      // L2 policy of the tensor-core block's X loads (WS::mma_l2)
 };
 
 namespace {
@@ -253,7 +254,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
         {sizeof(unsigned long long) * (size_t)(trk::PIV_CAP * B), &p_cand},
         {sizeof(int32_t) * (size_t)((N + 1) * B), &p_rp},
         {sizeof(int32_t) * (size_t)(N * B), &p_rs},
-        {sizeof(int32_t) * (size_t)(2 * B + 1), &p_tt},
+        {sizeof(int32_t) * (size_t)(2 * B + 2), &p_tt},
     };
     if (base) items.push_back({sizeof(uint32_t) * N * W * B, &p_bitsb});
     if (c->prm.graph_mode == 1) items.push_back({sizeof(uint16_t) * N * W * B, &p_upre});
@@ -300,6 +301,7 @@ turboreg_status alloc_ws(turboreg_ctx* c) {
     w.heavy_D_stride = cap * cap;
     w.heavy_list = static_cast<int32_t*>(p_hl);
     w.tile_tab = static_cast<int32_t*>(p_tt);
+    w.tile_ctr = w.tile_tab + 2 * B + 1;
     w.heavy_mask = static_cast<uint32_t*>(p_hm);
     w.light_mask = static_cast<uint32_t*>(p_lm);
     w.heavy_UP = static_cast<uint2*>(p_up);
@@ -346,6 +348,7 @@ void set_ws_params(turboreg_ctx* c) {
     // the tensor-core block needs the tensor map of the layout X was allocated in; without it, popcount only
     c->ws.sc2_path = (c->opt_sc2_path == 0 && !(c->alloc_fp4 ? c->tmX4_ok : c->tmX_ok)) ? 1 : c->opt_sc2_path;
     c->ws.x_fp4 = (c->ws.sc2_path == 0 && c->alloc_fp4) ? 1 : 0;
+    c->ws.mma_l2 = c->opt_mma_l2;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -525,6 +528,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
                 trk::k_tile_table<<<1, 1024, 0, s>>>(ws, batch, ws.x_fp4 ? 240 : trk::MMA_BN);
                 CK(cudaGetLastError());
             }
+            CK(cudaMemsetAsync(ws.tile_ctr, 0, sizeof(int32_t), s));
             CK(L.run(KID_SC2_MMA, [&] {
                 if (ws.x_fp4) trk::k_sc2_mma<true><<<c->num_sms, trk::MMA_THREADS, trk::MMA_SMEM_BYTES, s>>>(c->tmX4, ws, B);
                 else trk::k_sc2_mma<false><<<c->num_sms, trk::MMA_THREADS, trk::MMA_SMEM_BYTES, s>>>(c->tmX, ws, B);
@@ -846,6 +850,10 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
     } else if (k == "mma_fp4") {
         if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_mma_fp4 = (int32_t)value;
+    } else if (k == "mma_l2_policy") {
+        if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_mma_l2 = (int32_t)value;
+        drop_graphs(c);  // captured launches hold the workspace descriptor by value
     } else if (k == "sc2_chunks") {
         if (value < 0 || value > 64) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_sc2_chunks = (int32_t)value;

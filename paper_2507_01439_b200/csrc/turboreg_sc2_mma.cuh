@@ -26,6 +26,7 @@ constexpr int MMA_BM = 128;
 constexpr int MMA_BN = 256;
 constexpr int MMA_BK = 128;  // bytes = int8 elements per stage per row
 constexpr int MMA_STAGES = 4;
+constexpr int MMA_TILE_RING = 4;  // dynamic tile ids in flight between the producer and the consumers
 constexpr int MMA_A_BYTES = MMA_BM * MMA_BK;  // 16 KB
 constexpr int MMA_B_BYTES = MMA_BN * MMA_BK;  // 32 KB
 constexpr int MMA_STAGE_BYTES = MMA_A_BYTES + MMA_B_BYTES;
@@ -67,9 +68,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 // X tiles are re-read by every tile of their pair (35 per config-E pair): loaded with an L2 evict_last policy
 // so the pair's operand block stays in L2 while the edge stores stream past it.
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+__device__ __forceinline__ uint64_t l2_tile_policy(int which) {
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if (which == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else if (which == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, uint32_t bar, int c0, int c1, int c2,
@@ -184,8 +187,11 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     const uint32_t tiles = (base + 1023u) & ~1023u;  // 1024-byte aligned for the 128B swizzle
     const uint32_t bars = tiles + MMA_STAGES * MMA_STAGE_BYTES;
     // barriers: full[s] at bars + 8s, empty[s] at bars + 64 + 8s, tmem_full[2] at bars + 128,
-    // tmem_empty[2] at bars + 144; tmem ptr at bars + 192
+    // tmem_empty[2] at bars + 144; tile ring: tile_full[r] at bars + 32 + 8r, tile_empty[r] at bars + 96 + 8r,
+    // tile ids at bars + 160 + 4r; tmem ptr at bars + 192
     const uint32_t full0 = bars, empty0 = bars + 64, tfull0 = bars + 128, tempty0 = bars + 144, tptr = bars + 192;
+    const uint32_t gfull0 = bars + 32, gempty0 = bars + 96;
+    volatile int32_t* s_tg = reinterpret_cast<volatile int32_t*>(smem_raw + (bars + 160 - base));
     uint8_t* gen_tptr = smem_raw + (tptr - base);
     uint16_t* s_vt = reinterpret_cast<uint16_t*>(smem_raw + (bars + 256 - base));  // [warps][16][34] (Ĝ < 65536)
     int32_t* s_eb = reinterpret_cast<int32_t*>(s_vt + MMA_EPI_WARPS * 16 * 34);     // [warps][32] edge-list bases
@@ -204,6 +210,10 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
             mbar_init(tempty0 + 8 * b, MMA_EPI_WARPS);  // one arrive per epilogue warp
+        }
+        for (int r = 0; r < MMA_TILE_RING; ++r) {
+            mbar_init(gfull0 + 8 * r, 1);
+            mbar_init(gempty0 + 8 * r, 1 + MMA_EPI_WARPS);  // the MMA issuer and every epilogue warp read it
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -237,6 +247,18 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     // global tile range of this launch: every tile, or this rank's share of a split pair (batch 1, table)
     int g_lo = 0, g_hi = 0x7fffffff;
     if (ws.split_world > 1) split_range(ws, t_pre[batch], &g_lo, &g_hi);
+    // Dynamic tile scheduling: the producer takes the next global tile from ws.tile_ctr and publishes it in a
+    // shared-memory ring read by the MMA issuer and the epilogue warps (−1 = no more tiles).  The CTAs then
+    // work on one narrow window of the (pair, tile) list at any time, so a pair's X rows are fetched from
+    // HBM about once and re-read from L2 by its other tiles (static striding let the CTAs drift apart).
+    auto tile_get = [&](int lt) {  // consumers: wait for the ring slot of tile lt, read it
+        const int r = lt % MMA_TILE_RING;
+        mbar_wait(gfull0 + 8 * r, (lt / MMA_TILE_RING) & 1);
+        return s_tg[r];
+    };
+    auto tile_release = [&](int lt) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gempty0 + 8 * (lt % MMA_TILE_RING)) : "memory");
+    };
     if constexpr (FP4) {  // block scales: UE8M0 127 (= 1.0) in every byte of columns 496..511
         if (warp >= 2 && warp < 6) {
             const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 496u;
@@ -258,10 +280,15 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             TableCursor tc{t_pre, t_h, TN};
             int it = 0;
             int p, rb, cb, h;
-            const uint64_t pol = l2_evict_last_policy();
-            for (int g = g_lo + blockIdx.x;
-                 g < g_hi && tc.locate(batch, g, &p, &rb, &cb, &h);
-                 g += gridDim.x) {
+            const uint64_t pol = l2_tile_policy(ws.mma_l2);
+            for (int lt = 0;; ++lt) {
+                const int r = lt % MMA_TILE_RING;
+                if (lt >= MMA_TILE_RING) mbar_wait(gempty0 + 8 * r, (lt / MMA_TILE_RING - 1) & 1);
+                int g = g_lo + atomicAdd(ws.tile_ctr, 1);
+                if (!(g < g_hi && tc.locate(batch, g, &p, &rb, &cb, &h))) g = -1;
+                s_tg[r] = g;
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gfull0 + 8 * r) : "memory");
+                if (g < 0) break;
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % MMA_STAGES;
@@ -279,11 +306,13 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
             TableCursor tc{t_pre, t_h, TN};
-            int it = 0, lt = 0;
+            int it = 0;
             int p, rb, cb, h;
-            for (int g = g_lo + blockIdx.x;
-                 g < g_hi && tc.locate(batch, g, &p, &rb, &cb, &h);
-                 g += gridDim.x, ++lt) {
+            for (int lt = 0;; ++lt) {
+                const int g = tile_get(lt);
+                tile_release(lt);
+                if (g < 0) break;
+                tc.locate(batch, g, &p, &rb, &cb, &h);
                 const int KB = FP4 ? (ws.desc[p].W * 16 + MMA_BK - 1) / MMA_BK : ws.desc[p].W * 32 / MMA_BK;
                 const int acc = lt & 1;
                 if (lt >= 2) mbar_wait(tempty0 + 8 * acc, ((lt >> 1) - 1) & 1);  // epilogue drained it
@@ -317,7 +346,13 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         const int last_c = sub + (NCH - 1 - sub) / MMA_EPI_SUB * MMA_EPI_SUB;
         TableCursor tc{t_pre, t_h, TN};
         auto locate = [&](int gq, int* pp, int* rbp, int* cbp, int* hp) {
-            return gq < g_hi && tc.locate(batch, gq, pp, rbp, cbp, hp);
+            return gq >= 0 && tc.locate(batch, gq, pp, rbp, cbp, hp);
+        };
+        auto epi_tile = [&](int lt) {  // every lane reads the slot; lane 0 releases it for the warp
+            const int gq = tile_get(lt);
+            __syncwarp();
+            if (lane == 0) tile_release(lt);
+            return gq;
         };
         // per-warp tile metadata in registers (no block barrier between tiles): the heavy ids of this warp's
         // columns (lane = column of chunks sub and sub + MMA_EPI_SUB) and its rows' edge-list bases (lane =
@@ -328,7 +363,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             return (k < TN && cbq * TN + k < hq) ? __ldg(hlq + cbq * TN + k) : -1;
         };
         int p, rb, cb, h;
-        int g = g_lo + blockIdx.x;
+        int g = epi_tile(0);
         bool have = locate(g, &p, &rb, &cb, &h);
         int jb0 = -1, jb1 = -1;
         if (have) {
@@ -342,7 +377,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
         for (int lt = 0; have; ++lt) {
             const int acc = lt & 1;
             int pn, rbn, cbn, hn;
-            const bool next = locate(g + gridDim.x, &pn, &rbn, &cbn, &hn);
+            const int gn = epi_tile(lt + 1);
+            const bool next = locate(gn, &pn, &rbn, &cbn, &hn);
             int jbn0 = -1, jbn1 = -1, ja_n = -1, eb_n = -1;
             if (next) {
                 const int32_t* hln = ws.heavy_list + pn * ws.heavy_cap;
@@ -432,7 +468,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 __syncwarp();
                 if (c == sub && ja_n >= 0) eb_n = __ldg(ws.rowptr + pn * ws.rp_stride + ja_n);
             }
-            g += gridDim.x;
+            g = gn;
             p = pn, rb = rbn, cb = cbn, h = hn;
             jb0 = jbn0, jb1 = jbn1;
             s_eb[ew * 32 + lane] = eb_n;  // private to this warp: its reads of tile t are done
