@@ -586,6 +586,7 @@ __device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int
 __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
+    __shared__ uint4 s_list[SEL_WARPS][LIST_MAX / 8];  // a sparse row's list (rows of <= 256 words: list_max 64)
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
     const int n = d.n;
@@ -598,9 +599,9 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
     int mx = 0;
     const int row0 = blockIdx.x * DEG_ROWS_PER_BLOCK, row1 = min(row0 + DEG_ROWS_PER_BLOCK, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
-    auto finish_row = [&](int i, int deg, int ucnt) {  // ucnt: the row's total |U_i|
+    auto finish_row = [&](int i, int deg, int ucnt, bool pad = true) {  // ucnt: the row's total |U_i|
         uint16_t* L = lists + (int64_t)i * ws.list_max;
-        if (deg <= ws.list_max)
+        if (pad && deg <= ws.list_max)
             for (int t = deg + lane; t < ((deg + 7) & ~7); t += 32) L[t] = 0;  // pad to a 16-byte chunk
         if (lane == 0) { ws.deg_full[p * ws.row_stride + i] = deg; ws.deg[p * ws.row_stride + i] = ucnt; }
         mine += deg;
@@ -625,20 +626,21 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
                 int cnt = 0;
 #pragma unroll
                 for (int k = 0; k < WPL; ++k) cnt += __popc(v[k]);
-                const int incl = warp_incl_scan(cnt);
-                const int deg = __shfl_sync(FULL, incl, 31);
-                // |U_i| = deg - #neighbours below i: the lane holding word i>>5 counts them from its prefix
-                const int wi = i >> 5, li = wi / WPL, k0 = wi - li * WPL;
-                int below = incl - cnt;
-                {
-                    const uint32_t mb = (1u << (i & 31)) - 1u;
+                const int deg = (int)__reduce_add_sync(FULL, (unsigned)cnt);
+                // |U_i| = deg - #neighbours below i (no self loop)
+                const int wi = i >> 5;
+                const uint32_t mb = (1u << (i & 31)) - 1u;
+                int bl = 0;
 #pragma unroll
-                    for (int k = 0; k < WPL; ++k) below += (k < k0) ? __popc(v[k]) : (k == k0 ? __popc(v[k] & mb) : 0);
+                for (int k = 0; k < WPL; ++k) {
+                    const int w = w0 + k;
+                    bl += __popc(v[k] & (w < wi ? 0xffffffffu : (w == wi ? mb : 0u)));
                 }
-                const int ucnt = deg - __shfl_sync(FULL, below, li);
-                if (deg <= ws.list_max) {
+                const int ucnt = deg - (int)__reduce_add_sync(FULL, (unsigned)bl);
+                const bool smem_list = ws.list_max == LIST_MAX;  // (a batch with rows above 256 words: 256)
+                if (deg <= ws.list_max && !smem_list) {
                     uint16_t* L = lists + (int64_t)i * ws.list_max;
-                    int pos = incl - cnt;
+                    int pos = warp_incl_scan(cnt) - cnt;
 #pragma unroll
                     for (int k = 0; k < WPL; ++k) {
                         uint32_t x = v[k];
@@ -648,6 +650,26 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
                             L[pos++] = (uint16_t)((w0 + k) * 32 + b);
                         }
                     }
+                }
+                if (deg <= ws.list_max && smem_list) {  // sorted list built in shared memory, written as 16-byte chunks
+                    uint16_t* sl = reinterpret_cast<uint16_t*>(s_list[warp]);
+                    if (lane < LIST_MAX / 8) s_list[warp][lane] = make_uint4(0u, 0u, 0u, 0u);
+                    const int incl = warp_incl_scan(cnt);
+                    int pos = incl - cnt;
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < WPL; ++k) {
+                        uint32_t x = v[k];
+                        while (x) {
+                            const int b = __ffs(x) - 1;
+                            x &= x - 1u;
+                            sl[pos++] = (uint16_t)((w0 + k) * 32 + b);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane < ((deg + 7) >> 3))
+                        reinterpret_cast<uint4*>(lists + (int64_t)i * ws.list_max)[lane] = s_list[warp][lane];
+                    __syncwarp();
                 }
                 if (ws.uprefix) {  // SC^2 mode: rank of any j in U_i = uprefix[i][j>>5] + popc(U_i word below j)
                     int uc[WPL], ul = 0;
@@ -661,7 +683,7 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
                         run += uc[k];
                     }
                 }
-                finish_row(i, deg, ucnt);
+                finish_row(i, deg, ucnt, !smem_list);
             }
         };
         switch ((W + 31) >> 5) {

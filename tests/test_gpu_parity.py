@@ -80,6 +80,27 @@ def test_batch_mixed_sizes_and_statuses(tr_mod):
         assert np.all(res[p]["R"] == 0) and np.all(res[p]["t"] == 0)
 
 
+def test_batch_mixed_row_widths(tr_mod):
+    # a pair above 256 words per row (n = 9000) gives the whole batch 256-entry sparse-row lists; the small
+    # pair in the same batch must still match the oracle, and both must match their single-pair calls
+    cfg = synth.CONFIGS["B"]
+    big = synth.workload_instance(cfg, pair=40, n=9000)
+    small = synth.workload_instance(cfg, pair=41, n=2500)
+    n = np.array([2500, 9000], np.int32)
+    off = np.array([0, 2500], np.int64)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=9000, max_batch=2)
+    res = tr.register_batch(np.concatenate([small["src"], big["src"]]), np.concatenate([small["dst"], big["dst"]]),
+                            off, n)
+    assert [int(r) for r in res["status"]] == [0, 0]
+    r = {k: res[0][k] for k in res.dtype.names}
+    compare_pair(tr, 0, small["src"], small["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=r)
+    one_small = tr.register(small["src"], small["dst"])
+    one_big = tr.register(big["src"], big["dst"])
+    for one, b in ((one_small, res[0]), (one_big, res[1])):
+        assert tuple(one["clique"]) == tuple(b["clique"]) and one["inlier_count"] == b["inlier_count"]
+        assert one["num_edges"] == b["num_edges"] and one["num_cliques"] == b["num_cliques"]
+
+
 def test_device_inputs_match_host_inputs(tr_mod):
     import torch
 
