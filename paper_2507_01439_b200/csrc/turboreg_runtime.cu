@@ -493,7 +493,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
             if (c->prm.tau_base > 0.f) trk::k_compat<true><<<g, 256, 0, s>>>(ws, split);
             else if (c->opt_compat_variant == 1) trk::k_compat<false, 5, 16, 1><<<g, 256, 0, s>>>(ws, split);
             else if (c->opt_compat_variant == 2) trk::k_compat<false, 5, 16, -1><<<g, 256, 0, s>>>(ws, split);
-            else trk::k_compat<false, 5, 16, -2><<<g, 256, 0, s>>>(ws, split);
+            else trk::k_compat<false, 4, 16, -2><<<g, 256, 0, s>>>(ws, split);
         }));
     }
     if (!(phase & PH_TAIL)) return TURBOREG_OK;
