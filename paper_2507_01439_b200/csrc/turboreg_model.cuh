@@ -315,7 +315,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // engine) completing on per-stage mbarriers; the copy of chunk c+1 overlaps the arithmetic on chunk c.
 // Each lane is exactly the oracle's float32 FMA tree (reading r13), so counts are bit-identical.
 template <bool ERR, int NP>
-__global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : 4)) k_score(WS ws, int segs) {
+#ifndef TRK_SCORE_MINB
+#define TRK_SCORE_MINB 4
+#endif
+__global__ void __launch_bounds__(SCORE_THREADS, (NP == 1 ? 8 : TRK_SCORE_MINB)) k_score(WS ws, int segs) {
     // NP packed hypothesis pairs per thread: hypotheses h = base + threadIdx.x + SCORE_THREADS * u, u < 2 NP
     constexpr int NH = 2 * NP;
     __shared__ __align__(16) float4 s_src[2][SCORE_PC];

@@ -170,8 +170,11 @@ __device__ __forceinline__ int pgs_topk_list(const WS& ws, int q, const uint32_t
 
 // KL: per-lane top list length (2, 4, PGS_KL; 0 = K2 threshold rounds), fixed per launch so each
 // instantiation only holds the registers its own branch needs (occupancy: the kernel is latency-bound).
+#ifndef TRK_PGS_MINB
+#define TRK_PGS_MINB 6
+#endif
 template <int MODE, int KL>
-__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? 6 : 4)) k_pgs(WS ws) {
+__global__ void __launch_bounds__(PGS_WARPS * 32, (KL == 2 ? TRK_PGS_MINB : 4)) k_pgs(WS ws) {
     __shared__ uint2 s_q[PGS_WARPS][PGS_QCAP];
     const int q = blockIdx.y;
     const PairDesc d = ws.desc[q];

@@ -129,7 +129,10 @@ __device__ __forceinline__ void sc2_sparse_edge(const WS& ws, const uint16_t* li
 }
 
 template <int WPL>
-__global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 : 4)) k_sc2(WS ws, int cpi) {
+#ifndef TRK_SC2_MINB
+#define TRK_SC2_MINB 4
+#endif
+__global__ void __launch_bounds__(SC2_WARPS * 32, (WPL >= 16 ? 2 : WPL >= 8 ? 3 : TRK_SC2_MINB)) k_sc2(WS ws, int cpi) {
     constexpr int G = 4;
     constexpr int QCAP = sc2_qcap<WPL>();  // sparse-neighbour queue (a round adds at most 32 entries)
     extern __shared__ uint32_t s_dyn[];
@@ -404,8 +407,11 @@ __device__ __forceinline__ void light_flush(const WS& ws, int p, const uint32_t*
 }
 
 // LG (sparse rows per warp group): light_rows<WPL>() for batches; 2 when a small batch would leave SMs idle
+#ifndef TRK_LIGHT_MINB
+#define TRK_LIGHT_MINB 4  // shared memory allows 4 blocks per SM anyway: up to 64 registers
+#endif
 template <int WPL, int LG = light_rows<WPL>()>
-__global__ void __launch_bounds__(256) k_sc2_light(WS ws) {
+__global__ void __launch_bounds__(256, TRK_LIGHT_MINB) k_sc2_light(WS ws) {
     extern __shared__ uint32_t s_dyn[];
     const int p = blockIdx.y;
     const PairDesc d = ws.desc[p];
