@@ -48,7 +48,7 @@ def main():
         for e in engines:
             e.close()
         print(key, "ok" if ok else "MISMATCH", flush=True)
-    if "--full" in sys.argv:  # BASELINE-size pairs of configs C and D, a 4-pair batch, ER graphs
+    if "--full" in sys.argv:  # BASELINE-size pairs of configs C and D, a 4-pair batch, 1100 pairs, ER graphs
         for key in ("C", "D"):
             cfg = synth.CONFIGS[key]
             inst = synth.workload_instance(cfg, pair=2)
@@ -60,6 +60,20 @@ def main():
             ok &= r["status"] == 0 and all(tuple(x["clique"]) == tuple(r["clique"]) for x in res)
             print(key, "ok" if ok else "MISMATCH", flush=True)
             tr.close()
+        # 1100 pairs: beyond the shared-memory tile table (1024 pairs), the dynamically scheduled tensor-core
+        # block walks the global table across all of them
+        cfg = synth.CONFIGS["E"]
+        nb, n = 1100, 2000
+        insts = [synth.workload_instance(cfg, pair=p, n=n) for p in range(nb)]
+        tr = TurboReg(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n, max_batch=nb)
+        res = tr.register_batch(np.concatenate([x["src"] for x in insts]), np.concatenate([x["dst"] for x in insts]),
+                                np.arange(nb, dtype=np.int64) * n, np.full(nb, n, np.int32))
+        ok &= bool((res["status"] == 0).all())
+        for p in (0, 517, 1099):
+            r = tr.register(insts[p]["src"], insts[p]["dst"])
+            ok &= tuple(r["clique"]) == tuple(res[p]["clique"]) and r["inlier_count"] == res[p]["inlier_count"]
+        tr.close()
+        print("E x1100 ok" if ok else "E x1100 MISMATCH", flush=True)
         tr = TurboReg(0.01, 200, 4, 0.1, max_n=300)
         for dens in (0.05, 0.2, 0.5):
             tr.pgs_from_adjacency(synth.erdos_renyi(300, dens, seed=int(dens * 100)))
