@@ -285,8 +285,9 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "heavy_min_rows"   minimum |H| for the dense block to be used (default 128)
  *   "heavy_min_degree" minimum degree of a heavy row (default 32)
  *   "heavy_cap"        maximum |H| (multiple of 256, <= the allocated capacity)
- *   "pipeline_host_inputs" 1 = a call with host inputs and >= 16 pairs copies them in 4 sub-batches, each
- *                      copy overlapping the previous sub-batch's compatibility pass (default); 0 = one copy
+ *   "pipeline_host_inputs" 1 = a call with host inputs and >= 16 pairs copies them in 8 sub-batches of
+ *                      doubling size, each copy overlapping the previous sub-batch's compatibility pass
+ *                      (default); 0 = one copy
  *                      before one launch sequence
  *   "mma_fp4"          1 = run the dense block as kind::mxf4.block_scale on packed e2m1 operands (unit block
  *                      scales, fp32 accumulate; exact below 2^24) with 128x240 tiles (default); 0 = kind::i8
