@@ -231,6 +231,27 @@ def test_no_hypothesis(tr_mod):
     assert res["status"] == 5 and np.all(res["R"] == 0) and res["num_pivots"] == 0
 
 
+@pytest.mark.parametrize("case", ["triplicates", "one_point"])
+def test_duplicate_points(tr_mod, case):
+    # coincident correspondences: tests with S = 0 are never certified by the filter (S <= τ²(1 + 2^-16)), so
+    # every lane meeting one redoes its tests with the exact tree; all-identical points give the complete
+    # graph (|0 − 0| <= τ), all-tied weights and degenerate (non-unique) Kabsch fits
+    cfg = synth.CONFIGS["B"]
+    if case == "triplicates":
+        inst = synth.workload_instance(cfg, pair=9, n=300)
+        src = np.repeat(inst["src"], 3, axis=0)
+        dst = np.repeat(inst["dst"], 3, axis=0)
+        perm = np.random.default_rng(5).permutation(900)
+        src, dst = src[perm], dst[perm]
+    else:
+        src = np.tile(np.array([[0.5, -0.25, 2.0]], np.float32), (150, 1))
+        dst = np.tile(np.array([[-1.0, 0.75, 0.125]], np.float32), (150, 1))
+    n = src.shape[0]
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=n)
+    res = tr.register(src, dst)
+    compare_pair(tr, 0, src, dst, cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
 def test_full_size_batch_sampled_parity(tr_mod):
     # BASELINE sizes in the bench's launch configuration (a batch of config-E pairs), sampled pairs checked
     # against the oracle element by element, every pair checked for planted recovery.
