@@ -104,6 +104,7 @@ struct WS {
                           // (r20); k_finalize adds the segments in order into slot [h][0] (deterministic)
     int32_t x_fp4;        // heavy_X holds packed e2m1 (block-scaled fp4 tensor-core path) instead of uint8
     int32_t mma_l2;       // L2 policy of the X tile loads: 0 evict_normal, 1 evict_last, 2 evict_first
+    int32_t heavy_widen;  // 1: H takes every non-sparse row that fits the cap (else only at no extra block)
     int32_t err_mode;     // bit 0: accumulate herr; rank = err_mode >> 1: 0 inlier number, 1 MAE, 2 MSE
     // NEXT(1), one pair split over split_world ranks (1 = not split): this rank's share of every split work
     // list (compat block-row pairs from compat_b0, tensor-core tiles, dense-row items, sparse-row groups,

@@ -144,6 +144,7 @@ struct turboreg_ctx {
     int32_t opt_score_pairs = 2;
     int32_t opt_sc2_chunks = 0;  // 0 = auto
     int32_t opt_mma_l2 = 1;      // L2 policy of the tensor-core block's X loads (WS::mma_l2)
+    int32_t opt_heavy_widen = 1;  // WS::heavy_widen
 };
 
 namespace {
@@ -349,6 +350,7 @@ void set_ws_params(turboreg_ctx* c) {
     c->ws.sc2_path = (c->opt_sc2_path == 0 && !(c->alloc_fp4 ? c->tmX4_ok : c->tmX_ok)) ? 1 : c->opt_sc2_path;
     c->ws.x_fp4 = (c->ws.sc2_path == 0 && c->alloc_fp4) ? 1 : 0;
     c->ws.mma_l2 = c->opt_mma_l2;
+    c->ws.heavy_widen = c->opt_heavy_widen;
     c->ws.tau = c->prm.tau;
     c->ws.tau_base = c->prm.tau_base;
     c->ws.thr = c->prm.inlier_threshold;
@@ -854,6 +856,10 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
         if (value < 0 || value > 2) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_mma_l2 = (int32_t)value;
         drop_graphs(c);  // captured launches hold the workspace descriptor by value
+    } else if (k == "heavy_widen") {
+        if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        c->opt_heavy_widen = (int32_t)value;
+        drop_graphs(c);
     } else if (k == "sc2_chunks") {
         if (value < 0 || value > 64) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_sc2_chunks = (int32_t)value;

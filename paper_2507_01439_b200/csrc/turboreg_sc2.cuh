@@ -804,14 +804,18 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
         thr = hi;
         cnt = count_ge(thr);
     }
-    // widen H to every non-sparse row (degree > list_max) when that costs no extra 256-row block of the
-    // tensor-core contraction: those rows' dense-dense edges then come from the tensor cores instead of the
-    // latency-bound popcount path
+    // widen H to every non-sparse row (degree > list_max) that fits the cap (heavy_widen = 0: only when that
+    // costs no extra 256-row block of the tensor-core contraction): those rows' dense-dense edges then come
+    // from the tensor cores instead of the latency-bound popcount path (1623 config-E pairs: k_sc2 3.17 ->
+    // 2.68 us/pair for +0.04 on the block; N = 32 768: 3.96 -> 2.69 ms per pair)
     {
         const int thr2 = max(ws.heavy_min_deg, ws.list_max + 1);
         if (thr2 < thr) {
             const int cnt2 = count_ge(thr2);
-            if (cnt2 <= ws.heavy_cap && (cnt2 + 255) / 256 <= (cnt + 255) / 256) { thr = thr2; cnt = cnt2; }
+            if (cnt2 <= ws.heavy_cap && (ws.heavy_widen || (cnt2 + 255) / 256 <= (cnt + 255) / 256)) {
+                thr = thr2;
+                cnt = cnt2;
+            }
         }
     }
     // E = Σ deg / 2 beyond the context's edge capacity: the pair is skipped (no tensor-core block, no
