@@ -295,7 +295,8 @@ turboreg_status turboreg_profile_end(turboreg_ctx* ctx, const char** names, floa
  *   "sc2_chunks"       32-word chunks of a dense row per SC^2 work item: 0 = auto (whole rows for batches
  *                      >= 32 pairs, 4 chunks for rows above 512 words, single chunks otherwise), 1..64 fixed
  *   "heavy_widen"      1 = the dense block takes every non-sparse row (degree > list length) that fits the
- *                      cap (default); 0 = only when that adds no 256-row block of the contraction
+ *                      cap (default); 0 = only when that adds no 256-row block of the contraction; d > 1 =
+ *                      every row of degree >= d that fits the cap (tuning)
  *   "mma_l2_policy"    L2 policy of the dense block's operand (TMA) loads: 1 = evict_last (default),
  *                      0 = evict_normal, 2 = evict_first
  *   "score_pairs"      hypothesis pairs (f32x2 lanes) per scoring thread: 2 (default) or 1

@@ -857,7 +857,7 @@ turboreg_status turboreg_set_option(turboreg_ctx* c, const char* name, int64_t v
         c->opt_mma_l2 = (int32_t)value;
         drop_graphs(c);  // captured launches hold the workspace descriptor by value
     } else if (k == "heavy_widen") {
-        if (value < 0 || value > 1) return TURBOREG_ERR_INVALID_ARGUMENT;
+        if (value < 0 || value > 65535) return TURBOREG_ERR_INVALID_ARGUMENT;
         c->opt_heavy_widen = (int32_t)value;
         drop_graphs(c);
     } else if (k == "sc2_chunks") {

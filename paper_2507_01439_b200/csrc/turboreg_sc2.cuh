@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(1024) k_heavy(WS ws) {
     // from the tensor cores instead of the latency-bound popcount path (1623 config-E pairs: k_sc2 3.17 ->
     // 2.68 us/pair for +0.04 on the block; N = 32 768: 3.96 -> 2.69 ms per pair)
     {
-        const int thr2 = max(ws.heavy_min_deg, ws.list_max + 1);
+        const int thr2 = ws.heavy_widen > 1 ? ws.heavy_widen : max(ws.heavy_min_deg, ws.list_max + 1);
         if (thr2 < thr) {
             const int cnt2 = count_ge(thr2);
             if (cnt2 <= ws.heavy_cap && (ws.heavy_widen || (cnt2 + 255) / 256 <= (cnt + 255) / 256)) {
