@@ -16,7 +16,10 @@ constexpr int SC2_WARPS = 8;
 constexpr int DEG_ROWS_PER_BLOCK = 64;  // k_degree: rows per 8-warp block
 constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 128;
-constexpr int LIST_MAX = 64;       // rows with degree <= list_max keep a sorted uint16 neighbour list: 64, or
+#ifndef TRK_LIST_MAX
+#define TRK_LIST_MAX 64
+#endif
+constexpr int LIST_MAX = TRK_LIST_MAX;  // rows with degree <= list_max keep a sorted uint16 neighbour list: 64, or
 constexpr int LIST_MAX_BIG = 256;  // 256 for rows of more than 256 words (N > 8192, where outliers' degrees grow)
 template <int WPL>
 constexpr int list_max_of() { return WPL >= 16 ? LIST_MAX_BIG : LIST_MAX; }
