@@ -13,7 +13,10 @@ namespace trk {
 // per-lane register lists (K2 <= KL) merged by K2 warp argmax rounds, or K2 threshold rounds otherwise.
 constexpr int PGS_WARPS = 8;
 constexpr int PGS_KL = 8;
-constexpr int PGS_QCAP = 128;  // per-warp candidate queue (entries) of the O2 scan
+#ifndef TRK_PGS_QCAP
+#define TRK_PGS_QCAP 128
+#endif
+constexpr int PGS_QCAP = TRK_PGS_QCAP;  // per-warp candidate queue (entries) of the O2 scan
 
 // Candidate keys (reading r8: S desc, z asc) in 32 bits: S = Ĝ_ij + Ĝ_iz + Ĝ_jz < 3·2^15 takes 17 bits and
 // z < 2^15 (n <= 32768) the low 15, stored as 32767 − z; every candidate key is > 0 (S >= Ĝ_ij >= 1).

@@ -501,8 +501,9 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     if (!(phase & PH_TAIL)) return TURBOREG_OK;
     ws.list_max = list_cap(Wb);
     if (phase & PH_GRAPH) {
-    const dim3 grow((maxn_batch + trk::DEG_ROWS_PER_BLOCK - 1) / trk::DEG_ROWS_PER_BLOCK, B);
-    CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws); }));
+    const int deg_rows = batch >= 256 ? trk::DEG_ROWS_PER_BLOCK_BIG : trk::DEG_ROWS_PER_BLOCK;
+    const dim3 grow((maxn_batch + deg_rows - 1) / deg_rows, B);
+    CK(L.run(KID_DEGREE, [&] { trk::k_degree<<<grow, 256, 0, s>>>(ws, deg_rows); }));
     CK(L.run(KID_HEAVY, [&] { trk::k_heavy<<<B, 1024, 0, s>>>(ws); }));
     CK(L.run(KID_ROWCLASS, [&] { trk::k_rowclass<<<B, 1024, 0, s>>>(ws); }));
 #ifdef TRK_CHECKS
@@ -539,7 +540,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     const int wpl = (Wb + 31) / 32;
     {
-        const int sc2_bpp = std::max(trk::SC2_BLOCKS_PER_PAIR,
+        const int sc2_bpp = std::max(batch >= 256 ? trk::SC2_BLOCKS_PER_PAIR_BIG : trk::SC2_BLOCKS_PER_PAIR,
                                      std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
         const dim3 gp((unsigned)sc2_bpp, B);
         // chunks per item: whole rows for batches; 4 chunks (128 words) for large N, where one pair has

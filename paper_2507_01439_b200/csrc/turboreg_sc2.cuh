@@ -13,7 +13,9 @@ namespace trk {
 //   * both sparse → k_sc2_light.
 // The pivot passes (turboreg_select.cuh) then histogram the positive weights for the radix select (Eq. 4).
 constexpr int SC2_WARPS = 8;
-constexpr int DEG_ROWS_PER_BLOCK = 64;  // k_degree: rows per 8-warp block
+// k_degree: rows per 8-warp block — 64 for small batches (enough blocks to fill the GPU), 256 for batches
+// of >= 256 pairs (fewer, longer blocks: 1623 config-E pairs 1.34 -> 1.28 us/pair)
+constexpr int DEG_ROWS_PER_BLOCK = 64, DEG_ROWS_PER_BLOCK_BIG = 256;  // k_degree: rows per 8-warp block
 constexpr int SEL_WARPS = 8;
 constexpr int SEL_ROWS_PER_BLOCK = 128;
 #ifndef TRK_LIST_MAX
@@ -41,7 +43,10 @@ constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 *
 //   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
 // Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
 constexpr int SC2_PERSIST_BLOCKS_PER_SM = 6;
-constexpr int SC2_BLOCKS_PER_PAIR = 64;  // 512 warps stride over a pair's dense rows
+// at least 64 blocks per pair (512 warps over its dense rows), 16 for batches of >= 256 pairs, where the
+// grid is large anyway and fewer blocks amortise each block's staging of the row-class masks (1623 pairs:
+// k_sc2 2.68 -> 2.49 us/pair)
+constexpr int SC2_BLOCKS_PER_PAIR = 64, SC2_BLOCKS_PER_PAIR_BIG = 16;  // 512 warps stride over a pair's dense rows
 constexpr int SC2_CLAIM = 4;
 
 // |L ∩ N(i)| for a sorted list L of <= LM uint16 entries (16-byte aligned, zero padded) against row i's
@@ -385,7 +390,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 template <int WPL>
-constexpr int light_rows() { return WPL >= 16 ? 2 : 8; }  // LG: sparse rows per warp group
+#ifndef TRK_LIGHT_LG
+#define TRK_LIGHT_LG 8
+#endif
+constexpr int light_rows() { return WPL >= 16 ? 2 : TRK_LIGHT_LG; }  // LG: sparse rows per warp group
 template <int WPL, int LG = light_rows<WPL>()>
 constexpr int light_warp_words() {
     return LG * 32 * WPL + LG * (list_max_of<WPL>() / 2) + 64 + 64 + 4 * LG;
@@ -514,7 +522,7 @@ __global__ void __launch_bounds__(256, TRK_LIGHT_MINB) k_sc2_light(WS ws) {
 
 // The pivot passes stream the pair's compact O2 edge array (E words) with a grid stride: coalesced,
 // no per-row bookkeeping.
-constexpr int SEL_BLOCKS_PER_PAIR = 16;
+constexpr int SEL_BLOCKS_PER_PAIR = 8;  // (or more for small batches, to fill the GPU)
 
 // Histogram of Ĝ >> 7 over positive O2 weights (the high digit of the pivot radix select, Eq. 4).
 // The three edge passes below stream the pair's compact O2 edge array (edges_stride is a multiple of 4
@@ -592,7 +600,7 @@ __device__ __forceinline__ void deg_extract8(const uint32_t (&v)[8], int w0, int
         }
     }
 }
-__global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
+__global__ void __launch_bounds__(256, 6) k_degree(WS ws, int rows_per_block) {
     __shared__ unsigned long long s_sum;
     __shared__ int s_max;
     __shared__ uint4 s_list[SEL_WARPS][LIST_MAX / 8];  // a sparse row's list (rows of <= 256 words: list_max 64)
@@ -606,7 +614,7 @@ __global__ void __launch_bounds__(256, 6) k_degree(WS ws) {
     const uint32_t* bits = ws.bits + p * ws.bits_stride;
     unsigned mine = 0;
     int mx = 0;
-    const int row0 = blockIdx.x * DEG_ROWS_PER_BLOCK, row1 = min(row0 + DEG_ROWS_PER_BLOCK, n);
+    const int row0 = blockIdx.x * rows_per_block, row1 = min(row0 + rows_per_block, n);
     uint16_t* lists = ws.lists + p * ws.lists_stride;
     auto finish_row = [&](int i, int deg, int ucnt, bool pad = true) {  // ucnt: the row's total |U_i|
         uint16_t* L = lists + (int64_t)i * ws.list_max;
