@@ -526,6 +526,7 @@ def run_cuda(args, rank, world, local_rank):
 
     context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 and not args.no_context else None
     split_ctx = split_pair_context(world, local_rank) if world > 1 and not args.no_context else None
+    split_proj = split_phase_projection(local_rank) if world == 1 and not args.no_context else None
     if rank != 0:
         return
     pk = peaks()
@@ -561,6 +562,11 @@ def run_cuda(args, rank, world, local_rank):
     line.update(context or {})
     if split_ctx:
         line["split_pair_latency_ms"] = split_ctx
+    if split_proj:
+        line["split_phase_projection_1gpu"] = {
+            "what": "NEXT(1), N = 32768: G logical ranks' phases run one after another on this GPU (projection, "
+                    "not a multi-GPU measurement); per phase (compat / SC2 assembly / search) the slowest rank",
+            **split_proj}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample()
     print(json.dumps(line), flush=True)
@@ -692,6 +698,70 @@ def split_pair_context(world, local_rank, n=32768, reps=3):
     return {"N": n, "ranks": world, "ms": round(1e3 * float(np.median(ts)), 3), "status": int(res["status"]),
             "inlier_count": int(res["inlier_count"]),
             "recovered": bool(synth.rotation_error_deg(np.asarray(res["R"]).reshape(3, 3), inst["R"]) <= 5)}
+
+
+def split_phase_projection(local_rank, n=32768, groups=(1, 2, 4), reps=2):
+    """NEXT(1) on ONE GPU — a projection, not a multi-GPU measurement: the phases of G logical ranks for one
+    N-point pair run one after another on this GPU (the exchanges as device sums, untimed), each rank's
+    phase timed with CUDA events on the launching stream; per phase the slowest rank, and their sum, which a
+    G-GPU split would take before its exchanges (bytes per rank given; NVLink time not included)."""
+    import torch
+
+    from paper_2507_01439_b200 import TurboReg
+    from paper_2507_01439_b200._binding import SPLIT_BITS, SPLIT_EDGES, SPLIT_RESULT
+
+    c = synth.CONFIGS["B"]
+    inst = synth.workload_instance(c, pair=0, n=n)
+    dev = torch.device("cuda", local_rank)
+    s = torch.cuda.Stream(device=dev)
+    src, dst = torch.from_numpy(inst["src"]).to(dev), torch.from_numpy(inst["dst"]).to(dev)
+    out = {}
+    for g in groups:
+        engines = [TurboReg(c.tau, c.k1, c.k2, c.inlier_threshold, max_n=n, max_batch=1, device=local_rank,
+                            max_density=0.1) for _ in range(g)]
+        best = None
+        for rep in range(reps + 1):
+            ph = [[0.0] * g for _ in range(3)]
+
+            def timed(k, r, fn):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                v = fn()
+                b.record(s)
+                b.synchronize()
+                ph[k][r] = a.elapsed_time(b)
+                return v
+
+            with torch.cuda.stream(s):
+                for r, e in enumerate(engines):
+                    timed(0, r, lambda: e.split_begin(src, dst, r, g, stream=s))
+                if g > 1:  # each word was written by exactly one rank into zeros: the sum is the all-reduce
+                    bits = [e.split_tensor(SPLIT_BITS) for e in engines]
+                    tot = sum(b.to(torch.int64) for b in bits).to(torch.int32)
+                    for b in bits:
+                        b.copy_(tot)
+                es = [timed(1, r, lambda: e.split_sc2(stream=s)) for r, e in enumerate(engines)]
+                if g > 1 and es[0] > 0:
+                    ed = [e.split_tensor(SPLIT_EDGES, es[0]) for e in engines]
+                    tot = sum(x.to(torch.int64) for x in ed).to(torch.int32)
+                    for x in ed:
+                        x.copy_(tot)
+                for r, e in enumerate(engines):
+                    timed(2, r, lambda: e.split_search(stream=s))
+                parts = torch.cat([e.split_tensor(SPLIT_RESULT) for e in engines])
+                res = engines[0].split_merge(parts, g, stream=s)
+            torch.cuda.synchronize()
+            if rep:
+                cur = [max(x) for x in ph]
+                best = cur if best is None or sum(cur) < sum(best) else best
+        E = int(res["num_edges"])
+        out[f"G={g}"] = {"phase_ms_max_over_ranks": [round(x, 3) for x in best], "sum_ms": round(sum(best), 3),
+                         "exchange_MB_per_rank": round((2 * (g - 1) / g) * (n * ((n + 31) // 32) * 4 + 4 * E) / 1e6, 1),
+                         "status": int(res["status"]),
+                         "recovered": bool(synth.rotation_error_deg(np.asarray(res["R"]).reshape(3, 3), inst["R"]) <= 5)}
+        for e in engines:
+            e.close()
+    return out
 
 
 def ncu_traffic(kernel):
