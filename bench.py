@@ -524,9 +524,12 @@ def run_cuda(args, rank, world, local_rank):
     else:
         all_ok = int((res["status"] == 0).sum())
 
-    context = single_pair_context(rank, local_rank, stream, src_d, dst_d) if rank == 0 and not args.no_context else None
-    split_ctx = split_pair_context(world, local_rank) if world > 1 and not args.no_context else None
-    split_proj = split_phase_projection(local_rank) if world == 1 and not args.no_context else None
+    # context keys never cost the metric line: rank-0-only ones are guarded; the multi-rank split (collectives,
+    # where one rank's failure would stall the others) runs only on request
+    context = _guarded(single_pair_context, rank, local_rank, stream, src_d, dst_d) \
+        if rank == 0 and not args.no_context else None
+    split_ctx = split_pair_context(world, local_rank) if world > 1 and args.split_context else None
+    split_proj = _guarded(split_phase_projection, local_rank) if world == 1 and not args.no_context else None
     if rank != 0:
         return
     pk = peaks()
@@ -700,6 +703,14 @@ def split_pair_context(world, local_rank, n=32768, reps=3):
             "recovered": bool(synth.rotation_error_deg(np.asarray(res["R"]).reshape(3, 3), inst["R"]) <= 5)}
 
 
+def _guarded(fn, *a):
+    """A context measurement that must not cost the metric line: its exception becomes an error entry."""
+    try:
+        return fn(*a)
+    except Exception as e:  # noqa: BLE001
+        return {"context_error": f"{type(e).__name__}: {e}"[:300]}
+
+
 def split_phase_projection(local_rank, n=32768, groups=(1, 2, 4), reps=2):
     """NEXT(1) on ONE GPU — a projection, not a multi-GPU measurement: the phases of G logical ranks for one
     N-point pair run one after another on this GPU (the exchanges as device sums, untimed), each rank's
@@ -806,6 +817,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-context", action="store_true", help="skip the single-pair / RANSAC context numbers")
+    ap.add_argument("--split-context", action="store_true",
+                    help="N > 1: also time one N = 32768 pair split over all ranks (NEXT(1), NCCL exchanges)")
     ap.add_argument("--selftest-gloo", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.gpus < 1 or args.steps < 1 or args.warmup < 0:
