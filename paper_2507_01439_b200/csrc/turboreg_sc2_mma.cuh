@@ -406,6 +406,21 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
             for (int c = sub; c < NCH; c += MMA_EPI_SUB) {
+                const int b = bt + c * 32 + lane;
+                const int jb = (c == sub) ? jb0 : jb1;
+                const int a0 = rb * MMA_BM + q * 32;
+                // rows r < lim of this warp are heavy rows (a0 + r < h) below the lane's column (b > a0 + r)
+                const int lim = jb >= 0 ? min(b - a0, h - a0) : 0;
+                if (__all_sync(FULL, lim <= 0)) {  // the chunk holds no upper pair (below the diagonal / beyond H)
+                    if (c == last_c) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
+                    }
+                    if (c == sub && ja_n >= 0) eb_n = __ldg(ws.rowptr + pn * ws.rp_stride + ja_n);
+                    continue;
+                }
                 uint32_t v[32];
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * MMA_BN + c * 32);
                 asm volatile(
@@ -425,13 +440,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) k_sc2_mma(const __grid_constan
                 }
                 // transpose through shared memory: afterwards lane = column, loop over the warp's 32 rows, so
                 // the UP reads and edge stores of one row are coalesced
-                const int b = bt + c * 32 + lane;
-                const int jb = (c == sub) ? jb0 : jb1;
                 const uint32_t bit = 1u << (jb & 31);
                 const uint32_t jhi = (uint32_t)jb << 16, bm1 = bit - 1u;
-                const int a0 = rb * MMA_BM + q * 32;
-                // rows r < lim of this warp are heavy rows (a0 + r < h) below the lane's column (b > a0 + r)
-                const int lim = jb >= 0 ? min(b - a0, h - a0) : 0;
                 const char* upl = reinterpret_cast<const char*>(up0 + (size_t)a0 * W + (jb >= 0 ? (jb >> 5) : 0));
                 const size_t W8 = (size_t)W * sizeof(uint2);
 #pragma unroll
