@@ -540,7 +540,7 @@ turboreg_status launch_all(turboreg_ctx* c, int32_t batch, int32_t maxn_batch, c
     }
     const int wpl = (Wb + 31) / 32;
     {
-        const int sc2_bpp = std::max(batch >= 256 ? trk::SC2_BLOCKS_PER_PAIR_BIG : trk::SC2_BLOCKS_PER_PAIR,
+        const int sc2_bpp = std::max(batch >= 128 ? trk::SC2_BLOCKS_PER_PAIR_BIG : trk::SC2_BLOCKS_PER_PAIR,
                                      std::min((3 * c->num_sms + batch - 1) / batch, (maxn_batch + 7) / 8));
         const dim3 gp((unsigned)sc2_bpp, B);
         // chunks per item: whole rows for batches; 4 chunks (128 words) for large N, where one pair has

@@ -42,7 +42,7 @@ constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 *
 //       (entries of L_j below i, minus those up to j) falls out of the same pass over L_j;
 //   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
 // Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
-// at least 64 blocks per pair (512 warps over its dense rows), 16 for batches of >= 256 pairs, where the
+// at least 64 blocks per pair (512 warps over its dense rows), 16 for batches of >= 128 pairs, where the
 // grid is large anyway and fewer blocks amortise each block's staging of the row-class masks (1623 pairs:
 // k_sc2 2.68 -> 2.49 us/pair)
 constexpr int SC2_BLOCKS_PER_PAIR = 64, SC2_BLOCKS_PER_PAIR_BIG = 16;  // 512 warps stride over a pair's dense rows
