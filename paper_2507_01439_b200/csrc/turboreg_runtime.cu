@@ -963,7 +963,10 @@ turboreg_status turboreg_register_batch(turboreg_ctx* c, const float* src, const
     // (at most twice the previous sub-batch, ≈ 4.4 µs per N = 5000 pair over PCIe) hides behind the
     // previous sub-batch's compat (≈ 10 µs per pair).  Device inputs and small batches run as one launch
     // sequence.
-    const int nchunk = (!dev_in && batch >= 16 && c->use_chunks) ? NCHUNK : 1;
+    // as many doubling sub-batches as keep the first one at >= 4 pairs (launch overhead of tiny sub-batches)
+    int nchunk = 1;
+    if (!dev_in && batch >= 16 && c->use_chunks)
+        while (nchunk < NCHUNK && (int64_t)batch >= 4 * ((int64_t)(1 << (nchunk + 1)) - 1)) ++nchunk;
     int32_t bnd[NCHUNK + 1];
     for (int k = 0; k <= nchunk; ++k)
         bnd[k] = nchunk == 1 ? (k ? batch : 0) : (int32_t)((int64_t)batch * ((1 << k) - 1) / ((1 << nchunk) - 1));
