@@ -40,12 +40,13 @@ constexpr int sc2_smem_bytes() { return (SC2_WARPS * sc2_warp_words<WPL>() + 2 *
 //       Ĝ_ij = |L_j ∩ N(i)|, one edge per lane, list entries tested against row i's bitmap in shared
 //       memory.  For j > i the result goes to row i's slot; for j < i to row j's slot, whose rank
 //       (entries of L_j below i, minus those up to j) falls out of the same pass over L_j;
-//   (3) both dense but not both heavy (rare): warp-cooperative popcount(row_i AND row_j).
+//   (3) both dense but not both heavy (rare since H takes every non-sparse row that fits its cap):
+//       warp-cooperative popcount(row_i AND row_j).
 // Sparse-sparse edges are k_sc2_light's.  Every O2 edge is therefore written exactly once.
-// at least 64 blocks per pair (512 warps over its dense rows), 16 for batches of >= 128 pairs, where the
+// Blocks per pair: at least 64 (512 warps over its dense rows), 16 for batches of >= 128 pairs, where the
 // grid is large anyway and fewer blocks amortise each block's staging of the row-class masks (1623 pairs:
 // k_sc2 2.68 -> 2.49 us/pair)
-constexpr int SC2_BLOCKS_PER_PAIR = 64, SC2_BLOCKS_PER_PAIR_BIG = 16;  // 512 warps stride over a pair's dense rows
+constexpr int SC2_BLOCKS_PER_PAIR = 64, SC2_BLOCKS_PER_PAIR_BIG = 16;
 
 // |L ∩ N(i)| for a sorted list L of <= LM uint16 entries (16-byte aligned, zero padded) against row i's
 // bitmap in shared memory.  Entries past len are zeros, so a chunk is processed whole and the pad's bit 0
