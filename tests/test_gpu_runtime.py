@@ -217,6 +217,29 @@ def test_independent_contexts_concurrently(TR):
             assert tuple(r["clique"]) == tuple(refs[k]["clique"]) and r["inlier_count"] == refs[k]["inlier_count"]
 
 
+def test_create_destroy_releases_device_memory(TR):
+    """Every context owns one workspace allocation plus its streams, events, graphs and pinned slots; destroying
+    it returns them: 40 create / register (graph captured) / set_option re-layout / destroy cycles leave the
+    device's free memory where it was (within 64 MiB of allocator slack)."""
+    import torch
+
+    cfg = synth.CONFIGS["B"]
+    inst = synth.workload_instance(cfg, pair=3, n=1200)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for k in range(40):
+        tr = TR(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=1200, max_batch=4)
+        for _ in range(2):  # the second call replays the captured graph
+            assert tr.register(inst["src"], inst["dst"])["status"] == 0
+        if k % 4 == 0:
+            tr.set_option("mma_fp4", 0)  # workspace re-layout (allocate new, free old)
+            assert tr.register(inst["src"], inst["dst"])["status"] == 0
+        tr.close()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
+
+
 def test_binding_rejects_bad_extents(TR):
     cfg = synth.CONFIGS["A"]
     inst = synth.workload_instance(cfg, pair=1)
