@@ -469,6 +469,20 @@ def test_wide_rows_general_paths(tr_mod):
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
 
 
+@pytest.mark.parametrize("widen", [0, 1, 40, 200])
+@pytest.mark.parametrize("key", ["B", "D"])
+def test_heavy_set_rules_agree_with_oracle(tr_mod, widen, key):
+    # which rows the tensor-core block takes (heavy_widen: only at no extra block, every non-sparse row, or an
+    # explicit degree threshold, possibly below the sparse-row list length) only moves edges between the
+    # assembly paths: results are the oracle's whatever the rule
+    cfg = synth.CONFIGS[key]
+    inst = synth.workload_instance(cfg, pair=23, n=2400)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2400)
+    tr.set_option("heavy_widen", widen)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
 @pytest.mark.parametrize("cap", [256, 512])
 def test_heavy_cap_raises_threshold(tr_mod, cap):
     # more high-degree rows than the dense block holds: the degree threshold is raised until |H| <= cap
