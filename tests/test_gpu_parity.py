@@ -483,6 +483,17 @@ def test_heavy_set_rules_agree_with_oracle(tr_mod, widen, key):
     compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
 
 
+@pytest.mark.parametrize("policy", [0, 2])
+def test_tensor_core_l2_policies_agree_with_oracle(tr_mod, policy):
+    # the L2 policy of the operand loads is a cache hint: same results
+    cfg = synth.CONFIGS["B"]
+    inst = synth.workload_instance(cfg, pair=24, n=2300)
+    tr = tr_mod(cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, max_n=2300)
+    tr.set_option("mma_l2_policy", policy)
+    res = tr.register(inst["src"], inst["dst"])
+    compare_pair(tr, 0, inst["src"], inst["dst"], cfg.tau, cfg.k1, cfg.k2, cfg.inlier_threshold, result=res)
+
+
 @pytest.mark.parametrize("cap", [256, 512])
 def test_heavy_cap_raises_threshold(tr_mod, cap):
     # more high-degree rows than the dense block holds: the degree threshold is raised until |H| <= cap
